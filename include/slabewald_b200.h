@@ -1,0 +1,149 @@
+/*
+ * slabewald_b200.h -- C ABI of the B200-native RBSE2D / SOEwald2D energy-force path.
+ *
+ * The reference (arXiv 2403.01521 artifact, package `slabewald`) has no FFI; its
+ * operator boundary is the Python function layer above its numba kernels
+ * (SURVEY.md 8(b)).  Each entry point below replaces one of those kernels or
+ * the evaluation that strings them together, with plain pointers and sizes:
+ *
+ *   slab_sort_by_z          <- core.py:166-208  _bucket_sort_perm / sort_by_z
+ *   slab_fourier_sweep      <- soewald2d.py:85-208  _fourier_soe_sweep
+ *                              (+ _decay_table soewald2d.py:76-82, fused on device)
+ *   slab_zero_mode_sweep    <- soewald2d.py:211-296 _zero_mode_soe_sweep
+ *   slab_short_range        <- ewald2d.py:280-303  short_range_energy_forces
+ *                              (build_cell_list 141-157, _pair_kernel_cells 160-231,
+ *                               _pair_kernel_brute 234-277)
+ *   slab_sample_modes       <- rbse2d.py:105-207  _chain_kernel / ModeSampler.batch
+ *   slab_evaluate           <- rbse2d.py:274-317 rb_energy_forces and
+ *                              soewald2d.py:398-438 soe_energy_forces
+ *
+ * Conventions
+ *   - Every array pointer is DEVICE memory unless the name starts with h_.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Positions are (n,3) float64 row-major AoS exactly like ParticleSystem.pos;
+ *     per-particle scalars are float64 (n,).  Modes are (P,3) float64 rows
+ *     (kx, ky, |k|) as EwaldParams.kmodes / ModeSampler.batch.
+ *   - SOE coefficients are passed as host arrays of the M complex terms (re/im
+ *     split); M must be even and conjugate-paired (term M-1-l == conj(term l)),
+ *     which every contour from build_soe_contour satisfies (soe.py:77-84).
+ *   - Outputs are written (not accumulated) unless stated.
+ *   - Calls are stream-ordered and asynchronous; status that depends on device
+ *     data (coincident particles) is reported through device status words the
+ *     caller reads after synchronising.
+ *   - Return value: SLAB_OK or an error code; slab_last_error() gives text.
+ */
+#ifndef SLABEWALD_B200_H
+#define SLABEWALD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SLAB_OK = 0,
+  SLAB_ERR_ARG = 1,          /* bad argument (sizes, M odd / unpaired, ...) */
+  SLAB_ERR_CUDA = 2,         /* CUDA runtime error */
+  SLAB_ERR_UNSUPPORTED = 3,  /* e.g. unpaired SOE table */
+  SLAB_ERR_NOMEM = 4
+};
+
+/* device status word bits (written by kernels, read by the host after sync) */
+enum {
+  SLAB_STATUS_COINCIDENT = 1, /* d2 < 1e-24 pair: ewald2d.py:207-209,301-302 */
+  SLAB_STATUS_SINGULAR = 2    /* |b_l - k| < 2e-6 k: soewald2d.py:118-121 (analytic branch) */
+};
+
+typedef struct SlabBox {
+  double lx, ly, lz, sigma_top, sigma_bot; /* core.py:25-51 BoxGeometry */
+} SlabBox;
+
+typedef struct SlabSOE {
+  int m;                 /* number of complex terms (even) */
+  const double* h_w_re;  /* host, length m */
+  const double* h_w_im;
+  const double* h_s_re;
+  const double* h_s_im;
+} SlabSOE;
+
+/* One full energy + force evaluation.  rb_energy_forces when commonv_scalar is
+ * used ((H/P)(2 alpha/sqrt(pi)), rbse2d.py:301); soe_energy_forces when
+ * d_commonv carries (2 alpha/sqrt(pi)) exp(-k^2/4alpha^2) per mode
+ * (soewald2d.py:421-422). */
+typedef struct SlabEvalArgs {
+  int64_t n;
+  const double* d_pos;      /* (n,3) input order */
+  const double* d_charge;   /* (n,) */
+  SlabBox box;
+  double alpha;
+  double r_c;
+  SlabSOE soe;
+  const double* d_modes;    /* (P,3) kx,ky,|k| */
+  int64_t nmode;
+  const double* d_commonv;  /* (P,) or NULL -> commonv_scalar for every mode */
+  double commonv_scalar;
+  double charge_const;      /* C_Q (rbse2d.py:77-89) or u_q (soewald2d.py:408-413) */
+  int want_forces;          /* 0: energies only (forces untouched) */
+  int skip_short_range;     /* 1: u_s = 0, no short-range forces (sub-path calls) */
+  double* d_forces;         /* (n,3) out, input order */
+  double* d_energy;         /* (8,) out: u_s,u_l_k,u_l_0,u_self,u_ps,status,0,0 */
+  int64_t* d_perm;          /* optional (n,) out: the z-sort permutation, or NULL */
+} SlabEvalArgs;
+
+typedef struct SlabCtx SlabCtx;
+
+int slab_ctx_create(SlabCtx** out);
+int slab_ctx_destroy(SlabCtx* ctx);
+const char* slab_last_error(void);
+const char* slab_version(void);
+
+/* core.py:203-208: stable ascending-z permutation; z read as d_z[i*stride]. */
+int slab_sort_by_z(SlabCtx* ctx, const double* d_z, int64_t stride, int64_t n, int64_t* d_perm,
+                   void* stream);
+
+/* soewald2d.py:85-208 on ALREADY z-sorted SoA (x,y,z,q).  Writes the Kahan-
+ * combined mode energy to d_energy[0] (without any charge constant) and, when
+ * want_forces, ADDS the Fourier forces into d_forces_sorted (n,3) like the
+ * reference (which accumulates).  b_l = alpha * s_l. */
+int slab_fourier_sweep(SlabCtx* ctx, const double* d_x, const double* d_y, const double* d_z,
+                       const double* d_q, int64_t n, const double* d_modes,
+                       const double* d_commonv, double commonv_scalar, int64_t nmode,
+                       SlabSOE soe, double alpha, double area, int want_forces,
+                       double* d_forces_sorted, double* d_energy, int* d_status, void* stream);
+
+/* soewald2d.py:211-296 on sorted z,q: d_energy[0] = u_pair; when want_forces,
+ * ADDS fz (the bracket, before the 2 pi/A q factor) into d_fz. */
+int slab_zero_mode_sweep(SlabCtx* ctx, const double* d_z, const double* d_q, int64_t n,
+                         SlabSOE soe, double alpha, int want_forces, double* d_fz,
+                         double* d_energy, void* stream);
+
+/* ewald2d.py:280-303 (no r_c > L/2 check here; the host layer raises).  Writes
+ * d_energy[0] = u_s, d_forces (n,3) input order, ORs status bits. */
+int slab_short_range(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                     SlabBox box, double alpha, double r_c, double* d_forces, double* d_energy,
+                     int* d_status, void* stream);
+
+/* rbse2d.py:151-207 Metropolis independence chain over integer (mx,my) != 0 with
+ * a counter-based Philox4x32-10 stream.  d_state = {mx, my, since, counter,
+ * accepted, steps} (int64) persists across calls.  Writes P rows (kx,ky,|k|) to
+ * d_modes and the integer indices to d_idx (P,2) if not NULL.  burn_in > 0
+ * initialises the chain first (ModeSampler.__init__). */
+int slab_sample_modes(SlabCtx* ctx, int64_t* d_state, uint64_t seed, double alpha, double lx,
+                      double ly, int thin, int burn_in, int64_t P, double* d_modes,
+                      int64_t* d_idx, void* stream);
+
+/* Full evaluation (sort, gather, short range, Fourier sweep, zero mode, self,
+ * slab, assembly, scatter to input order). */
+int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* args, void* stream);
+
+/* Recursion of soewald2d.py:42-64 recursive_pair_sum on sorted z:
+ * out[a] = sum_{j<a} q_j exp(-i theta_j - beta (z_a - z_j)), complex interleaved. */
+int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,
+                            const double* d_z, int64_t n, double beta_re, double beta_im,
+                            double* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLABEWALD_B200_H */

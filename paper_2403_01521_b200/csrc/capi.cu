@@ -1,0 +1,385 @@
+// capi.cu -- extern "C" boundary (include/slabewald_b200.h): context, workspace
+// arena, argument checks, and the evaluation pipeline that strings the kernels
+// together in the order of rbse2d.py:283-317 / soewald2d.py:401-438.
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/slabewald_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using cd = std::complex<double>;
+
+static thread_local std::string g_err;
+
+int slab_record_cuda(cudaError_t e) {
+  g_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+  return SLAB_ERR_CUDA;
+}
+static int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+#define CK(expr)                                   \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) return slab_record_cuda(_e); \
+  } while (0)
+
+struct SlabCtx {
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  double* small = nullptr;  // scalars: [0]=u_s [1]=u_sweep [2]=u_pair ...
+  int* status = nullptr;
+  double* sampler_scratch = nullptr;
+  int64_t sampler_cap = 0;
+};
+
+namespace {
+
+struct Carver {
+  char* p;
+  template <typename T>
+  T* take(size_t count) {
+    uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 255) & ~(uintptr_t)255;
+    T* r = reinterpret_cast<T*>(a);
+    p = reinterpret_cast<char*>(a + sizeof(T) * (count ? count : 1));
+    return r;
+  }
+};
+
+size_t pad(size_t b) { return ((b ? b : 1) + 255) & ~(size_t)255; }
+
+int ensure_arena(SlabCtx* c, size_t bytes) {
+  if (c->small == nullptr) {
+    CK(cudaMalloc(&c->small, 64 * sizeof(double)));
+    CK(cudaMalloc(&c->status, 16 * sizeof(int)));
+  }
+  if (bytes <= c->arena_bytes) return SLAB_OK;
+  if (c->arena) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaFree(c->arena));
+    c->arena = nullptr;
+    c->arena_bytes = 0;
+  }
+  size_t want = bytes + bytes / 8;
+  if (cudaMalloc(&c->arena, want) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SLAB_ERR_NOMEM, "device workspace allocation failed");
+  }
+  c->arena_bytes = want;
+  return SLAB_OK;
+}
+
+struct SOEHost {
+  int m = 0, mh = 0;
+  slab::BVec b{};
+  slab::WVec w{};
+  slab::ZCoef z{};
+};
+
+int prepare_soe(const SlabSOE& soe, double alpha, SOEHost& out) {
+  if (soe.m < 2 || soe.m % 2 || soe.m > 24)
+    return fail(SLAB_ERR_ARG, "SOE term count must be even and in [2, 24]");
+  if (!soe.h_w_re || !soe.h_w_im || !soe.h_s_re || !soe.h_s_im)
+    return fail(SLAB_ERR_ARG, "SOE arrays must be given");
+  const int m = soe.m, mh = m / 2;
+  for (int l = 0; l < mh; ++l) {
+    const int r = m - 1 - l;
+    if (soe.h_s_re[r] != soe.h_s_re[l] || soe.h_s_im[r] != -soe.h_s_im[l] ||
+        soe.h_w_re[r] != soe.h_w_re[l] || soe.h_w_im[r] != -soe.h_w_im[l])
+      return fail(SLAB_ERR_UNSUPPORTED,
+                  "SOE table is not conjugate-paired (term M-1-l must equal conj(term l))");
+  }
+  for (int l = 0; l < m; ++l)
+    if (!(soe.h_s_re[l] > 0)) return fail(SLAB_ERR_ARG, "every exponent must have positive real part");
+  out.m = m;
+  out.mh = mh;
+  for (int l = 0; l < mh; ++l) {
+    const cd s(soe.h_s_re[l], soe.h_s_im[l]), w(soe.h_w_re[l], soe.h_w_im[l]);
+    out.b.re[l] = alpha * s.real();
+    out.b.im[l] = alpha * s.imag();
+    out.w.re[l] = w.real();
+    out.w.im[l] = w.imag();
+    const cd ws = w / s;
+    const cd ws2 = 2.0 * ws, w2 = 2.0 * w, f2 = 2.0 * (ws + 0.5 * w * s), aw2 = 2.0 * alpha * w;
+    out.z.ws2[2 * l] = ws2.real();
+    out.z.ws2[2 * l + 1] = ws2.imag();
+    out.z.w2[2 * l] = w2.real();
+    out.z.w2[2 * l + 1] = w2.imag();
+    out.z.f2[2 * l] = f2.real();
+    out.z.f2[2 * l + 1] = f2.imag();
+    out.z.aw2[2 * l] = aw2.real();
+    out.z.aw2[2 * l + 1] = aw2.imag();
+  }
+  return SLAB_OK;
+}
+
+// workspace for the z-sorted part of an evaluation
+struct SortedWork {
+  slab::SortWork sw;
+  double *xs, *ys, *zs, *qs;
+  double2* dtab;
+  double* fwork;
+  double* zwork;
+  double *fsorted, *fzf, *fzb;
+};
+
+size_t sorted_bytes(int64_t n, int mh, const slab::FourierPlan& fp, const slab::ZeroPlan& zp,
+                    bool with_sort) {
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  size_t b = 0;
+  if (with_sort) {
+    b += 2 * pad(8 * N) + 2 * pad(4 * N) + pad(4 * (size_t)slab::radix_hist_entries(n));
+    b += 4 * pad(8 * N);
+  }
+  b += pad(sizeof(double2) * (N + 1) * mh);
+  b += pad(8 * slab::fourier_work_doubles(fp));
+  b += pad(8 * slab::zero_work_doubles(zp));
+  b += pad(24 * N) + 2 * pad(8 * N);
+  return b;
+}
+
+void carve_sorted(Carver& cv, int64_t n, int mh, const slab::FourierPlan& fp,
+                  const slab::ZeroPlan& zp, bool with_sort, SortedWork& w) {
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  if (with_sort) {
+    w.sw.k0 = cv.take<uint64_t>(N);
+    w.sw.k1 = cv.take<uint64_t>(N);
+    w.sw.v0 = cv.take<int32_t>(N);
+    w.sw.v1 = cv.take<int32_t>(N);
+    w.sw.hist = cv.take<int32_t>(slab::radix_hist_entries(n));
+    w.xs = cv.take<double>(N);
+    w.ys = cv.take<double>(N);
+    w.zs = cv.take<double>(N);
+    w.qs = cv.take<double>(N);
+  }
+  w.dtab = cv.take<double2>((N + 1) * mh);
+  w.fwork = cv.take<double>(slab::fourier_work_doubles(fp));
+  w.zwork = cv.take<double>(slab::zero_work_doubles(zp));
+  w.fsorted = cv.take<double>(3 * N);
+  w.fzf = cv.take<double>(N);
+  w.fzb = cv.take<double>(N);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* slab_last_error(void) { return g_err.c_str(); }
+const char* slab_version(void) { return "slabewald_b200 0.1 (sm_100a)"; }
+
+int slab_ctx_create(SlabCtx** out) {
+  if (!out) return fail(SLAB_ERR_ARG, "null output pointer");
+  *out = new SlabCtx();
+  return SLAB_OK;
+}
+
+int slab_ctx_destroy(SlabCtx* ctx) {
+  if (!ctx) return SLAB_OK;
+  cudaDeviceSynchronize();
+  if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->small) cudaFree(ctx->small);
+  if (ctx->status) cudaFree(ctx->status);
+  if (ctx->sampler_scratch) cudaFree(ctx->sampler_scratch);
+  delete ctx;
+  return SLAB_OK;
+}
+
+int slab_sort_by_z(SlabCtx* ctx, const double* d_z, int64_t stride, int64_t n, int64_t* d_perm,
+                   void* stream) {
+  if (!ctx || n < 0 || (n > 0 && (!d_z || !d_perm)) || stride < 1)
+    return fail(SLAB_ERR_ARG, "bad sort arguments");
+  if (n > INT32_MAX) return fail(SLAB_ERR_ARG, "n exceeds int32 indexing");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  const size_t bytes = 2 * pad(8 * N) + 2 * pad(4 * N) + pad(4 * (size_t)slab::radix_hist_entries(n)) + 1024;
+  int rc = ensure_arena(ctx, bytes);
+  if (rc) return rc;
+  Carver cv{(char*)ctx->arena};
+  slab::SortWork sw;
+  sw.k0 = cv.take<uint64_t>(N);
+  sw.k1 = cv.take<uint64_t>(N);
+  sw.v0 = cv.take<int32_t>(N);
+  sw.v1 = cv.take<int32_t>(N);
+  sw.hist = cv.take<int32_t>(slab::radix_hist_entries(n));
+  int32_t* perm;
+  CK(slab::sort_by_z_device(d_z, stride, n, sw, st, &perm));
+  CK(slab::perm_to_int64(perm, n, d_perm, st));
+  return SLAB_OK;
+}
+
+int slab_fourier_sweep(SlabCtx* ctx, const double* d_x, const double* d_y, const double* d_z,
+                       const double* d_q, int64_t n, const double* d_modes,
+                       const double* d_commonv, double commonv_scalar, int64_t nmode,
+                       SlabSOE soe, double alpha, double area, int want_forces,
+                       double* d_forces_sorted, double* d_energy, int* d_status, void* stream) {
+  if (!ctx || n < 0 || nmode < 0 || !d_energy) return fail(SLAB_ERR_ARG, "bad sweep arguments");
+  if (nmode > 100000) return fail(SLAB_ERR_ARG, "too many modes for one sweep");
+  SOEHost sh;
+  int rc = prepare_soe(soe, alpha, sh);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto fp = slab::fourier_plan(n, (int)nmode, sh.mh);
+  auto zp = slab::zero_plan(n, sh.mh);
+  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, false) + 4096);
+  if (rc) return rc;
+  Carver cv{(char*)ctx->arena};
+  SortedWork w{};
+  carve_sorted(cv, n, sh.mh, fp, zp, false, w);
+  slab::FourierWork fw;
+  slab::fourier_work_carve(fp, w.fwork, fw);
+  CK(cudaMemsetAsync(d_energy, 0, sizeof(double), st));
+  if (n < 2 || nmode == 0) return SLAB_OK;
+  CK(slab::decay_table(d_z, n, sh.mh, sh.b, w.dtab, st));
+  int* status = d_status ? d_status : ctx->status;
+  if (!d_status) CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
+  CK(slab::fourier_run(fp, fw, d_x, d_y, d_z, d_q, w.dtab, d_modes, d_commonv, commonv_scalar,
+                       area, sh.b, sh.w, want_forces && d_forces_sorted, d_energy, status,
+                       d_forces_sorted, st));
+  return SLAB_OK;
+}
+
+int slab_zero_mode_sweep(SlabCtx* ctx, const double* d_z, const double* d_q, int64_t n,
+                         SlabSOE soe, double alpha, int want_forces, double* d_fz,
+                         double* d_energy, void* stream) {
+  if (!ctx || n < 0 || !d_energy) return fail(SLAB_ERR_ARG, "bad zero-mode arguments");
+  SOEHost sh;
+  int rc = prepare_soe(soe, alpha, sh);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto fp = slab::fourier_plan(n, 0, sh.mh);
+  auto zp = slab::zero_plan(n, sh.mh);
+  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, false) + 4096);
+  if (rc) return rc;
+  Carver cv{(char*)ctx->arena};
+  SortedWork w{};
+  carve_sorted(cv, n, sh.mh, fp, zp, false, w);
+  if (n < 2) return cudaMemsetAsync(d_energy, 0, sizeof(double), st) == cudaSuccess ? SLAB_OK : SLAB_ERR_CUDA;
+  CK(slab::decay_table(d_z, n, sh.mh, sh.b, w.dtab, st));
+  CK(slab::zero_run_b(zp, w.zwork, d_z, d_q, w.dtab, sh.z, sh.b, alpha, want_forces && d_fz,
+                      w.fzf, w.fzb, d_energy, st));
+  if (want_forces && d_fz) CK(slab::fz_accumulate(n, w.fzf, w.fzb, d_fz, st));
+  return SLAB_OK;
+}
+
+int slab_short_range(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                     SlabBox box, double alpha, double r_c, double* d_forces, double* d_energy,
+                     int* d_status, void* stream) {
+  if (!ctx || n < 0 || !d_energy || !d_status || (n > 0 && (!d_pos || !d_charge || !d_forces)))
+    return fail(SLAB_ERR_ARG, "bad short-range arguments");
+  if (!(alpha > 0) || !(r_c > 0)) return fail(SLAB_ERR_ARG, "alpha and r_c must be positive");
+  cudaStream_t st = (cudaStream_t)stream;
+  auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, r_c);
+  int rc = ensure_arena(ctx, slab::short_work_bytes(sp) + 1024);
+  if (rc) return rc;
+  CK(slab::short_run(sp, ctx->arena, d_pos, d_charge, box.lx, box.ly, box.lz, alpha, r_c,
+                     d_forces, d_energy, d_status, st));
+  return SLAB_OK;
+}
+
+int slab_sample_modes(SlabCtx* ctx, int64_t* d_state, uint64_t seed, double alpha, double lx,
+                      double ly, int thin, int burn_in, int64_t P, double* d_modes,
+                      int64_t* d_idx, void* stream) {
+  if (!ctx || !d_state || thin < 1 || P < 0 || burn_in < 0 || (P > 0 && !d_modes))
+    return fail(SLAB_ERR_ARG, "bad sampler arguments");
+  if (!(alpha > 0) || !(lx > 0) || !(ly > 0)) return fail(SLAB_ERR_ARG, "alpha and box must be positive");
+  const int64_t need = slab::sampler_scratch_doubles(P, thin, burn_in);
+  if (need > ctx->sampler_cap) {
+    if (ctx->sampler_scratch) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaFree(ctx->sampler_scratch));
+    }
+    CK(cudaMalloc(&ctx->sampler_scratch, sizeof(double) * need));
+    ctx->sampler_cap = need;
+  }
+  CK(slab::sample_modes(d_state, seed, alpha, lx, ly, thin, burn_in, P, d_modes, d_idx,
+                        ctx->sampler_scratch, ctx->sampler_cap, (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,
+                            const double* d_z, int64_t n, double beta_re, double beta_im,
+                            double* d_out, void* stream) {
+  if (!ctx || n < 0 || (n > 0 && (!d_q || !d_theta || !d_z || !d_out)))
+    return fail(SLAB_ERR_ARG, "bad recursive_pair_sum arguments");
+  int rc = ensure_arena(ctx, pad(sizeof(double2) * (size_t)(n / 64 + 2)) + 512);
+  if (rc) return rc;
+  CK(slab::recursive_pair_sum(d_q, d_theta, d_z, n, beta_re, beta_im, d_out,
+                              reinterpret_cast<double2*>(ctx->arena), (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
+  if (!ctx || !a) return fail(SLAB_ERR_ARG, "null context or arguments");
+  const int64_t n = a->n;
+  if (n < 0 || a->nmode < 0 || !a->d_energy || (n > 0 && (!a->d_pos || !a->d_charge)))
+    return fail(SLAB_ERR_ARG, "bad evaluation arguments");
+  if (a->want_forces && n > 0 && !a->d_forces) return fail(SLAB_ERR_ARG, "forces output missing");
+  if (n > INT32_MAX) return fail(SLAB_ERR_ARG, "n exceeds int32 indexing");
+  if (a->nmode > 0 && !a->d_modes) return fail(SLAB_ERR_ARG, "modes missing");
+  if (!(a->alpha > 0)) return fail(SLAB_ERR_ARG, "alpha must be positive");
+  SOEHost sh;
+  int rc = prepare_soe(a->soe, a->alpha, sh);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const SlabBox& box = a->box;
+  const double area = box.lx * box.ly;
+  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh);
+  auto zp = slab::zero_plan(n, sh.mh);
+  auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, a->r_c);
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  size_t bytes = sorted_bytes(n, sh.mh, fp, zp, true) + pad(24 * N) +
+                 (a->skip_short_range ? 0 : pad(slab::short_work_bytes(sp))) + 8192;
+  rc = ensure_arena(ctx, bytes);
+  if (rc) return rc;
+  Carver cv{(char*)ctx->arena};
+  SortedWork w{};
+  carve_sorted(cv, n, sh.mh, fp, zp, true, w);
+  double* fshort = cv.take<double>(3 * N);
+  void* swork = a->skip_short_range ? nullptr : cv.take<char>(slab::short_work_bytes(sp));
+  slab::FourierWork fw;
+  slab::fourier_work_carve(fp, w.fwork, fw);
+  double* u_s = ctx->small;
+  double* u_sweep = ctx->small + 1;
+  double* u_pair = ctx->small + 2;
+
+  CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(ctx->small, 0, 8 * sizeof(double), st));
+  int32_t* perm = nullptr;
+  if (n > 0) {
+    CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm));
+    CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm, st));
+  }
+  if (!a->skip_short_range)
+    CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
+                       a->r_c, fshort, u_s, ctx->status, st));
+  const bool forces = a->want_forces && n > 0;
+  if (n >= 2) {
+    CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
+    if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, st));
+    if (a->nmode > 0)
+      CK(slab::fourier_run(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, a->d_modes, a->d_commonv,
+                           a->commonv_scalar, area, sh.b, sh.w, forces ? 1 : 0, u_sweep,
+                           ctx->status, w.fsorted, st));
+    CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
+                        w.fzf, w.fzb, u_pair, st));
+  } else if (forces) {
+    CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * N, st));
+  }
+  if (forces) {
+    const double plane = box.sigma_top - box.sigma_bot;
+    CK(slab::assemble_forces(n, perm, w.qs, w.fsorted, n >= 2 ? w.fzf : nullptr, w.fzb,
+                             2.0 * slab::kPi / area, a->skip_short_range ? nullptr : fshort,
+                             a->d_charge, plane, a->d_forces, st));
+  }
+  CK(slab::assemble_energy(n, a->d_charge, a->d_pos, box.lz, box.sigma_top, box.sigma_bot,
+                           a->alpha, area, a->charge_const, u_s, u_sweep, u_pair, ctx->status,
+                           a->d_energy, st));
+  return SLAB_OK;
+}
+
+}  // extern "C"

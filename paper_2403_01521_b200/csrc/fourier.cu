@@ -1,0 +1,604 @@
+// fourier.cu -- the SOE Fourier sweep (the hot path), B200 layout.
+//
+// Replaces reference soewald2d.py:85-208 (_fourier_soe_sweep) and the per-call
+// decay table soewald2d.py:76-82.  Math, per mode t and
+// SOE term l with b_l = alpha s_l:
+//   forward   G_{l,a} = (G_{l,a-1} + u_{a-1}) e^{-b_l dz_a},  u = q e^{-i theta}
+//   backward  mirror with v = q e^{+i theta}
+//   p = kappa g - 2k sum_l c_l G_l,  zeta = 2 sum_l c_l b_l G_l - kappa g
+//   U_t += ck q Re(e^{i theta} p);  F += ... (soewald2d.py:158-202)
+//
+// B200 design:
+//  * Conjugate pairing.  s_{M-1-l} = conj(s_l) bitwise, so per pair one keeps two
+//    complex recurrences with REAL inputs (R: q cos theta, I: -+ q sin theta) and
+//    c_l G_l + conj = 2Re(c_l R_l) + 2i Re(c_l I_l).  kappa is real.
+//  * Lanes = (mode, direction) work items, particles in sequence.  Every lane of a
+//    warp walks the same z-sorted particle (forward lanes from the chunk start,
+//    backward lanes from its end), so the k-independent per-particle decays
+//    e^{-b_l dz} are BROADCAST from shared memory: they are computed once per
+//    step (decay_table_kernel) and reused by all 2P items -- the kernel is FP64
+//    bound, not HBM bound.
+//  * Particle axis split into chunks of R particles (one CTA each) with a 3-phase
+//    affine scan: (1) chunk aggregates X_c = sum_j u_j e^{-b (z_end - z_j)} using
+//    k-independent weights staged in smem, (2) a carry scan over chunks,
+//    (3) the exact recurrence from the carried-in state with the fused
+//    sincos/exp/energy/force epilogue.  All exponents stay <= 0 (stable in Lz).
+//  * Forces: per particle the 32 lanes' contributions are staged transposed in
+//    smem and row-summed (forward and backward lanes separately), accumulated
+//    per warp, then summed over warps in fixed order: deterministic, no atomics.
+#include <stdio.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace slab {
+
+constexpr int kSB = 8;          // force staging batch (particles)
+constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
+constexpr int kMaxR = 256;
+
+__host__ __device__ inline int ncomp_of(int mh) { return 2 * mh + 1; }
+
+// ---------------------------------------------------------------------------
+// k-independent tables
+// ---------------------------------------------------------------------------
+// dtab[a*mh + l] = exp(-b_l (z_a - z_{a-1})), row 0 = 1, row n = 0 (backward guard)
+__global__ void decay_table_kernel(const double* __restrict__ zs, int64_t n, int mh, BVec b,
+                                   double2* __restrict__ dtab) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (n + 1) * mh) return;
+  int64_t a = e / mh;
+  int l = (int)(e - a * mh);
+  double2 d;
+  if (a == 0) {
+    d = make_double2(1.0, 0.0);
+  } else if (a == n) {
+    d = make_double2(0.0, 0.0);
+  } else {
+    double dz = zs[a] - zs[a - 1];
+    C2 v = cexp_neg(b.re[l] * dz, b.im[l] * dz);
+    d = make_double2(v.re, v.im);
+  }
+  dtab[e] = d;
+}
+
+// zbound[c] = z_end(c), zbound[nch + c] = z_start(c);
+// Df[c*mh+l] = e^{-b_l (z_end(c) - z_end(c-1))}, Db[c*mh+l] = e^{-b_l (z_start(c+1) - z_start(c))}
+__global__ void chunk_bounds_kernel(const double* __restrict__ zs, int64_t n, int R, int nch,
+                                    int mh, BVec b, double* __restrict__ zbound,
+                                    double2* __restrict__ Df, double2* __restrict__ Db) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nch * mh) return;
+  int c = e / mh, l = e - c * mh;
+  int64_t a0 = (int64_t)c * R;
+  int64_t a1 = a0 + R < n ? a0 + R : n;
+  double zend = zs[a1 - 1], zst = zs[a0];
+  if (l == 0) {
+    zbound[c] = zend;
+    zbound[nch + c] = zst;
+  }
+  double2 df = make_double2(0.0, 0.0), db = make_double2(0.0, 0.0);
+  if (c > 0) {
+    double dz = zend - zs[a0 - 1];
+    C2 v = cexp_neg(b.re[l] * dz, b.im[l] * dz);
+    df = make_double2(v.re, v.im);
+  }
+  if (c + 1 < nch) {
+    double dz = zs[a1] - zst;
+    C2 v = cexp_neg(b.re[l] * dz, b.im[l] * dz);
+    db = make_double2(v.re, v.im);
+  }
+  Df[e] = df;
+  Db[e] = db;
+}
+
+// Per-mode coefficients (soewald2d.py:113-126), one thread per mode.
+__global__ void mode_table_kernel(const double* __restrict__ modes,
+                                  const double* __restrict__ commonv, double commonv_scalar,
+                                  int P, int mh, double area, BVec b, WVec w,
+                                  double* __restrict__ tab, int* __restrict__ status) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const double kx = modes[3 * t + 0], ky = modes[3 * t + 1], k = modes[3 * t + 2];
+  const double ct = commonv ? commonv[t] : commonv_scalar;
+  double* r = tab + (size_t)t * mode_stride(mh);
+  double kappa = 0.0;
+  int singular = 0;
+  for (int l = 0; l < mh; ++l) {
+    const double br = b.re[l], bi = b.im[l];
+    double cr = 0.0, ci = 0.0;
+    if (hypot(br - k, bi) < kSingularTol * k) {
+      singular = 1;  // analytic-limit branch (soewald2d.py:118-121) not on device
+    } else {
+      // c = w / (b^2 - k^2)
+      const double dr = br * br - bi * bi - k * k, di = 2.0 * br * bi;
+      const double den = dr * dr + di * di;
+      cr = (w.re[l] * dr + w.im[l] * di) / den;
+      ci = (w.im[l] * dr - w.re[l] * di) / den;
+    }
+    // C = 2c, CB = 2 c b; kappa = sum over all M terms of 2 c b = sum_pairs 2 Re(CB)
+    r[8 + 2 * l] = 2.0 * cr;
+    r[8 + 2 * l + 1] = 2.0 * ci;
+    const double cbr = 2.0 * (cr * br - ci * bi), cbi = 2.0 * (cr * bi + ci * br);
+    r[8 + 2 * mh + 2 * l] = cbr;
+    r[8 + 2 * mh + 2 * l + 1] = cbi;
+    kappa += 2.0 * cbr;
+  }
+  const double pref = kPi / area;
+  r[0] = kx;
+  r[1] = ky;
+  r[2] = k;
+  r[3] = pref * ct / k;
+  r[4] = pref * ct;
+  r[5] = kappa;
+  r[6] = singular;
+  r[7] = 0.0;
+  if (singular) atomicOr(status, SLAB_STATUS_SINGULAR_DEV);
+}
+
+// ---------------------------------------------------------------------------
+// phase 1: chunk aggregates
+// ---------------------------------------------------------------------------
+template <int MH>
+__global__ void __launch_bounds__(256) fourier_aggregate_kernel(
+    const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
+    const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
+    int ipg, BVec b, double2* __restrict__ carry) {
+  extern __shared__ double4 smem4[];
+  double* sx = reinterpret_cast<double*>(smem4);
+  double* sy = sx + R;
+  double* sz = sy + R;
+  double* sq = sz + R;
+  double2* sw = reinterpret_cast<double2*>(sq + R);  // [2][R][MH]: forward, backward weights
+  const int c = blockIdx.x, g = blockIdx.y;
+  const int64_t a0 = (int64_t)c * R;
+  const int len = (int)(a0 + R < n ? R : n - a0);
+  const double z_end = zs[a0 + len - 1], z_start = zs[a0];
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    sx[i] = xs[a0 + i];
+    sy[i] = ys[a0 + i];
+    sz[i] = zs[a0 + i];
+    sq[i] = qs[a0 + i];
+  }
+  for (int e = threadIdx.x; e < len * MH; e += blockDim.x) {
+    const int i = e / MH, l = e - i * MH;
+    const double z = zs[a0 + i];
+    const double df = z_end - z, db = z - z_start;
+    C2 wf = cexp_neg(b.re[l] * df, b.im[l] * df);
+    C2 wb = cexp_neg(b.re[l] * db, b.im[l] * db);
+    sw[e] = make_double2(wf.re, wf.im);
+    sw[R * MH + e] = make_double2(wb.re, wb.im);
+  }
+  __syncthreads();
+
+  const int nitems = 2 * P;
+  const int item = g * ipg + threadIdx.x;
+  const int gend = min(nitems, (g + 1) * ipg);
+  const bool active = item < gend;
+  const bool fwd = item < P;
+  const int t = active ? (fwd ? item : item - P) : 0;
+  const double* mt = modetab + (size_t)t * mode_stride(MH);
+  const double kx = mt[0], ky = mt[1], k = mt[2];
+  const double sigma = fwd ? 1.0 : -1.0;
+  const double2* W = sw + (fwd ? 0 : R * MH);
+
+  C2 Racc[MH], Iacc[MH];
+#pragma unroll
+  for (int l = 0; l < MH; ++l) Racc[l] = Iacc[l] = C2{0.0, 0.0};
+  C2 gacc{0.0, 0.0};
+  for (int i = 0; i < len; ++i) {
+    const double th = __dadd_rn(__dmul_rn(kx, sx[i]), __dmul_rn(ky, sy[i]));
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double q = sq[i];
+    const double ur = q * cs, ui = -sigma * q * sn;
+    const double dist = fwd ? (z_end - sz[i]) : (sz[i] - z_start);
+    const double wk = exp(-k * dist);
+    gacc.re = fma(ur, wk, gacc.re);
+    gacc.im = fma(ui, wk, gacc.im);
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      const double2 wl = W[i * MH + l];
+      Racc[l].re = fma(ur, wl.x, Racc[l].re);
+      Racc[l].im = fma(ur, wl.y, Racc[l].im);
+      Iacc[l].re = fma(ui, wl.x, Iacc[l].re);
+      Iacc[l].im = fma(ui, wl.y, Iacc[l].im);
+    }
+  }
+  if (active) {
+    const int nc = ncomp_of(MH);
+    double2* out = carry + (size_t)c * nc * nitems + item;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      out[(size_t)l * nitems] = make_double2(Racc[l].re, Racc[l].im);
+      out[(size_t)(MH + l) * nitems] = make_double2(Iacc[l].re, Iacc[l].im);
+    }
+    out[(size_t)(2 * MH) * nitems] = make_double2(gacc.re, gacc.im);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase 2: carry scan over chunks (in place: aggregates -> carried-in states)
+// ---------------------------------------------------------------------------
+constexpr int kCarryBatch = 16;
+
+__global__ void __launch_bounds__(128) fourier_carry_kernel(
+    double2* __restrict__ carry, int nch, int P, int mh, const double* __restrict__ modetab,
+    const double2* __restrict__ Df, const double2* __restrict__ Db,
+    const double* __restrict__ zbound) {
+  const int nitems = 2 * P, nc = ncomp_of(mh);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nitems * nc) return;
+  const int item = idx % nitems, comp = idx / nitems;
+  const bool fwd = item < P;
+  const int t = fwd ? item : item - P;
+  const bool isg = comp == 2 * mh;
+  const int l = comp < mh ? comp : comp - mh;
+  const double k = modetab[(size_t)t * mode_stride(mh) + 2];
+  const size_t cstride = (size_t)nc * nitems;
+  double2* base = carry + (size_t)comp * nitems + item;
+  C2 T{0.0, 0.0};
+  for (int b0 = 0; b0 < nch; b0 += kCarryBatch) {
+    double2 X[kCarryBatch];
+    C2 D[kCarryBatch];
+#pragma unroll
+    for (int j = 0; j < kCarryBatch; ++j) {
+      const int s = b0 + j;
+      if (s < nch) {
+        const int c = fwd ? s : nch - 1 - s;
+        X[j] = base[(size_t)c * cstride];
+        if (isg) {
+          double dz = fwd ? (c > 0 ? zbound[c] - zbound[c - 1] : 0.0)
+                          : (c + 1 < nch ? zbound[nch + c + 1] - zbound[nch + c] : 0.0);
+          D[j] = C2{exp(-k * dz), 0.0};
+        } else {
+          const double2 d = fwd ? Df[(size_t)c * mh + l] : Db[(size_t)c * mh + l];
+          D[j] = C2{d.x, d.y};
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kCarryBatch; ++j) {
+      const int s = b0 + j;
+      if (s < nch) {
+        const int c = fwd ? s : nch - 1 - s;
+        base[(size_t)c * cstride] = make_double2(T.re, T.im);
+        C2 nt = cmul(D[j], T);
+        T = C2{nt.re + X[j].x, nt.im + X[j].y};
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase 3: exact recurrence from the carried-in state + fused epilogue
+// ---------------------------------------------------------------------------
+template <int MH>
+__global__ void __launch_bounds__(256, 1) fourier_sweep_kernel(
+    const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
+    const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
+    const double* __restrict__ modetab, int P, int ipg, const double2* __restrict__ carry,
+    double* __restrict__ epart, double* __restrict__ fpart, int want_forces) {
+  extern __shared__ double4 smem4[];
+  const int nwarps = blockDim.x >> 5;
+  double* sx = reinterpret_cast<double*>(smem4);
+  double* sy = sx + R;
+  double* sq = sy + R;
+  double* sz = sq + R;                                  // R + 2 (halo below / above)
+  double2* sd = reinterpret_cast<double2*>(sz + R + 2);  // (R + 1) * MH
+  double* stage = reinterpret_cast<double*>(sd + (R + 1) * MH);  // nwarps * kSB*3 * 33
+  double* fw = stage + nwarps * kSB * 3 * kStageStride;          // nwarps * R * 3
+
+  const int c = blockIdx.x, g = blockIdx.y;
+  const int64_t a0 = (int64_t)c * R;
+  const int len = (int)(a0 + R < n ? R : n - a0);
+  const int64_t a1 = a0 + len;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    sx[i] = xs[a0 + i];
+    sy[i] = ys[a0 + i];
+    sq[i] = qs[a0 + i];
+    sz[i + 1] = zs[a0 + i];
+  }
+  if (threadIdx.x == 0) {
+    sz[0] = zs[a0 > 0 ? a0 - 1 : 0];
+    sz[len + 1] = zs[a1 < n ? a1 : a1 - 1];
+  }
+  for (int e = threadIdx.x; e < (len + 1) * MH; e += blockDim.x) sd[e] = dtab[a0 * MH + e];
+  for (int e = threadIdx.x; e < nwarps * len * 3; e += blockDim.x) {
+    const int wi = e / (len * 3);
+    fw[(size_t)wi * R * 3 + (e - wi * len * 3)] = 0.0;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nitems = 2 * P;
+  const int item = g * ipg + threadIdx.x;
+  const int gend = min(nitems, (g + 1) * ipg);
+  const bool active = item < gend;
+  const bool fwd = item < P;
+  const int t = active ? (fwd ? item : item - P) : 0;
+  const unsigned fmask = __ballot_sync(0xffffffffu, active && fwd);
+  const unsigned bmask = __ballot_sync(0xffffffffu, active && !fwd);
+
+  const double* mt = modetab + (size_t)t * mode_stride(MH);
+  const double kx = mt[0], ky = mt[1], k = mt[2];
+  const double sigma = fwd ? 1.0 : -1.0;
+  const double fxy_c = active ? sigma * mt[3] : 0.0;   // +-ck
+  const double fz_c = active ? -sigma * mt[4] : 0.0;   // -+cz
+  const double kappa = mt[5];
+  const double two_k = 2.0 * k;
+  C2 Cc[MH], CB[MH], Rs[MH], Is[MH];
+#pragma unroll
+  for (int l = 0; l < MH; ++l) {
+    Cc[l] = C2{mt[8 + 2 * l], mt[9 + 2 * l]};
+    CB[l] = C2{mt[8 + 2 * MH + 2 * l], mt[9 + 2 * MH + 2 * l]};
+  }
+  const int nc = ncomp_of(MH);
+  C2 gk{0.0, 0.0};
+  {
+    const double2* cin = carry + (size_t)c * nc * nitems + (active ? item : 0);
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      double2 r = cin[(size_t)l * nitems], im = cin[(size_t)(MH + l) * nitems];
+      Rs[l] = C2{r.x, r.y};
+      Is[l] = C2{im.x, im.y};
+    }
+    double2 gg = cin[(size_t)(2 * MH) * nitems];
+    gk = C2{gg.x, gg.y};
+  }
+
+  double* st = stage + warp * kSB * 3 * kStageStride;
+  double* fwp = fw + (size_t)warp * R * 3;
+  double E = 0.0;
+  for (int i = 0; i < len; ++i) {
+    const int ia = fwd ? i : len - 1 - i;
+    const int id = fwd ? ia : ia + 1;
+    const double dz = fwd ? (sz[ia + 1] - sz[ia]) : (sz[ia + 2] - sz[ia + 1]);
+    const double dk = exp(-k * dz);
+    // S_a = T_{a-1} * d_a  (forward) / T'_{a+1} * d_{a+1} (backward)
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      const double2 d = sd[id * MH + l];
+      Rs[l] = cmul(Rs[l], C2{d.x, d.y});
+      Is[l] = cmul(Is[l], C2{d.x, d.y});
+    }
+    gk.re *= dk;
+    gk.im *= dk;
+    double sgr = 0.0, sgi = 0.0, sbr = 0.0, sbi = 0.0;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      sgr = fma(Cc[l].re, Rs[l].re, fma(-Cc[l].im, Rs[l].im, sgr));
+      sgi = fma(Cc[l].re, Is[l].re, fma(-Cc[l].im, Is[l].im, sgi));
+      sbr = fma(CB[l].re, Rs[l].re, fma(-CB[l].im, Rs[l].im, sbr));
+      sbi = fma(CB[l].re, Is[l].re, fma(-CB[l].im, Is[l].im, sbi));
+    }
+    const double x = sx[ia], y = sy[ia], q = sq[ia];
+    const double th = __dadd_rn(__dmul_rn(kx, x), __dmul_rn(ky, y));
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double ps = sigma * sn;  // phase e^{+-i theta} = (cs, ps)
+    const double pr = fma(kappa, gk.re, -two_k * sgr);
+    const double pi = fma(kappa, gk.im, -two_k * sgi);
+    const double er = fma(cs, pr, -ps * pi);
+    const double ei = fma(cs, pi, ps * pr);
+    E = fma(q, er, E);
+    if (want_forces) {
+      const double ztr = fma(2.0, sbr, -kappa * gk.re);
+      const double zti = fma(2.0, sbi, -kappa * gk.im);
+      const double fxy = fxy_c * q * ei;
+      const int slot = i % kSB;
+      st[(slot * 3 + 0) * kStageStride + lane] = fxy * kx;
+      st[(slot * 3 + 1) * kStageStride + lane] = fxy * ky;
+      st[(slot * 3 + 2) * kStageStride + lane] = fz_c * q * fma(cs, ztr, -ps * zti);
+      if (slot == kSB - 1 || i == len - 1) {
+        __syncwarp();
+        const int nslot = slot + 1, ibase = i - slot;
+        const int s = lane / 3, comp = lane - 3 * (lane / 3);
+        double sf = 0.0, sb = 0.0;
+        if (lane < 3 * nslot) {
+          const double* row = st + (s * 3 + comp) * kStageStride;
+#pragma unroll 8
+          for (int j = 0; j < 32; ++j) {
+            const double v = row[j];
+            if ((fmask >> j) & 1u) sf += v;
+            if ((bmask >> j) & 1u) sb += v;
+          }
+          if (fmask) fwp[(ibase + s) * 3 + comp] += sf;
+        }
+        __syncwarp();
+        if (lane < 3 * nslot && bmask) fwp[(len - 1 - (ibase + s)) * 3 + comp] += sb;
+        __syncwarp();
+      }
+    }
+    // T_a = S_a + u_a (input is real for every recurrence)
+    const double ur = q * cs, ui = -sigma * q * sn;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      Rs[l].re += ur;
+      Is[l].re += ui;
+    }
+    gk.re += ur;
+    gk.im += ui;
+  }
+  if (active && fwd) epart[(size_t)c * P + t] = E;
+  if (!want_forces) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < len * 3; e += blockDim.x) {
+    double v = 0.0;
+    for (int wi = 0; wi < nwarps; ++wi) v += fw[(size_t)wi * R * 3 + e];
+    fpart[(size_t)g * n * 3 + a0 * 3 + e] = v;
+  }
+}
+
+// per-mode sums over chunks (fixed order), then Kahan over modes in mode order
+// exactly like soewald2d.py:204-207
+__global__ void fourier_energy_kernel(const double* __restrict__ epart, int nch, int P, int mh,
+                                      const double* __restrict__ modetab,
+                                      double* __restrict__ out) {
+  extern __shared__ double se[];
+  for (int t = threadIdx.x; t < P; t += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nch; ++c) s += epart[(size_t)c * P + t];
+    se[t] = modetab[(size_t)t * mode_stride(mh) + 3] * s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0, comp = 0.0;
+    for (int t = 0; t < P; ++t) {
+      double y = se[t] - comp;
+      double tt = u + y;
+      comp = (tt - u) - y;
+      u = tt;
+    }
+    out[0] = u;
+  }
+}
+
+// forces_sorted (+)= sum over item groups (fixed order)
+__global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int ngroups,
+                                            int64_t n3, double* __restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n3) return;
+  double v = 0.0;
+  for (int g = 0; g < ngroups; ++g) v += fpart[(size_t)g * n3 + e];
+  out[e] += v;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static size_t sweep_smem(int R, int mh, int warps) {
+  return sizeof(double) * (3 * (size_t)R + R + 2) + sizeof(double2) * (size_t)(R + 1) * mh +
+         sizeof(double) * (size_t)warps * kSB * 3 * kStageStride +
+         sizeof(double) * (size_t)warps * R * 3;
+}
+static size_t agg_smem(int R, int mh) {
+  return sizeof(double) * 4 * (size_t)R + sizeof(double2) * 2 * (size_t)R * mh;
+}
+
+FourierPlan fourier_plan(int64_t n, int P, int mh) {
+  FourierPlan p{};
+  p.n = n;
+  p.P = P;
+  p.mh = mh;
+  const int nitems = 2 * P;
+  p.ngroups = (nitems + 255) / 256;
+  if (p.ngroups < 1) p.ngroups = 1;
+  p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
+  p.warps = (p.ipg + 31) / 32;
+  if (p.warps < 1) p.warps = 1;
+  const int64_t target_ctas = 4 * 148;
+  int64_t rf = n * p.ngroups / target_ctas;
+  int R = 16;
+  while (R * 2 <= rf && R * 2 <= kMaxR) R *= 2;
+  p.R = R;
+  p.nch = (int)((n + R - 1) / R);
+  p.smem_agg = agg_smem(R, mh);
+  p.smem_sweep = sweep_smem(R, mh, p.warps);
+  return p;
+}
+
+size_t fourier_work_doubles(const FourierPlan& p) {
+  const size_t nitems = 2 * (size_t)p.P;
+  size_t d = (size_t)p.P * mode_stride(p.mh);
+  d += 2 * (size_t)p.nch * ncomp_of(p.mh) * nitems;  // carry (double2)
+  d += 2 * 2 * (size_t)p.nch * p.mh;                 // Df, Db (double2)
+  d += 2 * (size_t)p.nch;                            // zbound
+  d += (size_t)p.nch * p.P;                          // epart
+  d += (size_t)p.ngroups * p.n * 3;                  // fpart
+  return d + 64;
+}
+
+void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w) {
+  const size_t nitems = 2 * (size_t)p.P;
+  double* q = base;
+  w.modetab = q;
+  q += (size_t)p.P * mode_stride(p.mh);
+  q += (reinterpret_cast<uintptr_t>(q) / 8) & 1;  // 16-byte align for double2
+  w.carry = reinterpret_cast<double2*>(q);
+  q += 2 * (size_t)p.nch * ncomp_of(p.mh) * nitems;
+  w.dchunk = reinterpret_cast<double2*>(q);
+  q += 4 * (size_t)p.nch * p.mh;
+  w.zbound = q;
+  q += 2 * (size_t)p.nch;
+  w.epart = q;
+  q += (size_t)p.nch * p.P;
+  w.fpart = q;
+}
+
+cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, double2* dtab,
+                        cudaStream_t st) {
+  const int64_t tot = (n + 1) * mh;
+  decay_table_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(zs, n, mh, b, dtab);
+  return cudaGetLastError();
+}
+
+template <int MH>
+static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
+                          const double* ys, const double* zs, const double* qs,
+                          const double2* dtab, const BVec& b, int want_forces,
+                          cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(fourier_aggregate_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)agg_smem(kMaxR, MH));
+    cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sweep_smem(kMaxR, MH, 8));
+    attr_done = true;
+  }
+  dim3 grid(p.nch, p.ngroups);
+  if (p.nch > 1)
+    fourier_aggregate_kernel<MH><<<grid, p.warps * 32, p.smem_agg, st>>>(
+        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, p.ipg, b, w.carry);
+  else
+    cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
+  if (p.nch > 1) {
+    const int nthr = 2 * p.P * ncomp_of(MH);
+    fourier_carry_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(
+        w.carry, p.nch, p.P, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH, w.zbound);
+  }
+  fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
+      xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.ipg, w.carry, w.epart, w.fpart,
+      want_forces);
+  return cudaGetLastError();
+}
+
+cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double* xs,
+                        const double* ys, const double* zs, const double* qs,
+                        const double2* dtab, const double* modes, const double* commonv,
+                        double commonv_scalar, double area, const BVec& b, const WVec& wv,
+                        int want_forces, double* energy_out, int* status, double* forces_sorted,
+                        cudaStream_t st) {
+  if (p.P <= 0 || p.n < 2) return cudaSuccess;
+  mode_table_kernel<<<(p.P + 127) / 128, 128, 0, st>>>(modes, commonv, commonv_scalar, p.P, p.mh,
+                                                       area, b, wv, w.modetab, status);
+  const int nb = p.nch * p.mh;
+  chunk_bounds_kernel<<<(nb + 127) / 128, 128, 0, st>>>(zs, p.n, p.R, p.nch, p.mh, b, w.zbound,
+                                                        w.dchunk, w.dchunk + (size_t)p.nch * p.mh);
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (p.mh) {
+    case 2: e = run_mh<2>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 3: e = run_mh<3>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 4: e = run_mh<4>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 5: e = run_mh<5>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 6: e = run_mh<6>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 7: e = run_mh<7>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 8: e = run_mh<8>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 9: e = run_mh<9>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 10: e = run_mh<10>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 11: e = run_mh<11>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    case 12: e = run_mh<12>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  size_t sm = sizeof(double) * (size_t)p.P;
+  fourier_energy_kernel<<<1, 256, sm, st>>>(w.epart, p.nch, p.P, p.mh, w.modetab, energy_out);
+  if (want_forces) {
+    const int64_t n3 = p.n * 3;
+    fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(w.fpart, p.ngroups,
+                                                                              n3, forces_sorted);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace slab

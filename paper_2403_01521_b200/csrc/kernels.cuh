@@ -1,0 +1,130 @@
+// kernels.cuh -- internal host-side launch API shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace slab {
+
+// ---------------------------------------------------------------- sort.cu
+struct SortWork {
+  uint64_t* k0;
+  uint64_t* k1;
+  int32_t* v0;
+  int32_t* v1;
+  int32_t* hist;
+};
+int64_t radix_hist_entries(int64_t n);
+cudaError_t sort_by_z_device(const double* z, int64_t stride, int64_t n, SortWork& w,
+                             cudaStream_t st, int32_t** perm_out);
+template <typename K>
+cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_alt,
+                             int32_t* hist, int64_t n, int key_bits, cudaStream_t st,
+                             K** keys_out, int32_t** vals_out);
+cudaError_t gather_sorted(const double* pos, const double* charge, const int32_t* perm, int64_t n,
+                          double* xs, double* ys, double* zs, double* qs, int64_t* perm64,
+                          cudaStream_t st);
+cudaError_t perm_to_int64(const int32_t* p, int64_t n, int64_t* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- SOE constants
+struct BVec {  // b_l = alpha * s_l for the pair representatives l < mh
+  double re[12];
+  double im[12];
+};
+struct WVec {
+  double re[12];
+  double im[12];
+};
+struct ZCoef {  // zero-mode pair coefficients (all doubled for the conj partner)
+  double ws2[24];   // 2 w/s      (re,im interleaved)
+  double w2[24];    // 2 w
+  double f2[24];    // 2 (w/s + w s / 2)
+  double aw2[24];   // 2 alpha w
+};
+
+// ---------------------------------------------------------------- fourier.cu
+struct FourierPlan {
+  int64_t n;
+  int P;          // modes
+  int mh;         // SOE pairs
+  int R;          // particles per chunk
+  int nch;        // chunks
+  int ngroups;    // item groups per chunk
+  int ipg;        // items per group
+  int warps;      // warps per CTA
+  size_t smem_agg, smem_sweep;
+};
+FourierPlan fourier_plan(int64_t n, int P, int mh);
+// bytes of device workspace the plan needs (carry, chunk decays, mode table, partials)
+struct FourierWork {
+  double* modetab;   // P * mode_stride
+  double2* carry;    // nch * (2mh+1) * 2P
+  double2* dchunk;   // 2 * nch * mh   (Df, Db)
+  double* zbound;    // 2 * nch        (z_end, z_start)
+  double* epart;     // nch * P
+  double* fpart;     // ngroups * n * 3
+};
+size_t fourier_work_doubles(const FourierPlan& p);
+void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w);
+cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, double2* dtab,
+                        cudaStream_t st);
+cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double* xs,
+                        const double* ys, const double* zs, const double* qs,
+                        const double2* dtab, const double* modes, const double* commonv,
+                        double commonv_scalar, double area, const BVec& b, const WVec& wv,
+                        int want_forces, double* energy_out, int* status, double* forces_sorted,
+                        cudaStream_t st);
+
+// ---------------------------------------------------------------- zero.cu
+struct ZeroPlan {
+  int64_t n;
+  int mh;
+  int R;
+  int nch;
+};
+ZeroPlan zero_plan(int64_t n, int mh);
+size_t zero_work_doubles(const ZeroPlan& p);
+cudaError_t zero_run_b(const ZeroPlan& p, double* work, const double* zs, const double* qs,
+                       const double2* dtab, const ZCoef& zc, const BVec& b, double alpha,
+                       int want_forces, double* fzf, double* fzb, double* upair,
+                       cudaStream_t st);
+
+// ---------------------------------------------------------------- short.cu
+struct ShortPlan {
+  int64_t n;
+  int ncx, ncy, ncz;
+  int brute;
+  int64_t ncell;
+  int jsplit;     // brute path: j-range splits
+  int64_t nblk;   // energy partial count
+};
+ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc);
+size_t short_work_bytes(const ShortPlan& p);
+cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
+                      double lx, double ly, double lz, double alpha, double rc, double* forces,
+                      double* energy_out, int* status, cudaStream_t st);
+
+// ---------------------------------------------------------------- assemble.cu
+cudaError_t assemble_forces(int64_t n, const int32_t* perm, const double* qs,
+                            const double* fsorted, const double* fzf, const double* fzb,
+                            double zpref, const double* fshort, const double* charge,
+                            double fz_plane, double* forces, cudaStream_t st);
+cudaError_t assemble_energy(int64_t n, const double* charge, const double* pos, double lz,
+                            double sigma_top, double sigma_bot, double alpha, double area,
+                            double charge_const, const double* u_s, const double* u_sweep,
+                            const double* u_pair, const int* status, double* energy,
+                            cudaStream_t st);
+
+// ---------------------------------------------------------------- sampler.cu
+cudaError_t sample_modes(int64_t* state, uint64_t seed, double alpha, double lx, double ly,
+                         int thin, int burn_in, int64_t P, double* modes, int64_t* idx,
+                         double* scratch, int64_t scratch_doubles, cudaStream_t st);
+int64_t sampler_scratch_doubles(int64_t P, int thin, int burn_in);
+
+// ---------------------------------------------------------------- misc
+cudaError_t recursive_pair_sum(const double* q, const double* theta, const double* z, int64_t n,
+                               double beta_re, double beta_im, double* out, double2* agg,
+                               cudaStream_t st);
+cudaError_t fz_accumulate(int64_t n, const double* fzf, const double* fzb, double* fz,
+                          cudaStream_t st);
+
+}  // namespace slab

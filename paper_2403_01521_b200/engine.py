@@ -1,0 +1,261 @@
+"""Device-side engine: torch owns device memory and streams, the C-ABI does the work.
+
+``Engine`` wraps one ``SlabCtx`` per CUDA device.  Its methods take torch CUDA
+tensors and enqueue C-ABI calls on the current torch stream; they never fall
+back to the CPU.  ``DeviceEvaluator`` keeps a whole RBSE2D / SOEwald2D step
+device-resident (positions, sampled modes, forces, energies) and can replay it
+as a CUDA graph -- the form the MD loop and ``bench.py`` use.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native
+from ._native import SlabBox, SlabEvalArgs, SlabSOE, check
+
+_engines: dict = {}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def require_cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _native.NativeUnavailable(
+            "no CUDA device visible: this package has no CPU fallback")
+    _native.load()
+    return torch
+
+
+class _SOEPack:
+    """Host copies of the SOE table kept alive for the duration of a call."""
+
+    def __init__(self, soe):
+        w = np.asarray(soe.w, dtype=np.complex128)
+        s = np.asarray(soe.s, dtype=np.complex128)
+        self.arrays = [np.ascontiguousarray(a) for a in (w.real, w.imag, s.real, s.imag)]
+        p = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for a in self.arrays]
+        self.struct = SlabSOE(len(w), *p)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class Engine:
+    def __init__(self, device):
+        torch = require_cuda()
+        self.device = torch.device(device)
+        self.lib = _native.load()
+        self.ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(self.lib.slab_ctx_create(ctypes.byref(self.ctx)), "slab_ctx_create")
+
+    def _stream(self):
+        torch = _torch()
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    # -- sort ---------------------------------------------------------------
+    def sort_by_z(self, z, stride: int = 1):
+        torch = _torch()
+        n = z.numel() // stride if stride > 1 else z.numel()
+        perm = torch.empty(n, dtype=torch.int64, device=self.device)
+        check(self.lib.slab_sort_by_z(self.ctx, _ptr(z), stride, n, _ptr(perm), self._stream()),
+              "slab_sort_by_z")
+        return perm
+
+    # -- full evaluation ----------------------------------------------------
+    def evaluate(self, pos, charge, box, alpha, r_c, soe, modes, commonv, charge_const,
+                 forces=None, energy=None, want_forces=True, skip_short_range=False,
+                 perm=None, soe_pack=None):
+        """Enqueue one energy/force evaluation.  ``commonv`` is a float (RB) or a
+        (P,) device tensor (full mode sum).  Writes energy (8,) and forces (n,3)."""
+        torch = _torch()
+        n = charge.numel()
+        if energy is None:
+            energy = torch.empty(8, dtype=torch.float64, device=self.device)
+        if forces is None and want_forces:
+            forces = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        pack = soe_pack or _SOEPack(soe)
+        P = 0 if modes is None else modes.shape[0]
+        cv_t = commonv if torch.is_tensor(commonv) else None
+        args = SlabEvalArgs(
+            n=n, d_pos=_ptr(pos), d_charge=_ptr(charge),
+            box=SlabBox(box.lx, box.ly, box.lz, box.sigma_top, box.sigma_bot),
+            alpha=float(alpha), r_c=float(r_c), soe=pack.struct,
+            d_modes=_ptr(modes) if P else None, nmode=P, d_commonv=_ptr(cv_t),
+            commonv_scalar=0.0 if cv_t is not None else float(commonv),
+            charge_const=float(charge_const), want_forces=1 if want_forces else 0,
+            skip_short_range=1 if skip_short_range else 0,
+            d_forces=_ptr(forces) if want_forces else None, d_energy=_ptr(energy),
+            d_perm=_ptr(perm))
+        check(self.lib.slab_evaluate(self.ctx, ctypes.byref(args), self._stream()),
+              "slab_evaluate")
+        return energy, forces
+
+    # -- sub-paths ----------------------------------------------------------
+    def short_range(self, pos, charge, box, alpha, r_c):
+        torch = _torch()
+        n = charge.numel()
+        forces = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        energy = torch.zeros(1, dtype=torch.float64, device=self.device)
+        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        check(self.lib.slab_short_range(
+            self.ctx, _ptr(pos), _ptr(charge), n,
+            SlabBox(box.lx, box.ly, box.lz, box.sigma_top, box.sigma_bot), float(alpha),
+            float(r_c), _ptr(forces), _ptr(energy), _ptr(status), self._stream()),
+            "slab_short_range")
+        return energy, forces, status
+
+    def fourier_sweep(self, x, y, z, q, modes, commonv, soe, alpha, area, want_forces,
+                      forces_sorted=None):
+        torch = _torch()
+        n = q.numel()
+        energy = torch.zeros(1, dtype=torch.float64, device=self.device)
+        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        pack = _SOEPack(soe)
+        cv_t = commonv if torch.is_tensor(commonv) else None
+        check(self.lib.slab_fourier_sweep(
+            self.ctx, _ptr(x), _ptr(y), _ptr(z), _ptr(q), n, _ptr(modes), _ptr(cv_t),
+            0.0 if cv_t is not None else float(commonv), modes.shape[0], pack.struct,
+            float(alpha), float(area), 1 if want_forces else 0, _ptr(forces_sorted),
+            _ptr(energy), _ptr(status), self._stream()), "slab_fourier_sweep")
+        return energy, status
+
+    def zero_mode_sweep(self, z, q, soe, alpha, want_forces, fz=None):
+        torch = _torch()
+        energy = torch.zeros(1, dtype=torch.float64, device=self.device)
+        pack = _SOEPack(soe)
+        check(self.lib.slab_zero_mode_sweep(
+            self.ctx, _ptr(z), _ptr(q), q.numel(), pack.struct, float(alpha),
+            1 if want_forces else 0, _ptr(fz), _ptr(energy), self._stream()),
+            "slab_zero_mode_sweep")
+        return energy
+
+    def sample_modes(self, state, seed, alpha, lx, ly, thin, burn_in, P, modes=None, idx=None):
+        check(self.lib.slab_sample_modes(
+            self.ctx, _ptr(state), ctypes.c_uint64(seed), float(alpha), float(lx), float(ly),
+            int(thin), int(burn_in), int(P), _ptr(modes), _ptr(idx), self._stream()),
+            "slab_sample_modes")
+
+    def recursive_pair_sum(self, q, theta, z, beta):
+        torch = _torch()
+        out = torch.empty((q.numel(), 2), dtype=torch.float64, device=self.device)
+        check(self.lib.slab_recursive_pair_sum(
+            self.ctx, _ptr(q), _ptr(theta), _ptr(z), q.numel(), float(beta.real),
+            float(beta.imag), _ptr(out), self._stream()), "slab_recursive_pair_sum")
+        return out
+
+
+def get_engine(device=None) -> Engine:
+    torch = require_cuda()
+    dev = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+    if dev.index is None:
+        dev = torch.device(f"cuda:{torch.cuda.current_device()}")
+    eng = _engines.get(dev.index)
+    if eng is None:
+        eng = _engines[dev.index] = Engine(dev)
+    return eng
+
+
+def to_device(a, dtype=None, device=None):
+    torch = require_cuda()
+    eng = get_engine(device)
+    t = torch.as_tensor(np.ascontiguousarray(a), dtype=dtype or torch.float64)
+    return t.to(eng.device, non_blocking=False)
+
+
+def device_sort_perm(z: np.ndarray, lz: float) -> np.ndarray:
+    """Host helper behind core.sort_by_z: device radix sort, permutation to numpy."""
+    eng = get_engine()
+    torch = _torch()
+    if z.size == 0:
+        return np.zeros(0, dtype=np.int64)
+    zt = torch.as_tensor(np.ascontiguousarray(z, dtype=np.float64)).to(eng.device)
+    perm = eng.sort_by_z(zt, 1)
+    return perm.cpu().numpy()
+
+
+class DeviceEvaluator:
+    """A device-resident RBSE2D (``P`` sampled modes) or SOEwald2D (full mode set) step.
+
+    Positions / charges live on the device; each ``step()`` (optionally) draws a
+    fresh k-set with the device sampler and evaluates energy + forces, all on one
+    stream with no host synchronisation.  ``capture()`` records the step as a
+    CUDA graph so small systems are not launch bound.
+    """
+
+    def __init__(self, system, box, params, soe, P=None, H=None, c_q=None, seed=0, thin=10,
+                 burn_in=100, modes=None, device=None, sample=True):
+        from .rbse2d import charge_term_sum, normalization_H
+        from .soewald2d import full_sum_constants
+        torch = require_cuda()
+        self.eng = get_engine(device)
+        dev = self.eng.device
+        self.box, self.params, self.soe = box, params, soe
+        self.alpha = params.alpha
+        self.pack = _SOEPack(soe)
+        self.n = system.n
+        self.pos = torch.as_tensor(system.pos).to(dev)
+        self.charge = torch.as_tensor(system.charge).to(dev)
+        self.forces = torch.empty((self.n, 3), dtype=torch.float64, device=dev)
+        self.energy = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.graph = None
+        Q = float(np.sum(system.charge ** 2))
+        if P is None:  # deterministic full mode sum (soe_energy_forces)
+            self.P = params.kmodes.shape[0]
+            cv, uq = full_sum_constants(params, box, Q)
+            self.modes = torch.as_tensor(params.kmodes).to(dev)
+            self.commonv = torch.as_tensor(cv).to(dev)
+            self.charge_const = uq
+            self.sample = False
+        else:
+            self.P = int(P)
+            self.H = normalization_H(self.alpha, box) if H is None else H
+            self.charge_const = charge_term_sum(self.alpha, box, Q) if c_q is None else c_q
+            self.commonv = (self.H / self.P) * (2.0 / math.sqrt(math.pi)) * self.alpha
+            self.modes = torch.empty((self.P, 3), dtype=torch.float64, device=dev)
+            self.sample = sample and modes is None
+            if modes is not None:
+                self.modes.copy_(torch.as_tensor(np.asarray(modes, dtype=np.float64)))
+            self.seed, self.thin = int(seed), int(thin)
+            self.state = torch.zeros(6, dtype=torch.int64, device=dev)
+            if self.sample:
+                self.eng.sample_modes(self.state, self.seed, self.alpha, box.lx, box.ly,
+                                      self.thin, burn_in, 0)
+
+    def _enqueue(self):
+        if self.sample:
+            self.eng.sample_modes(self.state, self.seed, self.alpha, self.box.lx, self.box.ly,
+                                  self.thin, 0, self.P, self.modes)
+        self.eng.evaluate(self.pos, self.charge, self.box, self.alpha, self.params.r_c, self.soe,
+                          self.modes, self.commonv, self.charge_const, forces=self.forces,
+                          energy=self.energy, soe_pack=self.pack)
+
+    def capture(self):
+        torch = _torch()
+        s = torch.cuda.Stream(self.eng.device)
+        s.wait_stream(torch.cuda.current_stream(self.eng.device))
+        with torch.cuda.stream(s):
+            self._enqueue()  # warm-up outside capture (workspace, func attributes)
+        torch.cuda.current_stream(self.eng.device).wait_stream(s)
+        torch.cuda.synchronize(self.eng.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._enqueue()
+        self.graph = g
+        return g
+
+    def step(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._enqueue()
+        return self.energy, self.forces

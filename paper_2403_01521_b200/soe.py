@@ -1,0 +1,180 @@
+"""Sum-of-exponentials (SOE) coefficients for the unit Gaussian, host side.
+
+``exp(-x^2) ~= sum_l w_l exp(-s_l |x|)`` with M complex-conjugate-paired terms
+from trapezoidal quadrature of an inverse-Laplace integral along a hyperbolic
+contour ``z(u) = mu (1 + sin(i u - delta))``, ``s = 2 sqrt(z)``.
+
+Reference: ``pkg/src/slabewald/soe.py`` -- contour nodes ``_contour_nodes``
+(77-84), builder ``build_soe_contour`` (101-116), certification
+``certify_soe_raw`` (119-143), CSV tables (151-177).  The hot path only consumes
+``SOEApprox.w`` and ``.s``; this module is per-run setup.
+
+The device kernels rely on the exact conjugate pairing
+``s[M-1-l] == conj(s[l])`` and ``w[M-1-l] == conj(w[l])`` (bitwise), which every
+contour built here satisfies; ``is_conjugate_paired`` checks it.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+import math
+
+import numpy as np
+
+SQRT_PI = math.sqrt(math.pi)
+
+# Tuned contour parameters (mu, h, delta) per term count -- numeric data taken
+# from the reference table (``soe.py:28-36``) so that the coefficient tables
+# are identical to the reference's.
+CONTOUR_PARAMS = {
+    4: (9.488067269, 0.470062043, 1.017129457),
+    6: (5.538899482, 0.485312224, 0.911189212),
+    8: (5.471154454, 0.416613684, 0.876565397),
+    12: (11.247880597, 0.250206047, 0.970986853),
+    16: (19.946013034, 0.169984766, 1.018726016),
+    20: (29.503144889, 0.127993786, 1.068943730),
+    24: (35.541230958, 0.106333243, 1.074848562),
+}
+# informational sup errors (reference ``soe.py:39-40``); always re-measured
+ACHIEVED_EPS = {4: 1.6e-3, 6: 2.0e-4, 8: 3.2e-5, 12: 2.9e-7,
+                16: 1.4e-9, 20: 2.2e-11, 24: 2.3e-13}
+CERT_DOMAIN = 20.0
+# removable-singularity switch |b_l - k| < SINGULAR_TOL * k (reference soe.py:49)
+SINGULAR_TOL = 2e-6
+
+
+@dataclass(frozen=True)
+class SOEApprox:
+    """Certified coefficients: ``exp(-x^2) ~ sum w_l exp(-s_l |x|)``."""
+
+    m: int
+    w: np.ndarray
+    s: np.ndarray
+    eps_certified: float
+    domain_max: float
+
+    def __post_init__(self):
+        if np.any(np.asarray(self.s).real <= 0):
+            raise ValueError("every exponent must have positive real part")
+
+
+def eval_soe(w: np.ndarray, s: np.ndarray, x) -> np.ndarray:
+    """Complex value of ``sum_l w_l exp(-s_l |x|)`` (imaginary residue kept)."""
+    ax = np.abs(np.asarray(x, dtype=np.float64))
+    return np.exp(-np.multiply.outer(ax, s)) @ w
+
+
+def eval_soe_real(soe: SOEApprox, x) -> np.ndarray:
+    return np.real(eval_soe(soe.w, soe.s, x))
+
+
+def _nodes(m: int, mu: float, h: float, delta: float):
+    u = (np.arange(-(m // 2), m // 2) + 0.5) * h
+    arg = 1j * u - delta
+    z = mu * (1.0 + np.sin(arg))
+    dz = 1j * mu * np.cos(arg)
+    w = SQRT_PI * h / (2.0j * np.pi) * np.exp(z) * z ** (-0.5) * dz
+    return w, 2.0 * np.sqrt(z)
+
+
+def _params_for(m: int):
+    tuned = sorted(CONTOUR_PARAMS)
+    if not tuned[0] <= m <= tuned[-1]:
+        raise ValueError(f"term count {m} outside the tuned range {tuned[0]}..{tuned[-1]}; "
+                         "use load_soe_table for external coefficients")
+    if m in CONTOUR_PARAMS:
+        return CONTOUR_PARAMS[m]
+    hi = min(v for v in tuned if v >= m)
+    lo = max(v for v in tuned if v <= m)
+    t = (m - lo) / (hi - lo)
+    return tuple((1 - t) * a + t * b for a, b in zip(CONTOUR_PARAMS[lo], CONTOUR_PARAMS[hi]))
+
+
+def certify_soe_raw(w: np.ndarray, s: np.ndarray, x_max: float = CERT_DOMAIN,
+                    grid_n: int = 20001, target=None) -> float:
+    """Sup |Re SOE(x) - target(x)| on [0, x_max]: dense scan + bounded refinement
+    around each interior local maximum of the scan."""
+    from scipy.optimize import minimize_scalar
+
+    if grid_n < 1000:
+        raise ValueError("grid_n must be at least 1000")
+    f = target if target is not None else (lambda x: np.exp(-np.asarray(x, dtype=np.float64) ** 2))
+
+    def gap(x):
+        return np.abs(np.real(eval_soe(w, s, x)) - f(x))
+
+    grid = np.linspace(0.0, x_max, grid_n)
+    g = gap(grid)
+    sup = float(g.max())
+    peaks = np.flatnonzero((g[1:-1] >= g[:-2]) & (g[1:-1] >= g[2:])) + 1
+    for i in peaks:
+        r = minimize_scalar(lambda t: -gap(t), bounds=(grid[i - 1], grid[i + 1]),
+                            method="bounded", options={"xatol": 1e-12})
+        sup = max(sup, float(-r.fun))
+    return sup
+
+
+def certify_soe(soe: SOEApprox, x_max: float = CERT_DOMAIN, grid_n: int = 20001,
+                target=None) -> float:
+    return certify_soe_raw(soe.w, soe.s, x_max, grid_n, target)
+
+
+def build_soe_contour(m: int, x_max: float = CERT_DOMAIN) -> SOEApprox:
+    """M-term conjugate-paired contour SOE, certified on [0, x_max].
+
+    Odd M is bumped to the next even count (pairing needs it).
+    """
+    if m < 2:
+        raise ValueError("need at least two terms")
+    m += m % 2
+    w, s = _nodes(m, *_params_for(m))
+    if np.any(s.real <= 0):
+        raise ValueError("contour produced an exponent with nonpositive real part")
+    return SOEApprox(m=m, w=w, s=s, eps_certified=certify_soe_raw(w, s, x_max),
+                     domain_max=x_max)
+
+
+def load_soe_table(path, x_max: float = CERT_DOMAIN) -> SOEApprox:
+    """Read ``re_w,im_w,re_s,im_s`` CSV and recertify (never trust the file)."""
+    data = np.atleast_1d(np.genfromtxt(path, delimiter=",", names=True, dtype=np.float64))
+    if data.size == 0:
+        raise ValueError("empty coefficient table")
+    if list(data.dtype.names) != ["re_w", "im_w", "re_s", "im_s"]:
+        raise ValueError("coefficient table must have header re_w,im_w,re_s,im_s")
+    if not (np.all(np.isfinite(data["re_w"])) and np.all(np.isfinite(data["re_s"]))):
+        raise ValueError("coefficient table contains non-finite entries")
+    w = data["re_w"] + 1j * data["im_w"]
+    s = data["re_s"] + 1j * data["im_s"]
+    if np.any(s.real <= 0):
+        raise ValueError("every exponent must have positive real part")
+    return SOEApprox(m=len(w), w=w, s=s, eps_certified=certify_soe_raw(w, s, x_max),
+                     domain_max=x_max)
+
+
+def save_soe_table(path, soe: SOEApprox) -> None:
+    rows = ["re_w,im_w,re_s,im_s"]
+    rows += [f"{a.real:.17g},{a.imag:.17g},{b.real:.17g},{b.imag:.17g}"
+             for a, b in zip(soe.w, soe.s)]
+    with open(path, "w") as fh:
+        fh.write("\n".join(rows) + "\n")
+
+
+def is_conjugate_paired(soe: SOEApprox) -> bool:
+    """True when term M-1-l is bitwise the conjugate of term l for every l."""
+    w = np.asarray(soe.w, dtype=np.complex128)
+    s = np.asarray(soe.s, dtype=np.complex128)
+    if len(w) % 2:
+        return False
+    return bool(np.array_equal(w[::-1], np.conj(w)) and np.array_equal(s[::-1], np.conj(s)))
+
+
+def erf_soe(soe: SOEApprox, alpha: float, z):
+    """(2/sqrt(pi)) Re sum (w_l/s_l)(1 - exp(-alpha s_l z)) (reference soe.py:236-240)."""
+    e = np.exp(-np.multiply.outer(alpha * np.asarray(z, dtype=np.float64), soe.s))
+    return (2.0 / SQRT_PI) * np.real((1.0 - e) @ (soe.w / soe.s))
+
+
+def erfc_soe(soe: SOEApprox, x):
+    """(2/sqrt(pi)) Re sum (w_l/s_l) exp(-s_l x) (reference soe.py:243-253)."""
+    e = np.exp(-np.multiply.outer(np.asarray(x, dtype=np.float64), soe.s))
+    return (2.0 / SQRT_PI) * np.real(e @ (soe.w / soe.s))

@@ -1,0 +1,204 @@
+"""Generate golden fixtures by running the REAL reference package (in the build container).
+
+The reference (``/root/reference/pkg/src/slabewald``) is pure Python + numba and
+cannot travel to the GPU box, so its outputs on our seeded workloads are frozen
+here as small ``.npz`` fixtures.  Usage (build container only)::
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [names...]
+
+Inputs are regenerated from ``paper_2403_01521_b200.configs.make_workload`` (a
+sha256 of positions/charges is stored so a test can prove the regeneration is
+bit-identical).  Random-batch k-sets are drawn ONCE from the reference
+``ModeSampler`` and injected into ``rb_energy_forces`` through a stub whose
+``batch(P)`` returns them (``rbse2d.py:288`` only calls ``sampler.batch(P)``).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import importlib.util
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src"
+
+FULL_LIMIT = 20_000       # store full force / perm arrays up to this N
+N_SAMPLE = 4096           # otherwise a fixed random subset of particles
+
+
+def _load_pkg_module(name):
+    """Import one host module of our package without triggering its __init__
+    (which loads the CUDA library)."""
+    pkg = "paper_2403_01521_b200"
+    if pkg not in sys.modules:
+        spec = importlib.util.spec_from_file_location(
+            pkg, os.path.join(REPO, pkg, "__init__.py"),
+            submodule_search_locations=[os.path.join(REPO, pkg)])
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[pkg] = mod  # bare namespace, __init__ not executed
+    full = f"{pkg}.{name}"
+    spec = importlib.util.spec_from_file_location(full, os.path.join(REPO, pkg, f"{name}.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[full] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+class StubSampler:
+    def __init__(self, modes):
+        self.modes = modes
+
+    def batch(self, P):
+        assert P == self.modes.shape[0]
+        return self.modes
+
+
+def ref_modules():
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import slabewald  # noqa: F401
+    from slabewald import core, ewald2d, rbse2d, soe, soewald2d
+    return core, ewald2d, rbse2d, soe, soewald2d
+
+
+def golden_workload(name: str) -> dict:
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    configs = _load_pkg_module("core") and _load_pkg_module("configs")
+    wl = configs.make_workload(name)
+    b = wl.box
+    box = core.BoxGeometry(b.lx, b.ly, b.lz, b.sigma_top, b.sigma_bot)
+    sysm = core.make_system(wl.system.charge, wl.system.mass, wl.system.pos, box=box)
+    assert np.array_equal(sysm.pos, wl.system.pos)
+    params = core.make_ewald_params(wl.alpha, wl.s, box)
+    soe = rsoe.build_soe_contour(wl.m)
+    out = dict(name=name, n=wl.n, alpha=wl.alpha, s=wl.s, m=wl.m,
+               box=np.array([b.lx, b.ly, b.lz, b.sigma_top, b.sigma_bot]),
+               pos_sha=sha(wl.system.pos), charge_sha=sha(wl.system.charge),
+               soe_w=soe.w, soe_s=soe.s)
+    t0 = time.perf_counter()
+    if wl.P is None:
+        bd, forces = soewald2d.soe_energy_forces(sysm, box, params, soe)
+        out["modes"] = params.kmodes
+        out["P"] = 0
+    else:
+        sampler = rbse2d.ModeSampler(wl.alpha, box, seed=wl.seed)
+        modes = sampler.batch(wl.P)
+        H = rbse2d.normalization_H(wl.alpha, box)
+        c_q = rbse2d.charge_term_sum(wl.alpha, box, float(np.sum(sysm.charge ** 2)))
+        bd, forces = rbse2d.rb_energy_forces(sysm, box, params, soe, StubSampler(modes),
+                                             wl.P, H=H, c_q=c_q)
+        out.update(modes=modes, P=wl.P, H=H, c_q=c_q)
+    out["seconds"] = time.perf_counter() - t0
+    u_s, f_s = ewald2d.short_range_energy_forces(sysm, box, wl.alpha, params.r_c)
+    perm = core.sort_by_z(sysm, box.lz)
+    for k in ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps"):
+        out[k] = getattr(bd, k)
+    out["total"] = bd.total
+    out["u_s_alone"] = u_s
+    out["fmax"] = float(np.max(np.abs(forces)))
+    out["fsum"] = forces.sum(axis=0)
+    out["fabs"] = np.abs(forces).sum(axis=0)
+    out["perm_sha"] = sha(perm.astype(np.int64))
+    if wl.n <= FULL_LIMIT:
+        out["forces"] = forces
+        out["f_short"] = f_s
+        out["perm"] = perm.astype(np.int64)
+    else:
+        idx = np.sort(np.random.default_rng(12345).choice(wl.n, N_SAMPLE, replace=False))
+        out["sample_idx"] = idx
+        out["forces"] = forces[idx]
+        out["f_short"] = f_s[idx]
+        out["perm_head"] = perm[:N_SAMPLE].astype(np.int64)
+    return out
+
+
+def golden_units() -> dict:
+    """Small known-answer vectors: sort edge cases, recursion, sampler, H / C_Q."""
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    out = {}
+    rng = np.random.default_rng(2024)
+    cases = {
+        "sort_small": np.array([3.0, 1.0, 2.0]),
+        "sort_ties": np.array([1.0, 0.25, 1.0, 0.25, 1.0]),
+        "sort_negzero": np.array([0.0, -0.0, 0.5, -0.0, 0.0, 2.0, 2.0]),
+        "sort_random": rng.random(10_000) * 6.0,
+        "sort_clustered": np.round(rng.random(5000) * 7.0, 2),
+        "sort_reversed": np.linspace(5.0, 0.0, 3001),
+        "sort_top": np.array([4.0, 0.0, 4.0, 2.0, 4.0]),
+    }
+    for k, z in cases.items():
+        n = len(z)
+        lz = float(max(z.max(), 1.0))
+        pos = np.column_stack([np.zeros(n), np.zeros(n), z])
+        sysm = core.make_system(np.ones(n), np.ones(n), pos)
+        out[k + "_z"] = z
+        out[k + "_lz"] = lz
+        out[k + "_perm"] = core.sort_by_z(sysm, lz).astype(np.int64)
+    # recursive_pair_sum known answers
+    n = 64
+    q = rng.choice([-1.0, 1.0], size=n)
+    th = rng.uniform(-np.pi, np.pi, size=n)
+    z = np.sort(rng.uniform(0.0, 8.0, size=n))
+    for j, beta in enumerate([0.3 + 0.7j, 1.1 + 0.0j, 0.05 - 2.0j]):
+        out[f"rps_{j}_beta"] = np.array(beta)
+        out[f"rps_{j}_out"] = soewald2d.recursive_pair_sum(q, th, z, beta)
+    out["rps_q"], out["rps_theta"], out["rps_z"] = q, th, z
+    # H, C_Q over a spread of boxes
+    hv = []
+    for a, lx, ly in [(0.3, 100.0, 100.0), (0.464, 58.48, 58.48), (0.8, 10.0, 13.0),
+                      (0.05, 100.0, 100.0), (0.5, 20.0, 20.0)]:
+        box = core.BoxGeometry(lx, ly, 10.0)
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            hv.append([a, lx, ly, rbse2d.normalization_H(a, box),
+                       rbse2d.charge_term_sum(a, box, 50.0)])
+    out["H_cq_table"] = np.array(hv)
+    # reference sampler draws (statistical comparison only: different RNG stream)
+    box = core.BoxGeometry(100.0, 100.0, 10.0)
+    smp = rbse2d.ModeSampler(0.3, box, seed=11)
+    out["sampler_idx_a03_L100_seed11"] = smp.batch_indices(20000)
+    out["sampler_acc_a03_L100_seed11"] = smp.acceptance_rate
+    # single-mode energies on a small slab (fourier_mode_energy_soe, soe8)
+    box = core.BoxGeometry(20.0, 20.0, 10.0)
+    rng2 = np.random.default_rng(21)
+    posm = rng2.uniform([0.0, 0.0, 0.5], [20.0, 20.0, 9.5], size=(20, 3))
+    qm = np.array([1.0, -1.0] * 10)
+    sysm = core.make_system(qm, np.ones(20), posm, box=box)
+    params = core.make_ewald_params(0.5, 3.0, box)
+    soe8 = rsoe.build_soe_contour(8)
+    out["mode_pos"], out["mode_q"] = posm, qm
+    out["mode_energies"] = np.array([soewald2d.fourier_mode_energy_soe(sysm, box, params, soe8, i)
+                                     for i in range(params.kmodes.shape[0])])
+    out["mode_zero"] = soewald2d.zero_mode_energy_soe(sysm, box, 0.5, soe8)
+    bd, f = soewald2d.soe_energy_forces(sysm, box, params, soe8)
+    out["mode_total"] = bd.total
+    out["mode_forces"] = f
+    out["mode_forces_soe"] = soewald2d.forces_soe(sysm, box, params, soe8)
+    return out
+
+
+def main(argv):
+    names = argv or ["units", "cfg1", "cfg2", "small_600", "small_2000", "cfg5_1e4",
+                     "cfg3", "cfg5_1e5", "cfg4", "cfg5_1e6"]
+    for name in names:
+        t0 = time.perf_counter()
+        data = golden_units() if name == "units" else golden_workload(name)
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **{k: np.asarray(v) for k, v in data.items()})
+        print(f"{name}: wrote {path} ({os.path.getsize(path)/1e3:.0f} kB) "
+              f"in {time.perf_counter() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
