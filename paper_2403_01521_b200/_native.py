@@ -95,6 +95,7 @@ def load():
                                       vp, vp]
     lib.slab_evaluate.argtypes = [vp, ctypes.POINTER(SlabEvalArgs), vp]
     lib.slab_recursive_pair_sum.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, vp, vp]
+
     for name in EXPORTED:
         if name not in ("slab_last_error", "slab_version"):
             getattr(lib, name).restype = cint

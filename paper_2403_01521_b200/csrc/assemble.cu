@@ -37,15 +37,14 @@ __global__ void assemble_forces_kernel(int64_t n, const int32_t* __restrict__ pe
   forces[3 * i + 2] = sz + fz + (-2.0 * kPi * charge[i]) * plane;
 }
 
-__global__ void __launch_bounds__(1024) assemble_energy_kernel(
+constexpr int kEBlocks = 296;  // partial sums for Q = sum q^2 and u_ps
+
+__global__ void __launch_bounds__(256) energy_partials_kernel(
     int64_t n, const double* __restrict__ charge, const double* __restrict__ pos, double lz,
-    double sigma_top, double sigma_bot, double alpha, double area, double charge_const,
-    const double* __restrict__ u_s, const double* __restrict__ u_sweep,
-    const double* __restrict__ u_pair, const int* __restrict__ status,
-    double* __restrict__ energy) {
-  __shared__ double r0[1024], r1[1024];
+    double sigma_top, double sigma_bot, double* __restrict__ part) {
+  __shared__ double r0[256], r1[256];
   double q2 = 0.0, ups = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)kEBlocks * 256) {
     const double q = charge[i], z = pos[3 * i + 2];
     q2 = fma(q, q, q2);
     ups += q * (-2.0 * kPi * (sigma_top * (lz - z) + sigma_bot * z));
@@ -53,7 +52,29 @@ __global__ void __launch_bounds__(1024) assemble_energy_kernel(
   r0[threadIdx.x] = q2;
   r1[threadIdx.x] = ups;
   __syncthreads();
-  for (int s = 512; s > 0; s >>= 1) {
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      r0[threadIdx.x] += r0[threadIdx.x + s];
+      r1[threadIdx.x] += r1[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = r0[0];
+    part[kEBlocks + blockIdx.x] = r1[0];
+  }
+}
+
+__global__ void __launch_bounds__(512) assemble_energy_kernel(
+    int64_t n, const double* __restrict__ part, double alpha, double area, double charge_const,
+    const double* __restrict__ u_s, const double* __restrict__ u_sweep,
+    const double* __restrict__ u_pair, const int* __restrict__ status,
+    double* __restrict__ energy) {
+  __shared__ double r0[512], r1[512];
+  r0[threadIdx.x] = threadIdx.x < kEBlocks ? part[threadIdx.x] : 0.0;
+  r1[threadIdx.x] = threadIdx.x < kEBlocks ? part[kEBlocks + threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int s = 256; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
       r0[threadIdx.x] += r0[threadIdx.x + s];
       r1[threadIdx.x] += r1[threadIdx.x + s];
@@ -89,10 +110,13 @@ cudaError_t assemble_energy(int64_t n, const double* charge, const double* pos, 
                             double sigma_top, double sigma_bot, double alpha, double area,
                             double charge_const, const double* u_s, const double* u_sweep,
                             const double* u_pair, const int* status, double* energy,
-                            cudaStream_t st) {
-  assemble_energy_kernel<<<1, 1024, 0, st>>>(n, charge, pos, lz, sigma_top, sigma_bot, alpha,
-                                             area, charge_const, u_s, u_sweep, u_pair, status,
-                                             energy);
+                            double* energy_scratch, cudaStream_t st) {
+  // the 2*kEBlocks partials live in energy[8..] (callers pass >= 8 + 2*kEBlocks doubles
+  // of scratch through `energy_scratch`)
+  energy_partials_kernel<<<kEBlocks, 256, 0, st>>>(n, charge, pos, lz, sigma_top, sigma_bot,
+                                                    energy_scratch);
+  assemble_energy_kernel<<<1, 512, 0, st>>>(n, energy_scratch, alpha, area, charge_const, u_s,
+                                            u_sweep, u_pair, status, energy);
   return cudaGetLastError();
 }
 

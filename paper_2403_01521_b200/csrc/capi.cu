@@ -55,7 +55,7 @@ size_t pad(size_t b) { return ((b ? b : 1) + 255) & ~(size_t)255; }
 
 int ensure_arena(SlabCtx* c, size_t bytes) {
   if (c->small == nullptr) {
-    CK(cudaMalloc(&c->small, 64 * sizeof(double)));
+    CK(cudaMalloc(&c->small, 1024 * sizeof(double)));
     CK(cudaMalloc(&c->status, 16 * sizeof(int)));
   }
   if (bytes <= c->arena_bytes) return SLAB_OK;
@@ -378,7 +378,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   }
   CK(slab::assemble_energy(n, a->d_charge, a->d_pos, box.lz, box.sigma_top, box.sigma_bot,
                            a->alpha, area, a->charge_const, u_s, u_sweep, u_pair, ctx->status,
-                           a->d_energy, st));
+                           a->d_energy, ctx->small + 64, st));
   return SLAB_OK;
 }
 

@@ -220,16 +220,31 @@ __global__ void __launch_bounds__(256) fourier_aggregate_kernel(
 // ---------------------------------------------------------------------------
 // phase 2: carry scan over chunks (in place: aggregates -> carried-in states)
 // ---------------------------------------------------------------------------
-constexpr int kCarryBatch = 16;
+// One warp per chain (item, component): lane l composes a contiguous block of
+// chunks, a shuffle scan composes the lane blocks, then each lane rewrites its
+// block with the exclusive carries.  Affine map per chunk: T -> D T + X.
+__device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, int l, int mh,
+                                          double k, const double2* __restrict__ Df,
+                                          const double2* __restrict__ Db,
+                                          const double* __restrict__ zbound) {
+  if (isg) {
+    const double dz = fwd ? (c > 0 ? zbound[c] - zbound[c - 1] : 0.0)
+                          : (c + 1 < nch ? zbound[nch + c + 1] - zbound[nch + c] : 0.0);
+    return C2{exp(-k * dz), 0.0};
+  }
+  const double2 d = fwd ? Df[(size_t)c * mh + l] : Db[(size_t)c * mh + l];
+  return C2{d.x, d.y};
+}
 
 __global__ void __launch_bounds__(128) fourier_carry_kernel(
     double2* __restrict__ carry, int nch, int P, int mh, const double* __restrict__ modetab,
     const double2* __restrict__ Df, const double2* __restrict__ Db,
     const double* __restrict__ zbound) {
   const int nitems = 2 * P, nc = ncomp_of(mh);
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nitems * nc) return;
-  const int item = idx % nitems, comp = idx / nitems;
+  const int chain = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (chain >= nitems * nc) return;  // whole warp exits together
+  const int item = chain % nitems, comp = chain / nitems;
   const bool fwd = item < P;
   const int t = fwd ? item : item - P;
   const bool isg = comp == 2 * mh;
@@ -237,34 +252,53 @@ __global__ void __launch_bounds__(128) fourier_carry_kernel(
   const double k = modetab[(size_t)t * mode_stride(mh) + 2];
   const size_t cstride = (size_t)nc * nitems;
   double2* base = carry + (size_t)comp * nitems + item;
-  C2 T{0.0, 0.0};
-  for (int b0 = 0; b0 < nch; b0 += kCarryBatch) {
-    double2 X[kCarryBatch];
-    C2 D[kCarryBatch];
+  const int per = (nch + 31) / 32;
+  const int s0 = lane * per, s1 = min(nch, s0 + per);
+  // pass 1: compose this lane's block
+  C2 D{1.0, 0.0}, X{0.0, 0.0};
+  for (int s = s0; s < s1; ++s) {
+    const int c = fwd ? s : nch - 1 - s;
+    const double2 x = base[(size_t)c * cstride];
+    const C2 d = carry_decay(isg, fwd, c, nch, l, mh, k, Df, Db, zbound);
+    const C2 nx = cmul(d, X);
+    X = C2{nx.re + x.x, nx.im + x.y};
+    D = cmul(d, D);
+  }
+  // inclusive scan of lane maps (earlier lanes applied first)
 #pragma unroll
-    for (int j = 0; j < kCarryBatch; ++j) {
-      const int s = b0 + j;
-      if (s < nch) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const double dr = __shfl_up_sync(0xffffffffu, D.re, o), di = __shfl_up_sync(0xffffffffu, D.im, o);
+    const double xr = __shfl_up_sync(0xffffffffu, X.re, o), xi = __shfl_up_sync(0xffffffffu, X.im, o);
+    if (lane >= o) {
+      const C2 nx = cmul(D, C2{xr, xi});
+      X = C2{nx.re + X.re, nx.im + X.im};
+      D = cmul(D, C2{dr, di});
+    }
+  }
+  C2 T{__shfl_up_sync(0xffffffffu, X.re, 1), __shfl_up_sync(0xffffffffu, X.im, 1)};
+  if (lane == 0) T = C2{0.0, 0.0};
+  // pass 2: rewrite the block with exclusive carries (loads batched ahead of stores)
+  constexpr int B = 8;
+  for (int sb = s0; sb < s1; sb += B) {
+    double2 xs[B];
+    C2 ds[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int s = sb + j;
+      if (s < s1) {
         const int c = fwd ? s : nch - 1 - s;
-        X[j] = base[(size_t)c * cstride];
-        if (isg) {
-          double dz = fwd ? (c > 0 ? zbound[c] - zbound[c - 1] : 0.0)
-                          : (c + 1 < nch ? zbound[nch + c + 1] - zbound[nch + c] : 0.0);
-          D[j] = C2{exp(-k * dz), 0.0};
-        } else {
-          const double2 d = fwd ? Df[(size_t)c * mh + l] : Db[(size_t)c * mh + l];
-          D[j] = C2{d.x, d.y};
-        }
+        xs[j] = base[(size_t)c * cstride];
+        ds[j] = carry_decay(isg, fwd, c, nch, l, mh, k, Df, Db, zbound);
       }
     }
 #pragma unroll
-    for (int j = 0; j < kCarryBatch; ++j) {
-      const int s = b0 + j;
-      if (s < nch) {
+    for (int j = 0; j < B; ++j) {
+      const int s = sb + j;
+      if (s < s1) {
         const int c = fwd ? s : nch - 1 - s;
         base[(size_t)c * cstride] = make_double2(T.re, T.im);
-        C2 nt = cmul(D[j], T);
-        T = C2{nt.re + X[j].x, nt.im + X[j].y};
+        const C2 nt = cmul(ds[j], T);
+        T = C2{nt.re + xs[j].x, nt.im + xs[j].y};
       }
     }
   }
@@ -430,28 +464,34 @@ __global__ void __launch_bounds__(256, 1) fourier_sweep_kernel(
   }
 }
 
-// per-mode sums over chunks (fixed order), then Kahan over modes in mode order
-// exactly like soewald2d.py:204-207
-__global__ void fourier_energy_kernel(const double* __restrict__ epart, int nch, int P, int mh,
-                                      const double* __restrict__ modetab,
-                                      double* __restrict__ out) {
-  extern __shared__ double se[];
-  for (int t = threadIdx.x; t < P; t += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nch; ++c) s += epart[(size_t)c * P + t];
-    se[t] = modetab[(size_t)t * mode_stride(mh) + 3] * s;
-  }
+// per-mode sums over chunks (one block per mode, fixed-order tree), then Kahan
+// over modes in mode order exactly like soewald2d.py:204-207
+__global__ void __launch_bounds__(256) fourier_mode_energy_kernel(
+    const double* __restrict__ epart, int nch, int P, int mh, const double* __restrict__ modetab,
+    double* __restrict__ se) {
+  __shared__ double red[256];
+  const int t = blockIdx.x;
+  double s = 0.0;
+  for (int c = threadIdx.x; c < nch; c += 256) s += epart[(size_t)c * P + t];
+  red[threadIdx.x] = s;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double u = 0.0, comp = 0.0;
-    for (int t = 0; t < P; ++t) {
-      double y = se[t] - comp;
-      double tt = u + y;
-      comp = (tt - u) - y;
-      u = tt;
-    }
-    out[0] = u;
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) se[t] = modetab[(size_t)t * mode_stride(mh) + 3] * red[0];
+}
+
+__global__ void kahan_modes_kernel(const double* __restrict__ se, int P, double* __restrict__ out) {
+  if (threadIdx.x || blockIdx.x) return;
+  double u = 0.0, comp = 0.0;
+  for (int t = 0; t < P; ++t) {
+    const double y = se[t] - comp;
+    const double tt = u + y;
+    comp = (tt - u) - y;
+    u = tt;
+  }
+  out[0] = u;
 }
 
 // forces_sorted (+)= sum over item groups (fixed order)
@@ -504,7 +544,7 @@ size_t fourier_work_doubles(const FourierPlan& p) {
   d += 2 * (size_t)p.nch * ncomp_of(p.mh) * nitems;  // carry (double2)
   d += 2 * 2 * (size_t)p.nch * p.mh;                 // Df, Db (double2)
   d += 2 * (size_t)p.nch;                            // zbound
-  d += (size_t)p.nch * p.P;                          // epart
+  d += (size_t)p.nch * p.P + p.P;                    // epart + per-mode sums
   d += (size_t)p.ngroups * p.n * 3;                  // fpart
   return d + 64;
 }
@@ -522,7 +562,7 @@ void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w) {
   w.zbound = q;
   q += 2 * (size_t)p.nch;
   w.epart = q;
-  q += (size_t)p.nch * p.P;
+  q += (size_t)p.nch * p.P + p.P;
   w.fpart = q;
 }
 
@@ -553,7 +593,7 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
   else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {
-    const int nthr = 2 * p.P * ncomp_of(MH);
+    const int nthr = 32 * 2 * p.P * ncomp_of(MH);
     fourier_carry_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(
         w.carry, p.nch, p.P, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH, w.zbound);
   }
@@ -591,8 +631,9 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
-  size_t sm = sizeof(double) * (size_t)p.P;
-  fourier_energy_kernel<<<1, 256, sm, st>>>(w.epart, p.nch, p.P, p.mh, w.modetab, energy_out);
+  double* se = w.epart + (size_t)p.nch * p.P;  // P scratch doubles after the partials
+  fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.nch, p.P, p.mh, w.modetab, se);
+  kahan_modes_kernel<<<1, 1, 0, st>>>(se, p.P, energy_out);
   if (want_forces) {
     const int64_t n3 = p.n * 3;
     fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(w.fpart, p.ngroups,

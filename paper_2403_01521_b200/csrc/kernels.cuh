@@ -112,7 +112,7 @@ cudaError_t assemble_energy(int64_t n, const double* charge, const double* pos, 
                             double sigma_top, double sigma_bot, double alpha, double area,
                             double charge_const, const double* u_s, const double* u_sweep,
                             const double* u_pair, const int* status, double* energy,
-                            cudaStream_t st);
+                            double* energy_scratch, cudaStream_t st);
 
 // ---------------------------------------------------------------- sampler.cu
 cudaError_t sample_modes(int64_t* state, uint64_t seed, double alpha, double lx, double ly,

@@ -8,10 +8,15 @@
 // cells of edge >= r_c, all pairs when ncx < 3 or ncy < 3.
 //
 // Device layout: stable radix sort of the cell ids (deterministic order inside
-// each cell) -> cell-sorted SoA + cell_start by binary search.  One CTA per home
-// cell; each thread owns home particles and sums over the full 27-cell shell
-// (both orders of every pair) so each force is accumulated by exactly one
-// thread: deterministic, no atomics.  u_s = 1/2 of the full-shell sum.
+// each cell) -> cell-sorted SoA (fp64 + an fp32 copy) + cell_start.  One thread
+// per home particle (cell-sorted, so a warp walks the same 27 cells and every
+// candidate load is a broadcast).  Candidates are screened with a conservative
+// fp32 distance test and the survivors queued per thread in shared memory; when
+// any lane's queue fills, the warp drains all queues through the exact fp64
+// pair kernel (so the erfc/exp work runs on full warps instead of the ~15% of
+// lanes whose candidate happens to be in range).  Each force is accumulated by
+// exactly one thread over the full shell: deterministic, no atomics;
+// u_s = 1/2 of the full-shell sum.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -21,15 +26,18 @@ struct PairAcc {
   double fx, fy, fz, e;
 };
 
+// exact reference pair term (ewald2d.py:199-230).  The minimum image uses the
+// reference's rint(dx/lx); dx * (1/lx) only differs from dx/lx at exact
+// half-box ties, i.e. |dx| = L/2 >= r_c, outside the cutoff.
 __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi, double qi,
                                                 double xj, double yj, double zj, double qj,
-                                                double lx, double ly, double alpha, double rc2,
-                                                double c, PairAcc& acc, int& flag) {
-  // rounding exactly as the numba reference (no FMA contraction in the geometry)
+                                                double lx, double ly, double ilx, double ily,
+                                                double alpha, double rc2, double c, PairAcc& acc,
+                                                int& flag) {
   double dx = __dsub_rn(xi, xj), dy = __dsub_rn(yi, yj);
   const double dz = __dsub_rn(zi, zj);
-  dx = __dsub_rn(dx, __dmul_rn(lx, rint(__ddiv_rn(dx, lx))));
-  dy = __dsub_rn(dy, __dmul_rn(ly, rint(__ddiv_rn(dy, ly))));
+  dx = __dsub_rn(dx, __dmul_rn(lx, rint(__dmul_rn(dx, ilx))));
+  dy = __dsub_rn(dy, __dmul_rn(ly, rint(__dmul_rn(dy, ily))));
   const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
   if (d2 > rc2) return;
   if (d2 < 1e-24) {
@@ -38,9 +46,12 @@ __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi,
   }
   const double d = sqrt(d2);
   const double qq = qi * qj;
-  const double e = erfc(alpha * d);
-  acc.e += qq * e / d;
-  const double fmag = qq * (e / (d2 * d) + c * exp(-alpha * alpha * d2) / d2);
+  const double x = alpha * d;
+  const double g = exp(-x * x);   // shared by erfc and the force Gaussian
+  const double e = erfcx(x) * g;  // erfc(x) without a second exp
+  const double inv_d = 1.0 / d;
+  acc.e = fma(qq * e, inv_d, acc.e);
+  const double fmag = qq * (e * inv_d + c * g) * (inv_d * inv_d);
   acc.fx = fma(fmag, dx, acc.fx);
   acc.fy = fma(fmag, dy, acc.fy);
   acc.fz = fma(fmag, dz, acc.fz);
@@ -77,59 +88,89 @@ __global__ void cell_start_kernel(const uint32_t* __restrict__ skey, int64_t n, 
 
 __global__ void cell_gather_kernel(const double* __restrict__ pos, const double* __restrict__ q,
                                    const int32_t* __restrict__ order, int64_t n,
-                                   double4* __restrict__ cp) {
+                                   double4* __restrict__ cp, float4* __restrict__ cpf) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   int64_t i = order[a];
-  cp[a] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], q[i]);
+  const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+  cp[a] = make_double4(x, y, z, q[i]);
+  cpf[a] = make_float4((float)x, (float)y, (float)z, 0.0f);
 }
 
-constexpr int kCellThreads = 64;
+constexpr int kSRThreads = 128;
+constexpr int kQ = 32;  // per-thread queue of screened candidates
 
-__global__ void __launch_bounds__(kCellThreads) cell_pair_kernel(
-    const double4* __restrict__ cp, const int32_t* __restrict__ order,
-    const int32_t* __restrict__ start, int ncx, int ncy, int ncz, double lx, double ly,
-    double alpha, double rc2, double* __restrict__ forces, double* __restrict__ eblk,
+__global__ void __launch_bounds__(kSRThreads) short_cells_kernel(
+    const double4* __restrict__ cp, const float4* __restrict__ cpf,
+    const int32_t* __restrict__ order, const uint32_t* __restrict__ skey,
+    const int32_t* __restrict__ start, int64_t n, int ncx, int ncy, int ncz, double lx, double ly,
+    double alpha, double rc2, float rc2f, double* __restrict__ forces, double* __restrict__ eblk,
     int* __restrict__ status) {
-  const int cid = blockIdx.x;
-  const int cz = cid % ncz, cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
-  const int h0 = start[cid], h1 = start[cid + 1];
+  __shared__ int32_t queue[kQ][kSRThreads];
+  const int tid = threadIdx.x;
+  const int64_t a = blockIdx.x * (int64_t)kSRThreads + tid;
+  const bool active = a < n;
   const double c = kTwoOverSqrtPi * alpha;
-  double esum = 0.0;
-  int flag = 0;
-  for (int ii = h0 + threadIdx.x; ii < h1; ii += kCellThreads) {
-    const double4 pi = cp[ii];
-    PairAcc acc{0.0, 0.0, 0.0, 0.0};
-    for (int off = 0; off < 27; ++off) {
-      const int dxc = off / 9 - 1, dyc = (off / 3) % 3 - 1, dzc = off % 3 - 1;
-      const int nz = cz + dzc;
-      if (nz < 0 || nz >= ncz) continue;
-      const int nx = (cx + dxc + ncx) % ncx, ny = (cy + dyc + ncy) % ncy;
-      const int nid = (nx * ncy + ny) * ncz + nz;
-      const int b0 = start[nid], b1 = start[nid + 1];
-      for (int jj = b0; jj < b1; ++jj) {
-        if (jj == ii) continue;
-        const double4 pj = cp[jj];
-        pair_accumulate(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, alpha, rc2, c,
-                        acc, flag);
+  const double ilx = 1.0 / lx, ily = 1.0 / ly;
+  const float lxf = (float)lx, lyf = (float)ly, ilxf = 1.0f / lxf, ilyf = 1.0f / lyf;
+  const float4 pf = active ? cpf[a] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const double4 pd = active ? cp[a] : make_double4(0.0, 0.0, 0.0, 0.0);
+  const int cid = active ? (int)skey[a] : 0;
+  const int cz = cid % ncz, cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
+  PairAcc acc{0.0, 0.0, 0.0, 0.0};
+  int flag = 0, cnt = 0;
+  auto drain = [&]() {
+    const int m = __reduce_max_sync(0xffffffffu, cnt);
+    for (int k = 0; k < m; ++k) {
+      if (k < cnt) {
+        const double4 pj = cp[queue[k][tid]];
+        pair_accumulate(pd.x, pd.y, pd.z, pd.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
+                        rc2, c, acc, flag);
       }
     }
-    const int64_t i = order[ii];
+    cnt = 0;
+  };
+  for (int off = 0; off < 27; ++off) {
+    const int dxc = off / 9 - 1, dyc = (off / 3) % 3 - 1, dzc = off % 3 - 1;
+    const int nz = cz + dzc;
+    int b0 = 0, len = 0;
+    if (active && nz >= 0 && nz < ncz) {
+      const int nx = (cx + dxc + ncx) % ncx, ny = (cy + dyc + ncy) % ncy;
+      const int nid = (nx * ncy + ny) * ncz + nz;
+      b0 = start[nid];
+      len = start[nid + 1] - b0;
+    }
+    const int maxlen = __reduce_max_sync(0xffffffffu, len);
+    for (int it = 0; it < maxlen; ++it) {
+      if (it < len) {
+        const int jj = b0 + it;
+        const float4 pj = cpf[jj];
+        float dx = pf.x - pj.x, dy = pf.y - pj.y;
+        const float dz = pf.z - pj.z;
+        dx -= lxf * rintf(dx * ilxf);
+        dy -= lyf * rintf(dy * ilyf);
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        if (d2 <= rc2f && jj != a) queue[cnt++][tid] = jj;
+      }
+      if (__any_sync(0xffffffffu, cnt == kQ)) drain();
+    }
+  }
+  drain();
+  if (active) {
+    const int64_t i = order[a];
     forces[3 * i + 0] = acc.fx;
     forces[3 * i + 1] = acc.fy;
     forces[3 * i + 2] = acc.fz;
-    esum += acc.e;
   }
   if (flag) atomicOr(status, SLAB_STATUS_COINCIDENT_DEV);
-  // fixed-order block reduction
-  __shared__ double red[kCellThreads];
-  red[threadIdx.x] = esum;
+  __shared__ double red[kSRThreads];
+  red[tid] = acc.e;
   __syncthreads();
-  for (int s = kCellThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+  for (int s = kSRThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) red[tid] += red[tid + s];
     __syncthreads();
   }
-  if (threadIdx.x == 0) eblk[cid] = red[0];
+  if (tid == 0) eblk[blockIdx.x] = red[0];
 }
 
 // all pairs (ncx < 3 or ncy < 3): grid (i tiles, j splits)
@@ -142,6 +183,7 @@ __global__ void __launch_bounds__(128) brute_pair_kernel(
   const int64_t per = (n + jsplit - 1) / jsplit;
   const int64_t j0 = js * per, j1 = j0 + per < n ? j0 + per : n;
   const double c = kTwoOverSqrtPi * alpha;
+  const double ilx = 1.0 / lx, ily = 1.0 / ly;
   PairAcc acc{0.0, 0.0, 0.0, 0.0};
   int flag = 0;
   if (i < n) {
@@ -149,7 +191,7 @@ __global__ void __launch_bounds__(128) brute_pair_kernel(
     for (int64_t j = j0; j < j1; ++j) {
       if (j == i) continue;
       pair_accumulate(xi, yi, zi, qi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], q[j], lx, ly,
-                      alpha, rc2, c, acc, flag);
+                      ilx, ily, alpha, rc2, c, acc, flag);
     }
     double* f = fbuf + ((size_t)js * n + i) * 3;
     f[0] = acc.fx;
@@ -207,7 +249,8 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc) {
   const int64_t nbx = (n + 127) / 128;
   int js = (int)(592 / (nbx > 0 ? nbx : 1));
   p.jsplit = p.brute ? (js < 1 ? 1 : (js > 64 ? 64 : js)) : 1;
-  p.nblk = p.brute ? (int64_t)p.jsplit * (nbx > 0 ? nbx : 1) : p.ncell;
+  p.nblk = p.brute ? (int64_t)p.jsplit * (nbx > 0 ? nbx : 1)
+                   : (n + kSRThreads - 1) / kSRThreads;
   return p;
 }
 
@@ -215,15 +258,14 @@ static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 size_t short_work_bytes(const ShortPlan& p) {
   const size_t n = (size_t)(p.n > 0 ? p.n : 1);
-  size_t b = 0;
-  b += align256(sizeof(double) * p.nblk);  // eblk
+  size_t b = align256(sizeof(double) * (p.nblk > 0 ? p.nblk : 1));  // eblk
   if (p.brute) {
     b += align256(sizeof(double) * 3 * n * p.jsplit);
   } else {
     b += 2 * align256(sizeof(uint32_t) * n) + 2 * align256(sizeof(int32_t) * n);
     b += align256(sizeof(int32_t) * radix_hist_entries(p.n));
     b += align256(sizeof(int32_t) * (p.ncell + 1));
-    b += align256(sizeof(double4) * n);
+    b += align256(sizeof(double4) * n) + align256(sizeof(float4) * n);
   }
   return b + 256;
 }
@@ -262,6 +304,8 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     int32_t* start = reinterpret_cast<int32_t*>(w);
     w += align256(sizeof(int32_t) * (p.ncell + 1));
     double4* cp = reinterpret_cast<double4*>(w);
+    w += align256(sizeof(double4) * n);
+    float4* cpf = reinterpret_cast<float4*>(w);
     cell_index_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, n, lx, ly, lz, p.ncx,
                                                                   p.ncy, p.ncz, k0, v0);
     int bits = 8;
@@ -272,9 +316,14 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     if (e != cudaSuccess) return e;
     cell_start_kernel<<<(unsigned)((p.ncell + 1 + 255) / 256), 256, 0, st>>>(skey, n, p.ncell,
                                                                              start);
-    cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, cp);
-    cell_pair_kernel<<<(unsigned)p.ncell, kCellThreads, 0, st>>>(
-        cp, order, start, p.ncx, p.ncy, p.ncz, lx, ly, alpha, rc2, forces, eblk, status);
+    cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, cp,
+                                                                    cpf);
+    // conservative fp32 screen: positions rounded to fp32 move d2 by < 1e-2 for
+    // |r| <= 1e3; the exact fp64 test is applied to every survivor
+    const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);
+    short_cells_kernel<<<(unsigned)p.nblk, kSRThreads, 0, st>>>(
+        cp, cpf, order, skey, start, n, p.ncx, p.ncy, p.ncz, lx, ly, alpha, rc2, rc2f, forces,
+        eblk, status);
   }
   half_sum_kernel<<<1, 1024, 0, st>>>(eblk, p.nblk, energy_out);
   return cudaGetLastError();

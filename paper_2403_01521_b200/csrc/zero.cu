@@ -11,8 +11,11 @@
 //            + 1/(alpha sqrt pi) sum q_a Re sum w A                    (soewald2d.py:249)
 //   fz_a  += S0 - (2/sqrt pi) Re sum [(w/s + w s/2) A - alpha w B]   (forward, 264-277)
 //   fz_a  -= suffix mirror                                             (backward, 282-295)
-// Same 3-phase chunked scan as the Fourier path, one thread per (chunk, dir);
-// (A, B) compose as the affine pair  A' = D A + X_A,  B' = D (B + dz A) + X_B.
+// Same 3-phase chunked scan as the Fourier path, one thread per (chunk, dir)
+// for phases 1 and 3.  (A, B) compose as the affine map
+//   A' = D A + X_A,  B' = D (B + dz A) + X_B,   D = e^{-b dz},
+// closed under composition as (D, dz, X_A, X_B); phase 2 is a warp-cooperative
+// scan of those maps (one warp per (direction, pair) chain).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -34,7 +37,7 @@ __global__ void zero_aggregate_kernel(const double* __restrict__ zs, const doubl
     const int64_t a = dir == 0 ? a0 + s : a1 - 1 - s;
     const double q = qs[a];
     if (s > 0) {
-      const int64_t ad = dir == 0 ? a : a + 1;           // decay row
+      const int64_t ad = dir == 0 ? a : a + 1;  // decay row
       const double dz = zs[ad] - zs[ad - 1];
 #pragma unroll
       for (int l = 0; l < MH; ++l) {
@@ -58,40 +61,116 @@ __global__ void zero_aggregate_kernel(const double* __restrict__ zs, const doubl
   out[2 * MH] = make_double2(S0, S1);
 }
 
-// in-place: aggregates -> carried-in states.  thread per (dir, pair) + (dir, S)
-template <int MH>
-__global__ void zero_carry_kernel(const double* __restrict__ zs, int64_t n, int R, int nch,
-                                  BVec b, double2* __restrict__ zagg) {
+// zdz[dir*nch + c] = distance from the carried state's z to chunk c's far end;
+// zD[(dir*nch + c)*mh + l] = e^{-b_l zdz}
+__global__ void zero_chunk_decay_kernel(const double* __restrict__ zs, int64_t n, int R, int nch,
+                                        int mh, BVec b, double* __restrict__ zdz,
+                                        double2* __restrict__ zD) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= 2 * (MH + 1)) return;
-  const int dir = e / (MH + 1), l = e % (MH + 1);
-  const size_t rec = 2 * MH + 1;
-  if (l == MH) {  // plain prefix / suffix sums of q and q z
-    double S0 = 0.0, S1 = 0.0;
-    for (int s = 0; s < nch; ++s) {
+  if (e >= 2 * nch * mh) return;
+  const int l = e % mh, dc = e / mh, dir = dc / nch, c = dc % nch;
+  const int64_t a0 = (int64_t)c * R, a1 = a0 + R < n ? a0 + R : n;
+  double dz;
+  if (dir == 0) dz = c > 0 ? zs[a1 - 1] - zs[a0 - 1] : 0.0;
+  else dz = c + 1 < nch ? zs[a1] - zs[a0] : 0.0;
+  if (l == 0) zdz[dc] = dz;
+  const C2 D = cexp_neg(b.re[l] * dz, b.im[l] * dz);
+  zD[e] = make_double2(D.re, D.im);
+}
+
+struct ZMap {
+  C2 D, XA, XB;
+  double dz;
+};
+// apply `first`, then `then`
+__device__ __forceinline__ ZMap zcompose(const ZMap& first, const ZMap& then) {
+  ZMap r;
+  r.D = cmul(then.D, first.D);
+  r.dz = first.dz + then.dz;
+  const C2 xa = cmul(then.D, first.XA);
+  r.XA = C2{xa.re + then.XA.re, xa.im + then.XA.im};
+  const C2 xb = cmul(then.D, C2{fma(then.dz, first.XA.re, first.XB.re),
+                                fma(then.dz, first.XA.im, first.XB.im)});
+  r.XB = C2{xb.re + then.XB.re, xb.im + then.XB.im};
+  return r;
+}
+__device__ __forceinline__ ZMap zshfl_up(const ZMap& m, int o) {
+  ZMap r;
+  r.D = C2{__shfl_up_sync(0xffffffffu, m.D.re, o), __shfl_up_sync(0xffffffffu, m.D.im, o)};
+  r.XA = C2{__shfl_up_sync(0xffffffffu, m.XA.re, o), __shfl_up_sync(0xffffffffu, m.XA.im, o)};
+  r.XB = C2{__shfl_up_sync(0xffffffffu, m.XB.re, o), __shfl_up_sync(0xffffffffu, m.XB.im, o)};
+  r.dz = __shfl_up_sync(0xffffffffu, m.dz, o);
+  return r;
+}
+
+// in place: aggregates -> carried-in states.  One warp per (dir, chain), chain
+// = SOE pair l < mh, or mh for the (S0, S1) prefix sums.
+__global__ void __launch_bounds__(64) zero_carry_kernel(int nch, int mh,
+                                                        const double* __restrict__ zdz,
+                                                        const double2* __restrict__ zD,
+                                                        double2* __restrict__ zagg) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= 2 * (mh + 1)) return;
+  const int dir = w / (mh + 1), l = w % (mh + 1);
+  const size_t rec = 2 * mh + 1;
+  const int per = (nch + 31) / 32;
+  const int s0 = lane * per, s1 = min(nch, s0 + per);
+  if (l == mh) {  // plain prefix (fwd) / suffix (bwd) sums of q and q z
+    double a0 = 0.0, a1 = 0.0;
+    for (int s = s0; s < s1; ++s) {
       const int c = dir == 0 ? s : nch - 1 - s;
-      double2* p = zagg + ((size_t)c * 2 + dir) * rec + 2 * MH;
-      const double2 X = *p;
+      const double2 x = zagg[((size_t)c * 2 + dir) * rec + 2 * mh];
+      a0 += x.x;
+      a1 += x.y;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u0 = __shfl_up_sync(0xffffffffu, a0, o), u1 = __shfl_up_sync(0xffffffffu, a1, o);
+      if (lane >= o) {
+        a0 += u0;
+        a1 += u1;
+      }
+    }
+    double S0 = __shfl_up_sync(0xffffffffu, a0, 1), S1 = __shfl_up_sync(0xffffffffu, a1, 1);
+    if (lane == 0) S0 = S1 = 0.0;
+    for (int s = s0; s < s1; ++s) {
+      const int c = dir == 0 ? s : nch - 1 - s;
+      double2* p = zagg + ((size_t)c * 2 + dir) * rec + 2 * mh;
+      const double2 x = *p;
       *p = make_double2(S0, S1);
-      S0 += X.x;
-      S1 += X.y;
+      S0 += x.x;
+      S1 += x.y;
     }
     return;
   }
-  C2 TA{0.0, 0.0}, TB{0.0, 0.0};
-  for (int s = 0; s < nch; ++s) {
+  ZMap M{C2{1.0, 0.0}, C2{0.0, 0.0}, C2{0.0, 0.0}, 0.0};
+  for (int s = s0; s < s1; ++s) {
+    const int c = dir == 0 ? s : nch - 1 - s;
+    const double2* p = zagg + ((size_t)c * 2 + dir) * rec;
+    const double2 d = zD[((size_t)dir * nch + c) * mh + l];
+    ZMap e{C2{d.x, d.y}, C2{p[l].x, p[l].y}, C2{p[mh + l].x, p[mh + l].y},
+           zdz[(size_t)dir * nch + c]};
+    M = zcompose(M, e);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const ZMap u = zshfl_up(M, o);
+    if (lane >= o) M = zcompose(u, M);
+  }
+  const ZMap prev = zshfl_up(M, 1);
+  C2 TA = lane ? prev.XA : C2{0.0, 0.0};
+  C2 TB = lane ? prev.XB : C2{0.0, 0.0};
+  for (int s = s0; s < s1; ++s) {
     const int c = dir == 0 ? s : nch - 1 - s;
     double2* p = zagg + ((size_t)c * 2 + dir) * rec;
-    const double2 XA = p[l], XB = p[MH + l];
+    const double2 XA = p[l], XB = p[mh + l];
     p[l] = make_double2(TA.re, TA.im);
-    p[MH + l] = make_double2(TB.re, TB.im);
-    const int64_t a0 = (int64_t)c * R, a1 = a0 + R < n ? a0 + R : n;
-    double dz;  // distance from the carried state's z to this chunk's far end
-    if (dir == 0) dz = c > 0 ? zs[a1 - 1] - zs[a0 - 1] : 0.0;
-    else dz = c + 1 < nch ? zs[a1] - zs[a0] : 0.0;
-    const C2 D = cexp_neg(b.re[l] * dz, b.im[l] * dz);
-    C2 nb = cmul(D, C2{fma(dz, TA.re, TB.re), fma(dz, TA.im, TB.im)});
-    C2 na = cmul(D, TA);
+    p[mh + l] = make_double2(TB.re, TB.im);
+    const double2 d = zD[((size_t)dir * nch + c) * mh + l];
+    const double dz = zdz[(size_t)dir * nch + c];
+    const C2 D{d.x, d.y};
+    const C2 nb = cmul(D, C2{fma(dz, TA.re, TB.re), fma(dz, TA.im, TB.im)});
+    const C2 na = cmul(D, TA);
     TA = C2{na.re + XA.x, na.im + XA.y};
     TB = C2{nb.re + XB.x, nb.im + XB.y};
   }
@@ -160,22 +239,31 @@ __global__ void zero_sweep_kernel(const double* __restrict__ zs, const double* _
     S0 += q;
   }
   if (dir == 0) {
-    zep[3 * c + 0] = t0;
-    zep[3 * c + 1] = t1;
-    zep[3 * c + 2] = t2;
+    zep[c] = t0;
+    zep[nch + c] = t1;
+    zep[2 * nch + c] = t2;
   }
 }
 
-__global__ void zero_energy_kernel(const double* __restrict__ zep, int nch, double alpha,
-                                   double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    t0 += zep[3 * c];
-    t1 += zep[3 * c + 1];
-    t2 += zep[3 * c + 2];
+// three fixed-order block sums over chunks (one block per term), then combine
+__global__ void __launch_bounds__(256) zero_energy_kernel(const double* __restrict__ zep, int nch,
+                                                          double* __restrict__ tsum) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int c = threadIdx.x; c < nch; c += 256) s += zep[(size_t)blockIdx.x * nch + c];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
-  out[0] = t0 - kTwoOverSqrtPi * t1 + t2 / (alpha * kSqrtPi);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = red[0];
+}
+
+__global__ void zero_upair_kernel(const double* __restrict__ tsum, double alpha,
+                                  double* __restrict__ out) {
+  if (threadIdx.x || blockIdx.x) return;
+  out[0] = tsum[0] - kTwoOverSqrtPi * tsum[1] + tsum[2] / (alpha * kSqrtPi);
 }
 
 ZeroPlan zero_plan(int64_t n, int mh) {
@@ -183,14 +271,18 @@ ZeroPlan zero_plan(int64_t n, int mh) {
   p.n = n;
   p.mh = mh;
   int R = 32;
-  while (R * 2 <= 512 && (int64_t)R * 2 * 4096 <= n) R *= 2;
+  while (R * 2 <= 256 && (int64_t)R * 2 * 4096 <= n) R *= 2;
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
   return p;
 }
 
 size_t zero_work_doubles(const ZeroPlan& p) {
-  return 2 * (size_t)p.nch * 2 * (2 * p.mh + 1) + 3 * (size_t)p.nch + 8;
+  const size_t nch = (size_t)p.nch;
+  return 2 * nch * 2 * (2 * p.mh + 1)   // zagg (double2)
+         + 2 * 2 * nch * p.mh           // zD (double2)
+         + 2 * nch                      // zdz
+         + 3 * nch + 8;                 // zep, tsum
 }
 
 template <int MH>
@@ -198,14 +290,22 @@ static void zero_launch(const ZeroPlan& p, double* work, const double* zs, const
                         const double2* dtab, const ZCoef& zc, const BVec& b, double alpha,
                         int want_forces, double* fzf, double* fzb, double* upair,
                         cudaStream_t st) {
+  const size_t nch = (size_t)p.nch;
   double2* zagg = reinterpret_cast<double2*>(work);
-  double* zep = work + 2 * (size_t)p.nch * 2 * (2 * MH + 1);
+  double2* zD = zagg + 2 * nch * (2 * MH + 1);
+  double* zdz = reinterpret_cast<double*>(zD + 2 * nch * MH);
+  double* zep = zdz + 2 * nch;
+  double* tsum = zep + 3 * nch;
   const int nthr = 2 * p.nch;
   zero_aggregate_kernel<MH><<<(nthr + 63) / 64, 64, 0, st>>>(zs, qs, dtab, p.n, p.R, p.nch, zagg);
-  zero_carry_kernel<MH><<<1, 64, 0, st>>>(zs, p.n, p.R, p.nch, b, zagg);
+  const int nd = 2 * p.nch * MH;
+  zero_chunk_decay_kernel<<<(nd + 255) / 256, 256, 0, st>>>(zs, p.n, p.R, p.nch, MH, b, zdz, zD);
+  const int nwarp_thr = 32 * 2 * (MH + 1);
+  zero_carry_kernel<<<(nwarp_thr + 63) / 64, 64, 0, st>>>(p.nch, MH, zdz, zD, zagg);
   zero_sweep_kernel<MH><<<(nthr + 63) / 64, 64, 0, st>>>(zs, qs, dtab, p.n, p.R, p.nch, zagg, zc,
                                                          want_forces, fzf, fzb, zep);
-  zero_energy_kernel<<<1, 32, 0, st>>>(zep, p.nch, alpha, upair);
+  zero_energy_kernel<<<3, 256, 0, st>>>(zep, p.nch, tsum);
+  zero_upair_kernel<<<1, 1, 0, st>>>(tsum, alpha, upair);
 }
 
 cudaError_t zero_run_b(const ZeroPlan& p, double* work, const double* zs, const double* qs,

@@ -239,12 +239,18 @@ class DeviceEvaluator:
                           self.modes, self.commonv, self.charge_const, forces=self.forces,
                           energy=self.energy, soe_pack=self.pack)
 
+    def warmup(self):
+        """Run one step synchronously (workspace allocation, kernel attributes)."""
+        torch = _torch()
+        self._enqueue()
+        torch.cuda.synchronize(self.eng.device)
+
     def capture(self):
         torch = _torch()
         s = torch.cuda.Stream(self.eng.device)
         s.wait_stream(torch.cuda.current_stream(self.eng.device))
         with torch.cuda.stream(s):
-            self._enqueue()  # warm-up outside capture (workspace, func attributes)
+            self.warmup()  # outside capture: workspace, func attributes, list capacity
         torch.cuda.current_stream(self.eng.device).wait_stream(s)
         torch.cuda.synchronize(self.eng.device)
         g = torch.cuda.CUDAGraph()
