@@ -1,0 +1,440 @@
+"""Benchmark: RBSE2D energy + forces at N ~ 1e6 on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+One *step* = one rb_energy_forces-equivalent evaluation:
+device mode sampling (P modes), z radix sort + gather, short-range cell-list
+kernel, SOE Fourier 3-phase scan, k = 0 mode, self / slab terms, assembly and
+the scatter to input order -- on device-resident inputs.  Per-run constants
+(SOE table, H, C_Q, alpha) are outside the step, as in the reference MD loop
+(md.py:136-142).
+
+Default workload: cfg4 (N = 999,999 2:1 electrolyte, P = 100, M = 16), the
+configuration BASELINE.json's metric is quoted on.  Inputs are the seeded
+synthetic generators of paper_2403_01521_b200/configs.py (no public dataset).
+
+Multi-GPU (torchrun, one rank per GPU): particles replicated, the sampled modes
+and the short-range home particles are split across ranks, and forces + energies
+are combined with ONE NCCL all-reduce per step; the timed N (total work) is
+fixed -> "scaling": "strong".
+
+--impl reference: the reference algorithm's CPU implementation timed on the
+host cores.  The reference package is Python + numba and cannot travel to the
+GPU box, so this arm runs the repo's C restatement of it (oracle/, "port",
+pinned against the real reference's outputs in tests/golden), on all host
+threads, over a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "particles*steps/sec (energy+forces)"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0,
+                    help="seconds of single-thread CPU work for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (nvidia-smi sampler)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side (the C restatement of the reference algorithm)
+# ---------------------------------------------------------------------------
+def oracle_sample_run(name, n_sample, nthreads, seed_modes=0):
+    """One oracle evaluation on a cfg-recipe sample of n_sample particles.
+    Returns (seconds, n)."""
+    from oracle import oracle as O
+    wl = sample_workload(name, n_sample)
+    modes = host_modes(wl, seed_modes)
+    H = host_H(wl)
+    cq = host_cq(wl)
+    cv = O.rb_commonv(H, wl.P, wl.alpha)
+    t0 = time.perf_counter()
+    e, f, flag = O.energy_forces(wl.system.pos, wl.system.charge, wl.box, wl.alpha,
+                                 wl.params().r_c, modes, cv, cq, *soe_arrays(wl.m),
+                                 nthreads=nthreads)
+    return time.perf_counter() - t0, wl.n
+
+
+def sample_workload(name, n_sample):
+    """The cfg recipe at the same density / shape / charge mix with n_sample particles."""
+    from paper_2403_01521_b200.configs import DENSITY, Workload
+    from paper_2403_01521_b200.core import BoxGeometry, choose_alpha, make_system
+    if name != "cfg4":
+        from paper_2403_01521_b200.configs import make_workload
+        return make_workload(name)
+    n = 3 * max(1, n_sample // 3)
+    lz = (n / (4 * DENSITY)) ** (1.0 / 3.0)
+    box = BoxGeometry(2 * lz, 2 * lz, lz)
+    rng = np.random.default_rng(4)
+    pos = rng.random((n, 3)) * np.array([box.lx, box.ly, box.lz])
+    q = np.concatenate([np.full(n // 3, 2.0), np.full(2 * n // 3, -1.0)])
+    system = make_system(q, np.ones(n), pos, box=box)
+    return Workload("cfg4_sample", system, box, choose_alpha(n, box, "linear", 1.0, 4.0), 4.0,
+                    16, 100, 4)
+
+
+def soe_arrays(m):
+    from paper_2403_01521_b200.soe import build_soe_contour
+    soe = build_soe_contour(m)
+    return soe.w, soe.s
+
+
+def host_modes(wl, seed):
+    """A fixed k-set for the CPU arm: the Gaussian-weighted mode law sampled on the
+    host (independent draws; the CPU cost per evaluation does not depend on it)."""
+    rng = np.random.default_rng(1000 + seed)
+    ax = math.pi / (wl.alpha * wl.box.lx)
+    ay = math.pi / (wl.alpha * wl.box.ly)
+    out = []
+    while len(out) < wl.P:
+        mx = int(np.rint(rng.normal() / (ax * math.sqrt(2))))
+        my = int(np.rint(rng.normal() / (ay * math.sqrt(2))))
+        if mx or my:
+            kx, ky = 2 * math.pi * mx / wl.box.lx, 2 * math.pi * my / wl.box.ly
+            out.append((kx, ky, math.hypot(kx, ky)))
+    return np.array(out)
+
+
+def host_H(wl):
+    import warnings
+    from paper_2403_01521_b200.rbse2d import normalization_H
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return normalization_H(wl.alpha, wl.box)
+
+
+def host_cq(wl):
+    from paper_2403_01521_b200.rbse2d import charge_term_sum
+    return charge_term_sum(wl.alpha, wl.box, float(np.sum(wl.system.charge ** 2)))
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def calibrated_sample(name, nthreads, budget_s):
+    """Largest sample size whose single evaluation fits in budget_s seconds."""
+    n_probe = 30_000
+    t, n = oracle_sample_run(name, n_probe, nthreads)
+    per = t / n
+    n_fit = int(budget_s / per)
+    return max(3000, min(n_fit, 999_999)), per
+
+
+def cpu_baseline(name, budget_s):
+    """Single-thread oracle (the reference kernels are serial numba) on a sample."""
+    n_s, _ = calibrated_sample(name, 1, budget_s)
+    t, n = oracle_sample_run(name, n_s, 1)
+    return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"one full evaluation (P=100, M=16) of a {n}-particle sample of the "
+                      f"{name} recipe (same density, box shape, charge mix) by the C "
+                      f"restatement oracle/slab_oracle.c, 1 thread, {t:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    O.build()
+    threads = cpu_count()
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    budget_total = 150.0
+    per_step_budget = budget_total / (steps + warm + 1)
+    n_s, _ = calibrated_sample(args.config, threads, per_step_budget)
+    for _ in range(warm):
+        oracle_sample_run(args.config, n_s, threads)
+    t_tot, n = 0.0, 0
+    for s in range(steps):
+        t, n = oracle_sample_run(args.config, n_s, threads, seed_modes=s)
+        t_tot += t
+    value = n * steps / t_tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": 1e3 * t_tot / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": args.config, "sample_particles": n, "P": 100, "M": 16},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{n}-particle sample of the {args.config} recipe per "
+                                       f"step, C restatement of the reference path "
+                                       f"(oracle/slab_oracle.c), OpenMP over modes and "
+                                       f"cell slabs, {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def count_launches(ev, torch):
+    """Kernels of OUR library launched by one step (torch.profiler / CUPTI)."""
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        ev.step()
+        torch.cuda.synchronize()
+    n = 0
+    for e in prof.events():
+        name = getattr(e, "name", "")
+        if "slab::" in name and getattr(e, "device_type", None) is not None:
+            if str(e.device_type).endswith("CUDA"):
+                n += 1
+    return n
+
+
+def scan_flops(n, P, m, world):
+    # canonical algorithmic work: N K (48 M + 100) + N 99 M per step
+    return n * P * (48 * m + 100) + n * 99 * m
+
+
+def load_traffic(round_tag="r01"):
+    path = os.path.join(HERE, "profiles", f"ncu_{round_tag}_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("scan_dram_bytes_per_step")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}), flush=True)
+        return 1
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        group = dist.group.WORLD
+    import paper_2403_01521_b200 as pk
+    from paper_2403_01521_b200 import _native
+    from paper_2403_01521_b200.configs import make_workload
+    from paper_2403_01521_b200.engine import DeviceEvaluator, get_engine, pinned_like
+    from paper_2403_01521_b200.rbse2d import ModeSampler, charge_term_sum, normalization_H
+
+    wl = make_workload(args.config)
+    soe = pk.build_soe_contour(wl.m)
+    params = wl.params()
+    H = normalization_H(wl.alpha, wl.box)
+    c_q = charge_term_sum(wl.alpha, wl.box, float(np.sum(wl.system.charge ** 2)))
+    ev = DeviceEvaluator(wl.system, wl.box, params, soe, P=wl.P, H=H, c_q=c_q, seed=wl.seed,
+                         rank=rank, world=world, group=group)
+    use_graph = world == 1 and wl.n < 200_000
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        ev.step()
+    torch.cuda.synchronize()
+    if use_graph:
+        ev.capture()
+        for _ in range(2):
+            ev.step()
+    launches_per_step = count_launches(ev, torch) if rank == 0 else 0
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident, CUDA events, max over ranks ----
+    K = args.steps
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K)]
+    for a, b in scan_ev:  # materialise the cudaEvent_t handles
+        a.record()
+        b.record()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for k in range(K):
+        ev.step(scan_events=None if use_graph else scan_ev[k])
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = t0.elapsed_time(t1)
+    clk = clocks.stop()
+    scan_ms = None
+    if not use_graph:
+        scan_ms = sum(a.elapsed_time(b) for a, b in scan_ev) / K
+    else:  # graph replay: time the scan separately with the same events, K steps
+        ss = []
+        for a, b in scan_ev:
+            ev.step(scan_events=(a, b))
+        torch.cuda.synchronize()
+        ss = [a.elapsed_time(b) for a, b in scan_ev]
+        scan_ms = sum(ss) / len(ss)
+    if world > 1:
+        tt = torch.tensor([ms, scan_ms], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, scan_ms = float(tt[0]), float(tt[1])
+    e = ev.energy.cpu().numpy()
+    status = int(e[5])
+
+    # ---- e2e: the public API from pinned host memory, result read back ----
+    e2e = None
+    if world == 1:
+        sysm = wl.system
+        pinned_sys = pk.make_system(pinned_like(sysm.charge), sysm.mass, sysm.pos, box=wl.box)
+        pinned_sys.pos = pinned_like(sysm.pos)
+        pinned_sys.charge = pinned_like(sysm.charge)
+        sampler = ModeSampler(wl.alpha, wl.box, seed=wl.seed)
+        pk.rb_energy_forces(pinned_sys, wl.box, params, soe, sampler, wl.P, H=H, c_q=c_q)
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        for _ in range(K):
+            bd, f = pk.rb_energy_forces(pinned_sys, wl.box, params, soe, sampler, wl.P, H=H,
+                                        c_q=c_q)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - te
+        e2e = {"value": wl.n * K / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(sysm.pos.nbytes + sysm.charge.nbytes),
+               "d2h_bytes_per_step": int(f.nbytes + 8 * 8),
+               "api": "paper_2403_01521_b200.rb_energy_forces (numpy in / numpy out)"}
+
+    if rank != 0:
+        return 0
+    peak = ctypes_peak(_native)
+    flops = scan_flops(wl.n, wl.P, wl.m, world)
+    achieved = flops / (scan_ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": wl.n * K / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator of the cfg recipe; no public dataset)",
+        "config": {"workload": f"{args.config}: N={wl.n} 2:1 electrolyte, Lx=Ly=2Lz, "
+                               f"density 0.1, P={wl.P} sampled modes, M={wl.m} SOE terms, "
+                               f"alpha={wl.alpha:.5f}, r_c={params.r_c:.4f}",
+                   "N": wl.n, "P": wl.P, "M": wl.m, "parallelism": f"modes+cells x{world}",
+                   "l2": "no flush: per-step working set (~0.6 GB) exceeds the 126 MB L2",
+                   "cuda_graph": use_graph},
+        "roofline": {"bound": "fp64", "kernel": "SOE scan (3-phase Fourier scan + k=0 mode)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None,
+                     "peak_source": "measured live: DFMA microbenchmark (slab_fp64_peak); "
+                                    "MEASURED_PEAKS.json has no fp64 figure",
+                     "flops_per_step": flops,
+                     "flops_model": "N P (48 M + 100) + 99 N M canonical fp64 (SURVEY 8(d))",
+                     "scan_ms_per_step": scan_ms,
+                     "traffic": load_traffic()},
+        "clocks": clk,
+        "gpu_launches": launches_per_step * K,
+        "energy_total": float(e[0] + e[1] + e[2] - e[3] + e[4]),
+        "status": status,
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_budget)
+        except Exception as exc:  # the CPU baseline must never sink the GPU line
+            line["cpu_baseline"] = {"error": repr(exc)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def ctypes_peak(native):
+    import ctypes
+    lib = native.load()
+    out = ctypes.c_double(0.0)
+    if lib.slab_fp64_peak(ctypes.byref(out)) != 0:
+        return None
+    return out.value
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

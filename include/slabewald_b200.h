@@ -89,6 +89,19 @@ typedef struct SlabEvalArgs {
   double* d_forces;         /* (n,3) out, input order */
   double* d_energy;         /* (8,) out: u_s,u_l_k,u_l_0,u_self,u_ps,status,0,0 */
   int64_t* d_perm;          /* optional (n,) out: the z-sort permutation, or NULL */
+  /* Multi-GPU (one process per GPU, particles replicated): this
+   * rank evaluates only its share and the caller sums d_forces and d_energy[0..4]
+   * over ranks with ONE allreduce.  The caller passes this rank's slice of the
+   * sampled modes (d_modes/nmode) with commonv for the GLOBAL batch size; the
+   * library takes home particles [rank*n/count, (rank+1)*n/count) of the
+   * short-range cell order, and rank 0 alone adds the k = 0 mode, the constants
+   * (charge_const, self, slab) and the plane forces.  shard_count <= 1: all. */
+  int shard_rank;
+  int shard_count;
+  /* optional cudaEvent_t (as void*) recorded on `stream` around the SOE scan
+   * kernels (Fourier 3-phase scan + k = 0 mode) for roofline timing */
+  void* ev_scan_begin;
+  void* ev_scan_end;
 } SlabEvalArgs;
 
 typedef struct SlabCtx SlabCtx;
@@ -142,6 +155,10 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* args, void* stream);
 int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,
                             const double* d_z, int64_t n, double beta_re, double beta_im,
                             double* d_out, void* stream);
+
+/* FP64 roofline denominator: DFMA throughput microbenchmark on the current
+ * device (TFLOP/s, 2 flops per DFMA).  Synchronous. */
+int slab_fp64_peak(double* tflops);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ SLAB_STATUS_SINGULAR = 2
 EXPORTED = (
     "slab_ctx_create", "slab_ctx_destroy", "slab_last_error", "slab_version",
     "slab_sort_by_z", "slab_fourier_sweep", "slab_zero_mode_sweep", "slab_short_range",
-    "slab_sample_modes", "slab_evaluate", "slab_recursive_pair_sum",
+    "slab_sample_modes", "slab_evaluate", "slab_recursive_pair_sum", "slab_fp64_peak",
 )
 
 
@@ -65,6 +65,10 @@ class SlabEvalArgs(ctypes.Structure):
         ("d_forces", ctypes.c_void_p),
         ("d_energy", ctypes.c_void_p),
         ("d_perm", ctypes.c_void_p),
+        ("shard_rank", ctypes.c_int),
+        ("shard_count", ctypes.c_int),
+        ("ev_scan_begin", ctypes.c_void_p),
+        ("ev_scan_end", ctypes.c_void_p),
     ]
 
 
@@ -95,6 +99,7 @@ def load():
                                       vp, vp]
     lib.slab_evaluate.argtypes = [vp, ctypes.POINTER(SlabEvalArgs), vp]
     lib.slab_recursive_pair_sum.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, vp, vp]
+    lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
 
     for name in EXPORTED:
         if name not in ("slab_last_error", "slab_version"):

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(512) assemble_energy_kernel(
     int64_t n, const double* __restrict__ part, double alpha, double area, double charge_const,
     const double* __restrict__ u_s, const double* __restrict__ u_sweep,
     const double* __restrict__ u_pair, const int* __restrict__ status,
-    double* __restrict__ energy) {
+    double* __restrict__ energy, int include_constants) {
   __shared__ double r0[512], r1[512];
   r0[threadIdx.x] = threadIdx.x < kEBlocks ? part[threadIdx.x] : 0.0;
   r1[threadIdx.x] = threadIdx.x < kEBlocks ? part[kEBlocks + threadIdx.x] : 0.0;
@@ -85,11 +85,11 @@ __global__ void __launch_bounds__(512) assemble_energy_kernel(
     const double Q = r0[0];
     energy[0] = u_s ? u_s[0] : 0.0;
     energy[1] = charge_const + (u_sweep ? u_sweep[0] : 0.0);
-    double u0 = n ? -kSqrtPi * Q / (alpha * area) : 0.0;
+    double u0 = (n && include_constants) ? -kSqrtPi * Q / (alpha * area) : 0.0;
     if (u_pair) u0 += -2.0 * kPi / area * u_pair[0];
     energy[2] = u0;
-    energy[3] = alpha / kSqrtPi * Q;
-    energy[4] = r1[0];
+    energy[3] = include_constants ? alpha / kSqrtPi * Q : 0.0;
+    energy[4] = include_constants ? r1[0] : 0.0;
     energy[5] = status ? (double)status[0] : 0.0;
     energy[6] = Q;
     energy[7] = 0.0;
@@ -110,13 +110,13 @@ cudaError_t assemble_energy(int64_t n, const double* charge, const double* pos, 
                             double sigma_top, double sigma_bot, double alpha, double area,
                             double charge_const, const double* u_s, const double* u_sweep,
                             const double* u_pair, const int* status, double* energy,
-                            double* energy_scratch, cudaStream_t st) {
+                            double* energy_scratch, int include_constants, cudaStream_t st) {
   // the 2*kEBlocks partials live in energy[8..] (callers pass >= 8 + 2*kEBlocks doubles
   // of scratch through `energy_scratch`)
   energy_partials_kernel<<<kEBlocks, 256, 0, st>>>(n, charge, pos, lz, sigma_top, sigma_bot,
                                                     energy_scratch);
   assemble_energy_kernel<<<1, 512, 0, st>>>(n, energy_scratch, alpha, area, charge_const, u_s,
-                                            u_sweep, u_pair, status, energy);
+                                            u_sweep, u_pair, status, energy, include_constants);
   return cudaGetLastError();
 }
 
@@ -151,7 +151,7 @@ __global__ void rps_aggregate_kernel(const double* __restrict__ q, const double*
   C2 acc{0.0, 0.0};
   for (int64_t j = a0; j < a1; ++j) {
     double s, co;
-    sincos(th[j], &s, &co);
+    sincos_fast(th[j], &s, &co);
     const double dz = zend - z[j];
     C2 e = cexp_neg(br * dz, bi * dz);
     C2 u{q[j] * co, -q[j] * s};
@@ -191,7 +191,7 @@ __global__ void rps_final_kernel(const double* __restrict__ q, const double* __r
     out[2 * a] = T.re;
     out[2 * a + 1] = T.im;
     double s, co;
-    sincos(th[a], &s, &co);
+    sincos_fast(th[a], &s, &co);
     T.re += q[a] * co;
     T.im -= q[a] * s;
   }
@@ -209,4 +209,55 @@ cudaError_t recursive_pair_sum(const double* q, const double* theta, const doubl
   return cudaGetLastError();
 }
 
+}  // namespace slab
+
+// ---------------------------------------------------------------------------
+// FP64 roofline denominator: a DFMA throughput microbenchmark (8 independent
+// chains per thread, 2 CTAs of 1024 threads per SM).  MEASURED_PEAKS.json has
+// no fp64 figure, so bench.py measures it live on the box it runs on.
+// ---------------------------------------------------------------------------
+namespace slab {
+__global__ void __launch_bounds__(1024) dfma_peak_kernel(double* out, int iters, double a,
+                                                         double b) {
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = threadIdx.x * 1e-9 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma(acc[c], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+cudaError_t fp64_peak(double* tflops) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out;
+  cudaError_t e = cudaMalloc(&out, sizeof(double));
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = 2 * sms, threads = 1024, iters = 20000;
+  dfma_peak_kernel<<<blocks, threads>>>(out, 200, 1.0000001, 1e-7);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
+    dfma_peak_kernel<<<blocks, threads>>>(out, iters, 1.0000001, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  *tflops = 2.0 * 8.0 * iters * (double)blocks * threads / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError();
+}
 }  // namespace slab

@@ -277,7 +277,7 @@ int slab_short_range(SlabCtx* ctx, const double* d_pos, const double* d_charge, 
   int rc = ensure_arena(ctx, slab::short_work_bytes(sp) + 1024);
   if (rc) return rc;
   CK(slab::short_run(sp, ctx->arena, d_pos, d_charge, box.lx, box.ly, box.lz, alpha, r_c,
-                     d_forces, d_energy, d_status, st));
+                     d_forces, d_energy, d_status, 0, n, st));
   return SLAB_OK;
 }
 
@@ -354,10 +354,17 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
     CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm));
     CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm, st));
   }
-  if (!a->skip_short_range)
+  const int scount = a->shard_count > 1 ? a->shard_count : 1;
+  const int srank = scount > 1 ? a->shard_rank : 0;
+  if (srank < 0 || srank >= scount) return fail(SLAB_ERR_ARG, "shard_rank out of range");
+  const bool lead = srank == 0;  // the rank that owns the k = 0 mode and the constants
+  if (!a->skip_short_range) {
+    const int64_t h0 = n * srank / scount, h1 = n * (srank + 1) / scount;
     CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
-                       a->r_c, fshort, u_s, ctx->status, st));
+                       a->r_c, fshort, u_s, ctx->status, h0, h1, st));
+  }
   const bool forces = a->want_forces && n > 0;
+  if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, st));
   if (n >= 2) {
     CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
     if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, st));
@@ -365,21 +372,30 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
       CK(slab::fourier_run(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, a->d_modes, a->d_commonv,
                            a->commonv_scalar, area, sh.b, sh.w, forces ? 1 : 0, u_sweep,
                            ctx->status, w.fsorted, st));
-    CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
-                        w.fzf, w.fzb, u_pair, st));
+    if (lead)
+      CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
+                          w.fzf, w.fzb, u_pair, st));
   } else if (forces) {
     CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * N, st));
   }
+  if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, st));
   if (forces) {
-    const double plane = box.sigma_top - box.sigma_bot;
-    CK(slab::assemble_forces(n, perm, w.qs, w.fsorted, n >= 2 ? w.fzf : nullptr, w.fzb,
+    const double plane = lead ? box.sigma_top - box.sigma_bot : 0.0;
+    CK(slab::assemble_forces(n, perm, w.qs, w.fsorted, (n >= 2 && lead) ? w.fzf : nullptr, w.fzb,
                              2.0 * slab::kPi / area, a->skip_short_range ? nullptr : fshort,
                              a->d_charge, plane, a->d_forces, st));
   }
   CK(slab::assemble_energy(n, a->d_charge, a->d_pos, box.lz, box.sigma_top, box.sigma_bot,
-                           a->alpha, area, a->charge_const, u_s, u_sweep, u_pair, ctx->status,
-                           a->d_energy, ctx->small + 64, st));
+                           a->alpha, area, lead ? a->charge_const : 0.0, u_s, u_sweep,
+                           lead ? u_pair : nullptr, ctx->status, a->d_energy, ctx->small + 64,
+                           lead ? 1 : 0, st));
   return SLAB_OK;
 }
 
 }  // extern "C"
+
+extern "C" int slab_fp64_peak(double* tflops) {
+  if (!tflops) return fail(SLAB_ERR_ARG, "null output");
+  CK(slab::fp64_peak(tflops));
+  return SLAB_OK;
+}

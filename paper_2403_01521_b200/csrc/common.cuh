@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "fastmath.cuh"
+
 #define SLAB_CUDA_CHECK(expr)                              \
   do {                                                     \
     cudaError_t _e = (expr);                               \
@@ -34,10 +36,10 @@ __device__ __forceinline__ C2 cmul(C2 a, C2 b) {
   return {fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
 }
 __device__ __forceinline__ C2 cexp_neg(double xr, double xi) {
-  // exp(-(xr + i xi))
-  double e = exp(-xr);
+  // exp(-(xr + i xi)) for xr >= 0 (every caller: Re(b) > 0 times a z distance >= 0)
+  const double e = exp_neg(xr);
   double s, c;
-  sincos(xi, &s, &c);
+  sincos_fast(xi, &s, &c);
   return {e * c, -e * s};
 }
 

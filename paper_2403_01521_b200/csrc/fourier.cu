@@ -33,7 +33,7 @@
 
 namespace slab {
 
-constexpr int kSB = 8;          // force staging batch (particles)
+constexpr int kSB = 4;          // force staging batch (particles)
 constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
 constexpr int kMaxR = 256;
 
@@ -186,14 +186,15 @@ __global__ void __launch_bounds__(256) fourier_aggregate_kernel(
 #pragma unroll
   for (int l = 0; l < MH; ++l) Racc[l] = Iacc[l] = C2{0.0, 0.0};
   C2 gacc{0.0, 0.0};
+#pragma unroll 2
   for (int i = 0; i < len; ++i) {
     const double th = __dadd_rn(__dmul_rn(kx, sx[i]), __dmul_rn(ky, sy[i]));
     double sn, cs;
-    sincos(th, &sn, &cs);
+    sincos_fast(th, &sn, &cs);
     const double q = sq[i];
     const double ur = q * cs, ui = -sigma * q * sn;
     const double dist = fwd ? (z_end - sz[i]) : (sz[i] - z_start);
-    const double wk = exp(-k * dist);
+    const double wk = exp_neg(k * dist);
     gacc.re = fma(ur, wk, gacc.re);
     gacc.im = fma(ui, wk, gacc.im);
 #pragma unroll
@@ -230,7 +231,7 @@ __device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, in
   if (isg) {
     const double dz = fwd ? (c > 0 ? zbound[c] - zbound[c - 1] : 0.0)
                           : (c + 1 < nch ? zbound[nch + c + 1] - zbound[nch + c] : 0.0);
-    return C2{exp(-k * dz), 0.0};
+    return C2{exp_neg(k * dz), 0.0};
   }
   const double2 d = fwd ? Df[(size_t)c * mh + l] : Db[(size_t)c * mh + l];
   return C2{d.x, d.y};
@@ -307,21 +308,32 @@ __global__ void __launch_bounds__(128) fourier_carry_kernel(
 // ---------------------------------------------------------------------------
 // phase 3: exact recurrence from the carried-in state + fused epilogue
 // ---------------------------------------------------------------------------
+// Scaled state: per pair l the lane keeps H^R_l = C_l R_l and H^I_l = C_l I_l
+// (C_l = 2 c_l, k-dependent), so
+//   sum_l 2Re(c_l R_l) = sum_l Re(H^R_l)               (no C in the loop body)
+//   sum_l 2Re(c_l b_l R_l) = sum_l Re(b_l H^R_l)        (b_l k-independent: kernel param)
+// and the real input enters as H += C_l u.  C_l lives in shared memory
+// (per-lane column), which keeps the kernel at <= 128 registers: 2 CTAs / 16
+// warps per SM to hide the fp64 dependency latency.
+// Forces: per batch of kSB particles, lanes stage (Fx, Fy, Fz) transposed in
+// smem and 3*kSB lanes row-sum them; each warp writes its own partial buffer
+// (forward and backward lanes to separate buffers), reduced in fixed order
+// afterwards: deterministic, no atomics.
 template <int MH>
-__global__ void __launch_bounds__(256, 1) fourier_sweep_kernel(
+__global__ void __launch_bounds__(256, 2) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
-    const double* __restrict__ modetab, int P, int ipg, const double2* __restrict__ carry,
+    const double* __restrict__ modetab, int P, int ipg, BVec b, const double2* __restrict__ carry,
     double* __restrict__ epart, double* __restrict__ fpart, int want_forces) {
   extern __shared__ double4 smem4[];
   const int nwarps = blockDim.x >> 5;
-  double* sx = reinterpret_cast<double*>(smem4);
+  double2* sC = reinterpret_cast<double2*>(smem4);         // [MH][blockDim]
+  double2* sd = sC + MH * blockDim.x;                      // (R + 1) * MH
+  double* sx = reinterpret_cast<double*>(sd + (R + 1) * MH);
   double* sy = sx + R;
   double* sq = sy + R;
-  double* sz = sq + R;                                  // R + 2 (halo below / above)
-  double2* sd = reinterpret_cast<double2*>(sz + R + 2);  // (R + 1) * MH
-  double* stage = reinterpret_cast<double*>(sd + (R + 1) * MH);  // nwarps * kSB*3 * 33
-  double* fw = stage + nwarps * kSB * 3 * kStageStride;          // nwarps * R * 3
+  double* sz = sq + R;                                     // R + 2 (halo below / above)
+  double* stage = sz + R + 2;                              // nwarps * kSB*3 * 33
 
   const int c = blockIdx.x, g = blockIdx.y;
   const int64_t a0 = (int64_t)c * R;
@@ -338,11 +350,6 @@ __global__ void __launch_bounds__(256, 1) fourier_sweep_kernel(
     sz[len + 1] = zs[a1 < n ? a1 : a1 - 1];
   }
   for (int e = threadIdx.x; e < (len + 1) * MH; e += blockDim.x) sd[e] = dtab[a0 * MH + e];
-  for (int e = threadIdx.x; e < nwarps * len * 3; e += blockDim.x) {
-    const int wi = e / (len * 3);
-    fw[(size_t)wi * R * 3 + (e - wi * len * 3)] = 0.0;
-  }
-  __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nitems = 2 * P;
@@ -357,59 +364,71 @@ __global__ void __launch_bounds__(256, 1) fourier_sweep_kernel(
   const double* mt = modetab + (size_t)t * mode_stride(MH);
   const double kx = mt[0], ky = mt[1], k = mt[2];
   const double sigma = fwd ? 1.0 : -1.0;
-  const double fxy_c = active ? sigma * mt[3] : 0.0;   // +-ck
-  const double fz_c = active ? -sigma * mt[4] : 0.0;   // -+cz
+  const double fxy_c = active ? sigma * mt[3] : 0.0;  // +-ck
+  const double fz_c = active ? -sigma * mt[4] : 0.0;  // -+cz
   const double kappa = mt[5];
   const double two_k = 2.0 * k;
-  C2 Cc[MH], CB[MH], Rs[MH], Is[MH];
-#pragma unroll
-  for (int l = 0; l < MH; ++l) {
-    Cc[l] = C2{mt[8 + 2 * l], mt[9 + 2 * l]};
-    CB[l] = C2{mt[8 + 2 * MH + 2 * l], mt[9 + 2 * MH + 2 * l]};
-  }
   const int nc = ncomp_of(MH);
+  C2 HR[MH], HI[MH];
   C2 gk{0.0, 0.0};
   {
     const double2* cin = carry + (size_t)c * nc * nitems + (active ? item : 0);
 #pragma unroll
     for (int l = 0; l < MH; ++l) {
-      double2 r = cin[(size_t)l * nitems], im = cin[(size_t)(MH + l) * nitems];
-      Rs[l] = C2{r.x, r.y};
-      Is[l] = C2{im.x, im.y};
+      const C2 cl{mt[8 + 2 * l], mt[9 + 2 * l]};
+      sC[l * blockDim.x + threadIdx.x] = make_double2(cl.re, cl.im);
+      const double2 r = cin[(size_t)l * nitems], im = cin[(size_t)(MH + l) * nitems];
+      HR[l] = cmul(cl, C2{r.x, r.y});
+      HI[l] = cmul(cl, C2{im.x, im.y});
     }
-    double2 gg = cin[(size_t)(2 * MH) * nitems];
+    const double2 gg = cin[(size_t)(2 * MH) * nitems];
     gk = C2{gg.x, gg.y};
   }
+  __syncthreads();
 
+  // partial force buffers: one per (group, warp); the single warp that holds
+  // both directions sends its backward lanes to the extra buffer G*W
+  const int gw = g * nwarps + warp;
+  double* fbuf_f = fpart + (size_t)gw * n * 3;
+  double* fbuf_b = fpart + (size_t)(fmask ? gridDim.y * nwarps : gw) * n * 3;
+  const double2* sCl = sC + threadIdx.x;
   double* st = stage + warp * kSB * 3 * kStageStride;
-  double* fwp = fw + (size_t)warp * R * 3;
   double E = 0.0;
+  // Software pipeline: the k-dependent transcendentals of the NEXT particle
+  // (sincos of theta, e^{-k dz}) are issued in the same basic block as this
+  // particle's recurrence, so their dependency chains interleave.
+  auto phase = [&](int i, double& cs_, double& sn_, double& dk_, double& q_) {
+    const int ia = fwd ? i : len - 1 - i;
+    const double dz = fwd ? (sz[ia + 1] - sz[ia]) : (sz[ia + 2] - sz[ia + 1]);
+    dk_ = exp_neg(k * dz);
+    const double th = __dadd_rn(__dmul_rn(kx, sx[ia]), __dmul_rn(ky, sy[ia]));
+    sincos_fast(th, &sn_, &cs_);
+    q_ = sq[ia];
+  };
+  double cs, sn, dk, q;
+  phase(0, cs, sn, dk, q);
   for (int i = 0; i < len; ++i) {
+    double cs_n, sn_n, dk_n, q_n;
+    phase(i + 1 < len ? i + 1 : i, cs_n, sn_n, dk_n, q_n);
     const int ia = fwd ? i : len - 1 - i;
     const int id = fwd ? ia : ia + 1;
-    const double dz = fwd ? (sz[ia + 1] - sz[ia]) : (sz[ia + 2] - sz[ia + 1]);
-    const double dk = exp(-k * dz);
     // S_a = T_{a-1} * d_a  (forward) / T'_{a+1} * d_{a+1} (backward)
 #pragma unroll
     for (int l = 0; l < MH; ++l) {
       const double2 d = sd[id * MH + l];
-      Rs[l] = cmul(Rs[l], C2{d.x, d.y});
-      Is[l] = cmul(Is[l], C2{d.x, d.y});
+      HR[l] = cmul(HR[l], C2{d.x, d.y});
+      HI[l] = cmul(HI[l], C2{d.x, d.y});
     }
     gk.re *= dk;
     gk.im *= dk;
     double sgr = 0.0, sgi = 0.0, sbr = 0.0, sbi = 0.0;
 #pragma unroll
     for (int l = 0; l < MH; ++l) {
-      sgr = fma(Cc[l].re, Rs[l].re, fma(-Cc[l].im, Rs[l].im, sgr));
-      sgi = fma(Cc[l].re, Is[l].re, fma(-Cc[l].im, Is[l].im, sgi));
-      sbr = fma(CB[l].re, Rs[l].re, fma(-CB[l].im, Rs[l].im, sbr));
-      sbi = fma(CB[l].re, Is[l].re, fma(-CB[l].im, Is[l].im, sbi));
+      sgr += HR[l].re;
+      sgi += HI[l].re;
+      sbr = fma(b.re[l], HR[l].re, fma(-b.im[l], HR[l].im, sbr));
+      sbi = fma(b.re[l], HI[l].re, fma(-b.im[l], HI[l].im, sbi));
     }
-    const double x = sx[ia], y = sy[ia], q = sq[ia];
-    const double th = __dadd_rn(__dmul_rn(kx, x), __dmul_rn(ky, y));
-    double sn, cs;
-    sincos(th, &sn, &cs);
     const double ps = sigma * sn;  // phase e^{+-i theta} = (cs, ps)
     const double pr = fma(kappa, gk.re, -two_k * sgr);
     const double pi = fma(kappa, gk.im, -two_k * sgi);
@@ -427,41 +446,50 @@ __global__ void __launch_bounds__(256, 1) fourier_sweep_kernel(
       if (slot == kSB - 1 || i == len - 1) {
         __syncwarp();
         const int nslot = slot + 1, ibase = i - slot;
-        const int s = lane / 3, comp = lane - 3 * (lane / 3);
-        double sf = 0.0, sb = 0.0;
         if (lane < 3 * nslot) {
+          const int s = lane / 3, comp = lane - 3 * s;
           const double* row = st + (s * 3 + comp) * kStageStride;
+          double sf = 0.0, sb = 0.0;
+          if (bmask == 0u || fmask == 0u) {  // single-direction warp (all but one)
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              acc0 += row[j];
+              acc1 += row[j + 1];
+            }
+            (bmask == 0u ? sf : sb) = acc0 + acc1;
+          } else {
 #pragma unroll 8
-          for (int j = 0; j < 32; ++j) {
-            const double v = row[j];
-            if ((fmask >> j) & 1u) sf += v;
-            if ((bmask >> j) & 1u) sb += v;
+            for (int j = 0; j < 32; ++j) {
+              const double v = row[j];
+              if ((fmask >> j) & 1u) sf += v;
+              if ((bmask >> j) & 1u) sb += v;
+            }
           }
-          if (fmask) fwp[(ibase + s) * 3 + comp] += sf;
+          if (fmask) fbuf_f[(a0 + ibase + s) * 3 + comp] = sf;
+          if (bmask) fbuf_b[(a0 + len - 1 - (ibase + s)) * 3 + comp] = sb;
         }
-        __syncwarp();
-        if (lane < 3 * nslot && bmask) fwp[(len - 1 - (ibase + s)) * 3 + comp] += sb;
         __syncwarp();
       }
     }
-    // T_a = S_a + u_a (input is real for every recurrence)
+    // T_a = S_a + u_a: real input scaled by C_l into the scaled state
     const double ur = q * cs, ui = -sigma * q * sn;
 #pragma unroll
     for (int l = 0; l < MH; ++l) {
-      Rs[l].re += ur;
-      Is[l].re += ui;
+      const double2 cl = sCl[l * blockDim.x];
+      HR[l].re = fma(cl.x, ur, HR[l].re);
+      HR[l].im = fma(cl.y, ur, HR[l].im);
+      HI[l].re = fma(cl.x, ui, HI[l].re);
+      HI[l].im = fma(cl.y, ui, HI[l].im);
     }
     gk.re += ur;
     gk.im += ui;
+    cs = cs_n;
+    sn = sn_n;
+    dk = dk_n;
+    q = q_n;
   }
   if (active && fwd) epart[(size_t)c * P + t] = E;
-  if (!want_forces) return;
-  __syncthreads();
-  for (int e = threadIdx.x; e < len * 3; e += blockDim.x) {
-    double v = 0.0;
-    for (int wi = 0; wi < nwarps; ++wi) v += fw[(size_t)wi * R * 3 + e];
-    fpart[(size_t)g * n * 3 + a0 * 3 + e] = v;
-  }
 }
 
 // per-mode sums over chunks (one block per mode, fixed-order tree), then Kahan
@@ -494,13 +522,13 @@ __global__ void kahan_modes_kernel(const double* __restrict__ se, int P, double*
   out[0] = u;
 }
 
-// forces_sorted (+)= sum over item groups (fixed order)
-__global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int ngroups,
+// forces_sorted += sum of the per-warp partial buffers (fixed order)
+__global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int nbuf,
                                             int64_t n3, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n3) return;
   double v = 0.0;
-  for (int g = 0; g < ngroups; ++g) v += fpart[(size_t)g * n3 + e];
+  for (int b = 0; b < nbuf; ++b) v += fpart[(size_t)b * n3 + e];
   out[e] += v;
 }
 
@@ -508,9 +536,9 @@ __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, in
 // host side
 // ---------------------------------------------------------------------------
 static size_t sweep_smem(int R, int mh, int warps) {
-  return sizeof(double) * (3 * (size_t)R + R + 2) + sizeof(double2) * (size_t)(R + 1) * mh +
-         sizeof(double) * (size_t)warps * kSB * 3 * kStageStride +
-         sizeof(double) * (size_t)warps * R * 3;
+  return sizeof(double2) * (size_t)mh * warps * 32 + sizeof(double2) * (size_t)(R + 1) * mh +
+         sizeof(double) * (3 * (size_t)R + R + 2) +
+         sizeof(double) * (size_t)warps * kSB * 3 * kStageStride;
 }
 static size_t agg_smem(int R, int mh) {
   return sizeof(double) * 4 * (size_t)R + sizeof(double2) * 2 * (size_t)R * mh;
@@ -535,6 +563,11 @@ FourierPlan fourier_plan(int64_t n, int P, int mh) {
   p.nch = (int)((n + R - 1) / R);
   p.smem_agg = agg_smem(R, mh);
   p.smem_sweep = sweep_smem(R, mh, p.warps);
+  // one partial force buffer per (group, warp) + one for the backward lanes of
+  // the (at most one) warp that holds both directions
+  const int g_of_p = P / p.ipg;  // group containing item P (first backward item)
+  const bool mixed = P < nitems && ((P - g_of_p * p.ipg) % 32) != 0;
+  p.nbuf = p.ngroups * p.warps + (mixed ? 1 : 0);
   return p;
 }
 
@@ -545,7 +578,7 @@ size_t fourier_work_doubles(const FourierPlan& p) {
   d += 2 * 2 * (size_t)p.nch * p.mh;                 // Df, Db (double2)
   d += 2 * (size_t)p.nch;                            // zbound
   d += (size_t)p.nch * p.P + p.P;                    // epart + per-mode sums
-  d += (size_t)p.ngroups * p.n * 3;                  // fpart
+  d += (size_t)(p.nbuf + 1) * p.n * 3;               // fpart
   return d + 64;
 }
 
@@ -598,7 +631,7 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
         w.carry, p.nch, p.P, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH, w.zbound);
   }
   fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
-      xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.ipg, w.carry, w.epart, w.fpart,
+      xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.ipg, b, w.carry, w.epart, w.fpart,
       want_forces);
   return cudaGetLastError();
 }
@@ -617,17 +650,11 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
                                                         w.dchunk, w.dchunk + (size_t)p.nch * p.mh);
   cudaError_t e = cudaErrorInvalidValue;
   switch (p.mh) {
-    case 2: e = run_mh<2>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 3: e = run_mh<3>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 4: e = run_mh<4>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 5: e = run_mh<5>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 6: e = run_mh<6>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 7: e = run_mh<7>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 8: e = run_mh<8>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 9: e = run_mh<9>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 10: e = run_mh<10>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 11: e = run_mh<11>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    case 12: e = run_mh<12>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+#define FCASE(K) \
+  case K: e = run_mh<K>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
+    FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
+    FCASE(12)
+#undef FCASE
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
@@ -636,7 +663,7 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
   kahan_modes_kernel<<<1, 1, 0, st>>>(se, p.P, energy_out);
   if (want_forces) {
     const int64_t n3 = p.n * 3;
-    fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(w.fpart, p.ngroups,
+    fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(w.fpart, p.nbuf,
                                                                               n3, forces_sorted);
   }
   return cudaGetLastError();

@@ -51,6 +51,7 @@ struct FourierPlan {
   int ngroups;    // item groups per chunk
   int ipg;        // items per group
   int warps;      // warps per CTA
+  int nbuf;       // partial force buffers (per group x warp, + 1 if a warp mixes directions)
   size_t smem_agg, smem_sweep;
 };
 FourierPlan fourier_plan(int64_t n, int P, int mh);
@@ -61,7 +62,7 @@ struct FourierWork {
   double2* dchunk;   // 2 * nch * mh   (Df, Db)
   double* zbound;    // 2 * nch        (z_end, z_start)
   double* epart;     // nch * P
-  double* fpart;     // ngroups * n * 3
+  double* fpart;     // nbuf * n * 3
 };
 size_t fourier_work_doubles(const FourierPlan& p);
 void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w);
@@ -101,7 +102,8 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc);
 size_t short_work_bytes(const ShortPlan& p);
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
-                      double* energy_out, int* status, cudaStream_t st);
+                      double* energy_out, int* status, int64_t home_begin, int64_t home_end,
+                      cudaStream_t st);
 
 // ---------------------------------------------------------------- assemble.cu
 cudaError_t assemble_forces(int64_t n, const int32_t* perm, const double* qs,
@@ -112,7 +114,7 @@ cudaError_t assemble_energy(int64_t n, const double* charge, const double* pos, 
                             double sigma_top, double sigma_bot, double alpha, double area,
                             double charge_const, const double* u_s, const double* u_sweep,
                             const double* u_pair, const int* status, double* energy,
-                            double* energy_scratch, cudaStream_t st);
+                            double* energy_scratch, int include_constants, cudaStream_t st);
 
 // ---------------------------------------------------------------- sampler.cu
 cudaError_t sample_modes(int64_t* state, uint64_t seed, double alpha, double lx, double ly,
@@ -127,4 +129,8 @@ cudaError_t recursive_pair_sum(const double* q, const double* theta, const doubl
 cudaError_t fz_accumulate(int64_t n, const double* fzf, const double* fzb, double* fz,
                           cudaStream_t st);
 
+}  // namespace slab
+
+namespace slab {
+cudaError_t fp64_peak(double* tflops);
 }  // namespace slab

@@ -32,7 +32,8 @@ struct PairAcc {
 __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi, double qi,
                                                 double xj, double yj, double zj, double qj,
                                                 double lx, double ly, double ilx, double ily,
-                                                double alpha, double rc2, double c, PairAcc& acc,
+                                                double alpha, double rc2, double c,
+                                                const double* __restrict__ etab, PairAcc& acc,
                                                 int& flag) {
   double dx = __dsub_rn(xi, xj), dy = __dsub_rn(yi, yj);
   const double dz = __dsub_rn(zi, zj);
@@ -47,8 +48,8 @@ __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi,
   const double d = sqrt(d2);
   const double qq = qi * qj;
   const double x = alpha * d;
-  const double g = exp(-x * x);   // shared by erfc and the force Gaussian
-  const double e = erfcx(x) * g;  // erfc(x) without a second exp
+  double e, g;  // erfc(x) and the force Gaussian e^{-x^2} share one exp
+  erfc_gauss(x, etab, &e, &g);
   const double inv_d = 1.0 / d;
   acc.e = fma(qq * e, inv_d, acc.e);
   const double fmag = qq * (e * inv_d + c * g) * (inv_d * inv_d);
@@ -98,18 +99,22 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
 }
 
 constexpr int kSRThreads = 128;
-constexpr int kQ = 32;  // per-thread queue of screened candidates
+constexpr int kQ = 32;  // per-thread queue of screened candidates (16 KB per block)
 
 __global__ void __launch_bounds__(kSRThreads) short_cells_kernel(
     const double4* __restrict__ cp, const float4* __restrict__ cpf,
     const int32_t* __restrict__ order, const uint32_t* __restrict__ skey,
-    const int32_t* __restrict__ start, int64_t n, int ncx, int ncy, int ncz, double lx, double ly,
-    double alpha, double rc2, float rc2f, double* __restrict__ forces, double* __restrict__ eblk,
-    int* __restrict__ status) {
-  __shared__ int32_t queue[kQ][kSRThreads];
+    const int32_t* __restrict__ start, int64_t a_begin, int64_t a_end, int ncx, int ncy, int ncz,
+    double lx, double ly, double alpha, double rc2, float rc2f, double* __restrict__ forces,
+    double* __restrict__ eblk, int* __restrict__ status) {
+  extern __shared__ int32_t queue_raw[];
+  int32_t (*queue)[kSRThreads] = reinterpret_cast<int32_t (*)[kSRThreads]>(queue_raw);
+  __shared__ double etab[SLAB_ERFCX_NINT * kErfcxStride];
+  load_erfcx_table(etab);
+  __syncthreads();
   const int tid = threadIdx.x;
-  const int64_t a = blockIdx.x * (int64_t)kSRThreads + tid;
-  const bool active = a < n;
+  const int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + tid;
+  const bool active = a < a_end;
   const double c = kTwoOverSqrtPi * alpha;
   const double ilx = 1.0 / lx, ily = 1.0 / ly;
   const float lxf = (float)lx, lyf = (float)ly, ilxf = 1.0f / lxf, ilyf = 1.0f / lyf;
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(kSRThreads) short_cells_kernel(
       if (k < cnt) {
         const double4 pj = cp[queue[k][tid]];
         pair_accumulate(pd.x, pd.y, pd.z, pd.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
-                        rc2, c, acc, flag);
+                        rc2, c, etab, acc, flag);
       }
     }
     cnt = 0;
@@ -175,10 +180,13 @@ __global__ void __launch_bounds__(kSRThreads) short_cells_kernel(
 
 // all pairs (ncx < 3 or ncy < 3): grid (i tiles, j splits)
 __global__ void __launch_bounds__(128) brute_pair_kernel(
-    const double* __restrict__ pos, const double* __restrict__ q, int64_t n, int jsplit,
-    double lx, double ly, double alpha, double rc2, double* __restrict__ fbuf,
-    double* __restrict__ eblk, int* __restrict__ status) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const double* __restrict__ pos, const double* __restrict__ q, int64_t n, int64_t i_begin,
+    int64_t i_end, int jsplit, double lx, double ly, double alpha, double rc2,
+    double* __restrict__ fbuf, double* __restrict__ eblk, int* __restrict__ status) {
+  __shared__ double etab[SLAB_ERFCX_NINT * kErfcxStride];
+  load_erfcx_table(etab);
+  __syncthreads();
+  const int64_t i = i_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int js = blockIdx.y;
   const int64_t per = (n + jsplit - 1) / jsplit;
   const int64_t j0 = js * per, j1 = j0 + per < n ? j0 + per : n;
@@ -186,12 +194,12 @@ __global__ void __launch_bounds__(128) brute_pair_kernel(
   const double ilx = 1.0 / lx, ily = 1.0 / ly;
   PairAcc acc{0.0, 0.0, 0.0, 0.0};
   int flag = 0;
-  if (i < n) {
+  if (i < i_end) {
     const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2], qi = q[i];
     for (int64_t j = j0; j < j1; ++j) {
       if (j == i) continue;
       pair_accumulate(xi, yi, zi, qi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], q[j], lx, ly,
-                      ilx, ily, alpha, rc2, c, acc, flag);
+                      ilx, ily, alpha, rc2, c, etab, acc, flag);
     }
     double* f = fbuf + ((size_t)js * n + i) * 3;
     f[0] = acc.fx;
@@ -272,24 +280,32 @@ size_t short_work_bytes(const ShortPlan& p) {
 
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
-                      double* energy_out, int* status, cudaStream_t st) {
+                      double* energy_out, int* status, int64_t h0, int64_t h1,
+                      cudaStream_t st) {
   const int64_t n = p.n;
-  if (n < 2) {
+  if (n < 2 || h1 <= h0) {
     cudaMemsetAsync(energy_out, 0, sizeof(double), st);
     if (n > 0) cudaMemsetAsync(forces, 0, sizeof(double) * 3 * n, st);
     return cudaGetLastError();
   }
+  // a shard (multi-GPU) writes only its home particles: clear the rest first
+  const bool partial = h0 > 0 || h1 < n;
+  if (partial) cudaMemsetAsync(forces, 0, sizeof(double) * 3 * n, st);
+  const int64_t nh = h1 - h0;
   char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(work) + 255) & ~(uintptr_t)255);
   double* eblk = reinterpret_cast<double*>(w);
   w += align256(sizeof(double) * p.nblk);
   const double rc2 = rc * rc;
   if (p.brute) {
     double* fbuf = reinterpret_cast<double*>(w);
-    const unsigned nbx = (unsigned)((n + 127) / 128);
-    brute_pair_kernel<<<dim3(nbx, p.jsplit), 128, 0, st>>>(pos, charge, n, p.jsplit, lx, ly, alpha,
-                                                           rc2, fbuf, eblk, status);
+    const unsigned nbx = (unsigned)((nh + 127) / 128);
+    if (partial) cudaMemsetAsync(fbuf, 0, sizeof(double) * 3 * n * p.jsplit, st);
+    brute_pair_kernel<<<dim3(nbx, p.jsplit), 128, 0, st>>>(pos, charge, n, h0, h1, p.jsplit, lx, ly,
+                                                           alpha, rc2, fbuf, eblk, status);
     brute_force_reduce_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(fbuf, p.jsplit,
                                                                                3 * n, forces);
+    half_sum_kernel<<<1, 1024, 0, st>>>(eblk, (int64_t)nbx * p.jsplit, energy_out);
+    return cudaGetLastError();
   } else {
     uint32_t* k0 = reinterpret_cast<uint32_t*>(w);
     w += align256(sizeof(uint32_t) * n);
@@ -321,11 +337,18 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     // conservative fp32 screen: positions rounded to fp32 move d2 by < 1e-2 for
     // |r| <= 1e3; the exact fp64 test is applied to every survivor
     const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);
-    short_cells_kernel<<<(unsigned)p.nblk, kSRThreads, 0, st>>>(
-        cp, cpf, order, skey, start, n, p.ncx, p.ncy, p.ncz, lx, ly, alpha, rc2, rc2f, forces,
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(short_cells_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(int32_t) * kQ * kSRThreads));
+      attr = true;
+    }
+    const int64_t nblk = (nh + kSRThreads - 1) / kSRThreads;
+    short_cells_kernel<<<(unsigned)nblk, kSRThreads, sizeof(int32_t) * kQ * kSRThreads, st>>>(
+        cp, cpf, order, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, lx, ly, alpha, rc2, rc2f, forces,
         eblk, status);
+    half_sum_kernel<<<1, 1024, 0, st>>>(eblk, nblk, energy_out);
   }
-  half_sum_kernel<<<1, 1024, 0, st>>>(eblk, p.nblk, energy_out);
   return cudaGetLastError();
 }
 

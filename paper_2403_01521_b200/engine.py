@@ -74,9 +74,13 @@ class Engine:
     # -- full evaluation ----------------------------------------------------
     def evaluate(self, pos, charge, box, alpha, r_c, soe, modes, commonv, charge_const,
                  forces=None, energy=None, want_forces=True, skip_short_range=False,
-                 perm=None, soe_pack=None):
+                 perm=None, soe_pack=None, shard=(0, 1), scan_events=None):
         """Enqueue one energy/force evaluation.  ``commonv`` is a float (RB) or a
-        (P,) device tensor (full mode sum).  Writes energy (8,) and forces (n,3)."""
+        (P,) device tensor (full mode sum).  Writes energy (8,) and forces (n,3).
+
+        ``shard=(rank, count)``: multi-GPU share (caller passes this rank's mode
+        slice and sums forces / energy[0:5] over ranks).  ``scan_events``: a pair
+        of torch.cuda.Event recorded around the SOE scan kernels."""
         torch = _torch()
         n = charge.numel()
         if energy is None:
@@ -95,7 +99,9 @@ class Engine:
             charge_const=float(charge_const), want_forces=1 if want_forces else 0,
             skip_short_range=1 if skip_short_range else 0,
             d_forces=_ptr(forces) if want_forces else None, d_energy=_ptr(energy),
-            d_perm=_ptr(perm))
+            d_perm=_ptr(perm), shard_rank=int(shard[0]), shard_count=int(shard[1]),
+            ev_scan_begin=ctypes.c_void_p(scan_events[0].cuda_event) if scan_events else None,
+            ev_scan_end=ctypes.c_void_p(scan_events[1].cuda_event) if scan_events else None)
         check(self.lib.slab_evaluate(self.ctx, ctypes.byref(args), self._stream()),
               "slab_evaluate")
         return energy, forces
@@ -166,10 +172,27 @@ def get_engine(device=None) -> Engine:
 
 
 def to_device(a, dtype=None, device=None):
+    """Host array -> device tensor.  Memory that is already page-locked (e.g. a
+    numpy view of a pinned torch buffer) is copied asynchronously by DMA."""
     torch = require_cuda()
     eng = get_engine(device)
     t = torch.as_tensor(np.ascontiguousarray(a), dtype=dtype or torch.float64)
-    return t.to(eng.device, non_blocking=False)
+    return t.to(eng.device, non_blocking=t.is_pinned())
+
+
+_pinned_keepalive: list = []
+
+
+def pinned_like(a) -> np.ndarray:
+    """A numpy array backed by pinned (page-locked) host memory, filled with `a`
+    (the backing torch buffer is kept alive for the life of the process)."""
+    torch = require_cuda()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    buf = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    _pinned_keepalive.append(buf)
+    out = buf.numpy()
+    out[...] = a
+    return out
 
 
 def device_sort_perm(z: np.ndarray, lz: float) -> np.ndarray:
@@ -190,10 +213,18 @@ class DeviceEvaluator:
     fresh k-set with the device sampler and evaluates energy + forces, all on one
     stream with no host synchronisation.  ``capture()`` records the step as a
     CUDA graph so small systems are not launch bound.
+
+    Multi-GPU (``world > 1``, one process per GPU): particles are
+    replicated, every rank draws the SAME k-set (same seed, counter-based
+    stream), evaluates its contiguous slice of the modes plus its share of the
+    short-range home particles (rank 0 adds the k = 0 mode and the constants),
+    and the partial forces + energies -- one packed (3N + 8) fp64 buffer -- are
+    combined with ONE all-reduce (NCCL over NVLink).
     """
 
     def __init__(self, system, box, params, soe, P=None, H=None, c_q=None, seed=0, thin=10,
-                 burn_in=100, modes=None, device=None, sample=True):
+                 burn_in=100, modes=None, device=None, sample=True, rank=0, world=1,
+                 group=None):
         from .rbse2d import charge_term_sum, normalization_H
         from .soewald2d import full_sum_constants
         torch = require_cuda()
@@ -203,10 +234,13 @@ class DeviceEvaluator:
         self.alpha = params.alpha
         self.pack = _SOEPack(soe)
         self.n = system.n
+        self.rank, self.world, self.group = int(rank), int(world), group
         self.pos = torch.as_tensor(system.pos).to(dev)
         self.charge = torch.as_tensor(system.charge).to(dev)
-        self.forces = torch.empty((self.n, 3), dtype=torch.float64, device=dev)
-        self.energy = torch.zeros(8, dtype=torch.float64, device=dev)
+        # forces and energies in one buffer: the multi-GPU path all-reduces it once
+        self.packed = torch.zeros(3 * self.n + 8, dtype=torch.float64, device=dev)
+        self.forces = self.packed[:3 * self.n].view(self.n, 3)
+        self.energy = self.packed[3 * self.n:]
         self.graph = None
         Q = float(np.sum(system.charge ** 2))
         if P is None:  # deterministic full mode sum (soe_energy_forces)
@@ -230,14 +264,29 @@ class DeviceEvaluator:
             if self.sample:
                 self.eng.sample_modes(self.state, self.seed, self.alpha, box.lx, box.ly,
                                       self.thin, burn_in, 0)
+        # this rank's contiguous slice of the mode list (items are independent)
+        self.t0 = self.P * self.rank // self.world
+        self.t1 = self.P * (self.rank + 1) // self.world
 
-    def _enqueue(self):
+    def set_positions(self, pos):
+        """Replace the device positions (e.g. after an MD update), in place."""
+        self.pos.copy_(pos if hasattr(pos, "device") else
+                       _torch().as_tensor(np.asarray(pos, dtype=np.float64)))
+
+    def _enqueue(self, scan_events=None):
+        torch = _torch()
         if self.sample:
             self.eng.sample_modes(self.state, self.seed, self.alpha, self.box.lx, self.box.ly,
                                   self.thin, 0, self.P, self.modes)
+        modes = self.modes[self.t0:self.t1] if self.t1 > self.t0 else None
+        cv = self.commonv[self.t0:self.t1] if torch.is_tensor(self.commonv) else self.commonv
         self.eng.evaluate(self.pos, self.charge, self.box, self.alpha, self.params.r_c, self.soe,
-                          self.modes, self.commonv, self.charge_const, forces=self.forces,
-                          energy=self.energy, soe_pack=self.pack)
+                          modes, cv, self.charge_const, forces=self.forces, energy=self.energy,
+                          soe_pack=self.pack, shard=(self.rank, self.world),
+                          scan_events=scan_events)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
 
     def warmup(self):
         """Run one step synchronously (workspace allocation, kernel attributes)."""
@@ -246,11 +295,14 @@ class DeviceEvaluator:
         torch.cuda.synchronize(self.eng.device)
 
     def capture(self):
+        """Record one step as a CUDA graph (single GPU; small systems are launch bound)."""
         torch = _torch()
+        if self.world > 1:
+            raise RuntimeError("graph capture is single-GPU only")
         s = torch.cuda.Stream(self.eng.device)
         s.wait_stream(torch.cuda.current_stream(self.eng.device))
         with torch.cuda.stream(s):
-            self.warmup()  # outside capture: workspace, func attributes, list capacity
+            self.warmup()  # outside capture: workspace, func attributes
         torch.cuda.current_stream(self.eng.device).wait_stream(s)
         torch.cuda.synchronize(self.eng.device)
         g = torch.cuda.CUDAGraph()
@@ -259,9 +311,9 @@ class DeviceEvaluator:
         self.graph = g
         return g
 
-    def step(self):
-        if self.graph is not None:
+    def step(self, scan_events=None):
+        if self.graph is not None and scan_events is None:
             self.graph.replay()
         else:
-            self._enqueue()
+            self._enqueue(scan_events)
         return self.energy, self.forces
