@@ -48,6 +48,9 @@ def lib():
         L.oracle_zero_mode_sweep.argtypes = ([_D, _D, i64] + [_D] * 6 + [cint, dbl, dbl, _D, _D,
                                                                        cint, _D])
         L.oracle_zero_mode_sweep.restype = dbl
+        L.oracle_short_range_home.argtypes = [_D, _D, i64, dbl, dbl, dbl, dbl, dbl, i64, i64, _D,
+                                              ctypes.POINTER(cint)]
+        L.oracle_short_range_home.restype = dbl
         _lib = L
     return _lib
 
@@ -77,6 +80,36 @@ def short_range(pos, charge, box, alpha, r_c, nthreads=1):
                                  float(alpha), float(r_c), _p(f), ctypes.byref(flag),
                                  int(nthreads))
     return u, f, flag.value
+
+
+def short_range_home(pos, charge, box, alpha, r_c, h0, h1):
+    """Shard share of the short range (tests of the multi-GPU decomposition)."""
+    pos, charge = _c(pos), _c(charge)
+    f = np.zeros((len(charge), 3))
+    flag = ctypes.c_int(0)
+    u = lib().oracle_short_range_home(_p(pos), _p(charge), len(charge), box.lx, box.ly, box.lz,
+                                      float(alpha), float(r_c), int(h0), int(h1), _p(f),
+                                      ctypes.byref(flag))
+    return u, f, flag.value
+
+
+def fourier_sweep(x, y, z, q, modes, commonv, soe_w, soe_s, alpha, area, nthreads=1):
+    """soewald2d.py:85-208 on sorted arrays: (energy, forces_sorted)."""
+    x, y, z, q = (_c(a) for a in (x, y, z, q))
+    modes = _c(modes).reshape(-1, 3)
+    kx, ky, kv = (_c(modes[:, i]) for i in range(3))
+    commonv = _c(commonv)
+    w = np.asarray(soe_w, dtype=np.complex128)
+    b = alpha * np.asarray(soe_s, dtype=np.complex128)
+    wr, wi, br, bi = _c(w.real), _c(w.imag), _c(b.real), _c(b.imag)
+    n, m = len(q), len(w)
+    dr, di = np.zeros(n * m), np.zeros(n * m)
+    lib().oracle_decay_table(_p(z), n, _p(br), _p(bi), m, _p(dr), _p(di))
+    f = np.zeros((n, 3))
+    u = lib().oracle_fourier_sweep_mt(_p(x), _p(y), _p(z), _p(q), n, _p(kx), _p(ky), _p(kv),
+                                      _p(commonv), len(kv), _p(wr), _p(wi), _p(br), _p(bi), m,
+                                      float(area), _p(dr), _p(di), 1, _p(f), int(nthreads))
+    return u, f
 
 
 def energy_forces(pos, charge, box, alpha, r_c, modes, commonv, charge_const, soe_w, soe_s,

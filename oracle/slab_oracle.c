@@ -584,3 +584,45 @@ int oracle_energy_forces(const double* pos, const double* charge, int64_t n, dou
   free(perm); free(zin); free(xs); free(fs); free(fsorted);
   return flag;
 }
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU shard check (tests only): the short-range share of one rank as the
+ * device path computes it -- full-shell forces and half the pair energy for the
+ * home particles [h0, h1) of the stable cell order (ewald2d.py:141-157 cells).
+ * Summing over ranks reproduces oracle_short_range.
+ * ------------------------------------------------------------------------- */
+double oracle_short_range_home(const double* pos, const double* charge, int64_t n, double lx,
+                               double ly, double lz, double alpha, double rc, int64_t h0,
+                               int64_t h1, double* forces, int* flag) {
+  *flag = 0;
+  if (n < 2) return 0.0;
+  int64_t nc[3];
+  int64_t *start, *order;
+  build_cells(pos, n, lx, ly, lz, rc, nc, &start, &order);
+  const double rc2 = rc * rc, c = 2.0 / SQRT_PI * alpha;
+  double energy = 0.0, comp = 0.0;
+  double* tmp = (double*)calloc((size_t)(3 * n), sizeof(double));
+  for (int64_t hh = h0; hh < h1; ++hh) {
+    /* the brute path (one cell) uses input order for the home split */
+    int64_t i = nc[0] == 1 ? hh : order[hh];
+    double e_i = 0.0, c_i = 0.0;
+    double fi[3] = {0, 0, 0};
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      double ej = 0.0, cj = 0.0;
+      memset(tmp + 3 * i, 0, 3 * sizeof(double));
+      memset(tmp + 3 * j, 0, 3 * sizeof(double));
+      pair_term(pos, charge, i, j, lx, ly, alpha, rc2, c, &ej, &cj, flag, tmp);
+      e_i += ej;
+      fi[0] += tmp[3 * i]; fi[1] += tmp[3 * i + 1]; fi[2] += tmp[3 * i + 2];
+    }
+    forces[3 * i] += fi[0]; forces[3 * i + 1] += fi[1]; forces[3 * i + 2] += fi[2];
+    double yv = 0.5 * e_i - comp;
+    double t2 = energy + yv;
+    comp = (t2 - energy) - yv;
+    energy = t2;
+    (void)c_i;
+  }
+  free(tmp); free(start); free(order);
+  return energy;
+}

@@ -235,6 +235,7 @@ class DeviceEvaluator:
         self.pack = _SOEPack(soe)
         self.n = system.n
         self.rank, self.world, self.group = int(rank), int(world), group
+        self.reduce = self.world > 1  # one all-reduce of `packed` per step
         self.pos = torch.as_tensor(system.pos).to(dev)
         self.charge = torch.as_tensor(system.charge).to(dev)
         # forces and energies in one buffer: the multi-GPU path all-reduces it once
@@ -265,8 +266,8 @@ class DeviceEvaluator:
                 self.eng.sample_modes(self.state, self.seed, self.alpha, box.lx, box.ly,
                                       self.thin, burn_in, 0)
         # this rank's contiguous slice of the mode list (items are independent)
-        self.t0 = self.P * self.rank // self.world
-        self.t1 = self.P * (self.rank + 1) // self.world
+        from .sharding import mode_slice
+        self.t0, self.t1 = mode_slice(self.P, self.rank, self.world)
 
     def set_positions(self, pos):
         """Replace the device positions (e.g. after an MD update), in place."""
@@ -284,7 +285,7 @@ class DeviceEvaluator:
                           modes, cv, self.charge_const, forces=self.forces, energy=self.energy,
                           soe_pack=self.pack, shard=(self.rank, self.world),
                           scan_events=scan_events)
-        if self.world > 1:
+        if self.reduce:
             import torch.distributed as dist
             dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
 

@@ -66,7 +66,9 @@ def _axis_logq(m, ax):
     am = abs(int(m))
     if am == 0:
         return math.log(math.erf(0.5 * ax))
-    return math.log(0.5 * (math.erf((am + 0.5) * ax) - math.erf((am - 0.5) * ax)))
+    # tail-stable erfc difference (the device sampler uses the same form); mass 0 -> -inf
+    mass = 0.5 * (math.erfc((am - 0.5) * ax) - math.erfc((am + 0.5) * ax))
+    return math.log(mass) if mass > 0 else -math.inf
 
 
 class ModeSampler:
@@ -122,8 +124,12 @@ class ModeSampler:
         return idx.cpu().numpy()
 
     def batch(self, P: int) -> np.ndarray:
-        """P modes as (kx, ky, |k|) rows (kx = 2 pi mx / lx, |k| = hypot)."""
-        return self.batch_device(int(P)).cpu().numpy()
+        """P modes as (kx, ky, |k|) rows (kx = 2 pi mx / lx, |k| = hypot), formed on
+        the host from the device-drawn integer indices exactly as rbse2d.py:205-207."""
+        rec = self.batch_indices(int(P))
+        kx = 2 * np.pi * rec[:, 0] / self.box.lx
+        ky = 2 * np.pi * rec[:, 1] / self.box.ly
+        return np.column_stack([kx, ky, np.hypot(kx, ky)])
 
 
 def metropolis_batch(sampler: ModeSampler, P: int) -> np.ndarray:
@@ -176,10 +182,7 @@ def rb_energy_forces(system: ParticleSystem, box: BoxGeometry, params: EwaldPara
         H = normalization_H(alpha, box)
     if c_q is None:
         c_q = charge_term_sum(alpha, box, float(np.sum(system.charge ** 2)))
-    if isinstance(sampler, ModeSampler):
-        modes = sampler.batch_device(P).cpu().numpy()
-    else:
-        modes = sampler.batch(P)
+    modes = sampler.batch(P)
     e, f = device_evaluate(system, box, alpha, params.r_c, soe, modes, _rb_commonv(H, P, alpha),
                            c_q)
     return _breakdown(e), f

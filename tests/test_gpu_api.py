@@ -1,0 +1,354 @@
+"""GPU: the drop-in API through the CUDA library, mirroring the reference's own
+test strategy (pkg/tests/test_soewald2d.py, test_rbse2d.py, test_core.py,
+test_ewald2d.py): known answers, O(N^2) relational checks, finite-difference
+gradients, statistics of the sampler, error messages.  Every call below runs
+the sm_100a kernels (there is no CPU path)."""
+
+import math
+
+import numpy as np
+import pytest
+from scipy.special import erfc
+from scipy.stats import chisquare
+
+from helpers import StubSampler, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_2403_01521_b200 as pk
+    return pk
+
+
+def _slab_system(pk, n_pairs, box, seed, margin=0.5):
+    rng = np.random.default_rng(seed)
+    n = 2 * n_pairs
+    pos = rng.uniform([0.0, 0.0, margin], [box.lx, box.ly, box.lz - margin], size=(n, 3))
+    charge = np.array([1.0, -1.0] * n_pairs)
+    return pk.make_system(charge, np.ones(n), pos, box)
+
+
+def _numerical_gradient(f, pos, h=1e-5):
+    pos = np.array(pos, dtype=np.float64)
+    grad = np.zeros_like(pos)
+    for i in range(pos.shape[0]):
+        for d in range(3):
+            keep = pos[i, d]
+            pos[i, d] = keep + h
+            up = f(pos)
+            pos[i, d] = keep - h
+            dn = f(pos)
+            pos[i, d] = keep
+            grad[i, d] = (up - dn) / (2 * h)
+    return grad
+
+
+# --------------------------------------------------------------- recursion
+def test_recursion_known_answers(pk):
+    out = pk.recursive_pair_sum(np.array([2.0]), np.array([0.3]), np.array([1.0]), 0.5 + 0j)
+    assert out.shape == (1,) and out[0] == 0.0
+    q = np.array([1.0, 1.0])
+    th = np.array([0.7, 0.7])
+    a = pk.recursive_pair_sum(q, th, np.array([0.0, 1.0]), complex(np.log(2.0)))
+    s = np.sum(q * np.exp(1j * th) * a)
+    assert s.real == pytest.approx(0.5, rel=1e-14) and abs(s.imag) <= 1e-15
+
+
+def test_recursion_matches_reference_golden_and_direct(pk):
+    g = load_golden("units")
+    q, th, z = g["rps_q"], g["rps_theta"], g["rps_z"]
+    for j in range(3):
+        beta = complex(g[f"rps_{j}_beta"])
+        got = pk.recursive_pair_sum(q, th, z, beta)
+        want = g[f"rps_{j}_out"]
+        scale = max(1.0, float(np.max(np.abs(want))))
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-12 * scale)
+        # O(N^2) direct evaluation (reference tests/oracles.py:127-143)
+        direct = np.array([np.sum(q[:a] * np.exp(-1j * th[:a] - beta * (z[a] - z[:a])))
+                           for a in range(len(z))])
+        np.testing.assert_allclose(got, direct, rtol=0, atol=1e-12 * scale)
+
+
+def test_recursion_errors(pk):
+    with pytest.raises(ValueError, match="sorted"):
+        pk.recursive_pair_sum(np.ones(3), np.zeros(3), np.array([0.0, 2.0, 1.0]), 1.0 + 0j)
+    with pytest.raises(ValueError, match="nonnegative"):
+        pk.recursive_pair_sum(np.ones(2), np.zeros(2), np.array([0.0, 1.0]), -0.1 + 1.0j)
+
+
+# --------------------------------------------------------------- sort
+def test_sort_cases_bit_exact(pk):
+    g = load_golden("units")
+    cases = sorted({k[:-2] for k in g if k.startswith("sort_") and k.endswith("_z")})
+    for c in cases:
+        z, lz, want = g[c + "_z"], float(g[c + "_lz"]), g[c + "_perm"]
+        pos = np.column_stack([np.zeros(len(z)), np.zeros(len(z)), z])
+        s = pk.make_system(np.ones(len(z)), np.ones(len(z)), pos)
+        np.testing.assert_array_equal(pk.sort_by_z(s, lz), want, err_msg=c)
+
+
+def test_sort_negative_and_nonfinite(pk):
+    z = np.array([0.5, -1.0, 0.0, -0.0, -1.0, 2.0])
+    pos = np.column_stack([np.zeros(6), np.zeros(6), z])
+    s = pk.make_system(np.ones(6), np.ones(6), pos)
+    np.testing.assert_array_equal(pk.sort_by_z(s, 3.0), np.argsort(z, kind="stable"))
+    pos[1, 2] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        pk.sort_by_z(pk.make_system(np.ones(6), np.ones(6), pos), 3.0)
+
+
+def test_sort_large_random_bijection(pk):
+    z = np.random.default_rng(4).random(300_001) * 6.0
+    pos = np.column_stack([np.zeros_like(z), np.zeros_like(z), z])
+    s = pk.make_system(np.ones(len(z)), np.ones(len(z)), pos)
+    np.testing.assert_array_equal(pk.sort_by_z(s, 6.0), np.argsort(z, kind="stable"))
+
+
+# --------------------------------------------------------------- per-mode / zero mode
+def test_mode_energies_and_zero_mode_match_reference(pk):
+    g = load_golden("units")
+    box = pk.BoxGeometry(20.0, 20.0, 10.0)
+    s = pk.make_system(g["mode_q"], np.ones(20), g["mode_pos"], box)
+    params = pk.make_ewald_params(0.5, 3.0, box)
+    soe8 = pk.build_soe_contour(8)
+    got = np.array([pk.fourier_mode_energy_soe(s, box, params, soe8, i)
+                    for i in range(params.kmodes.shape[0])])
+    ref = g["mode_energies"]
+    np.testing.assert_allclose(got, ref, rtol=1e-10, atol=1e-12 * np.max(np.abs(ref)))
+    z0 = pk.zero_mode_energy_soe(s, box, 0.5, soe8)
+    assert z0 == pytest.approx(float(g["mode_zero"]), rel=1e-10)
+    bd, f = pk.soe_energy_forces(s, box, params, soe8)
+    assert bd.total == pytest.approx(float(g["mode_total"]), rel=1e-10)
+    np.testing.assert_allclose(f, g["mode_forces"], rtol=0,
+                               atol=1e-9 * np.max(np.abs(g["mode_forces"])))
+    np.testing.assert_allclose(pk.forces_soe(s, box, params, soe8), g["mode_forces_soe"], rtol=0,
+                               atol=1e-9 * np.max(np.abs(g["mode_forces_soe"])))
+
+
+def test_single_particle_mode_energy_is_charge_term(pk):
+    box = pk.BoxGeometry(20.0, 20.0, 10.0)
+    s = pk.make_system([1.0], [1.0], [[3.0, 4.0, 5.0]], box)
+    params = pk.make_ewald_params(0.5, 3.0, box)
+    soe8 = pk.build_soe_contour(8)
+    for idx in (0, 3):
+        k = params.kmodes[idx, 2]
+        want = np.pi * erfc(k / 1.0) / (k * box.area)
+        assert pk.fourier_mode_energy_soe(s, box, params, soe8, idx) == pytest.approx(want,
+                                                                                   rel=1e-13)
+    with pytest.raises(IndexError, match="mode index"):
+        pk.fourier_mode_energy_soe(s, box, params, soe8, params.kmodes.shape[0])
+
+
+def test_zero_mode_equal_heights(pk):
+    box = pk.BoxGeometry(12.0, 9.0, 6.0)
+    charge = np.array([1.0, -2.0, 1.0])
+    pos = np.array([[1.0, 1.0, 2.5], [4.0, 7.0, 2.5], [9.0, 3.0, 2.5]])
+    s = pk.make_system(charge, np.ones(3), pos, box)
+    soe8 = pk.build_soe_contour(8)
+    alpha = 0.7
+    g0 = complex(np.sum(soe8.w)).real / (alpha * math.sqrt(math.pi))
+    want = (-2.0 * np.pi / box.area) * -3.0 * g0 - math.sqrt(math.pi) * 6.0 / (alpha * box.area)
+    assert pk.zero_mode_energy_soe(s, box, alpha, soe8) == pytest.approx(want, rel=1e-13)
+
+
+def test_presorted_paths_match_full(pk):
+    box = pk.BoxGeometry(20.0, 20.0, 10.0)
+    s = _slab_system(pk, 15, box, 5)
+    params = pk.make_ewald_params(0.5, 3.0, box)
+    soe = pk.build_soe_contour(16)
+    perm = np.argsort(s.pos[:, 2], kind="stable")
+    pre = (s.pos[perm, 0], s.pos[perm, 1], s.pos[perm, 2], s.charge[perm])
+    a = pk.fourier_energy_soe(s, box, params, soe)
+    b = pk.fourier_energy_soe(s, box, params, soe, _presorted=pre)
+    assert a == pytest.approx(b, rel=1e-12)
+    za = pk.zero_mode_energy_soe(s, box, 0.5, soe)
+    zb = pk.zero_mode_energy_soe(s, box, 0.5, soe, _presorted=pre)
+    assert za == pytest.approx(zb, rel=1e-12)
+    bad = (pre[0], pre[1], pre[2][::-1].copy(), pre[3])
+    with pytest.raises(ValueError, match="sorted ascending"):
+        pk.fourier_energy_soe(s, box, params, soe, _presorted=bad)
+
+
+# --------------------------------------------------------------- forces
+def test_forces_are_exact_gradient(pk):
+    box = pk.BoxGeometry(10.0, 10.0, 6.0)
+    s = _slab_system(pk, 8, box, 41, margin=0.8)
+    params = pk.make_ewald_params(0.8, 3.0, box)
+    soe8 = pk.build_soe_contour(8)
+    _, forces = pk.soe_energy_forces(s, box, params, soe8)
+
+    def energy(pos):
+        moved = pk.make_system(s.charge, s.mass, pos, box)
+        return pk.total_energy_soe(moved, box, params, soe8).total
+
+    grad = _numerical_gradient(energy, s.pos)
+    np.testing.assert_allclose(forces, -grad, rtol=0, atol=1e-5 * np.max(np.abs(forces)))
+
+
+def test_two_particle_forces_antisymmetric(pk):
+    box = pk.BoxGeometry(10.0, 10.0, 6.0)
+    s = pk.make_system([1.0, -1.0], np.ones(2), [[1.2, 3.4, 1.7], [6.8, 5.1, 4.2]], box)
+    f = pk.forces_soe(s, box, pk.make_ewald_params(0.8, 3.0, box), pk.build_soe_contour(8))
+    np.testing.assert_allclose(f[0], -f[1], rtol=0, atol=5e-14 * np.max(np.abs(f)))
+
+
+def test_rb_force_estimate_is_gradient_of_frozen_batch(pk):
+    box = pk.BoxGeometry(10.0, 10.0, 5.0, sigma_top=0.003, sigma_bot=-0.001)
+    s = _slab_system(pk, 5, box, 63, margin=0.8)
+    alpha = 0.8
+    soe8 = pk.build_soe_contour(8)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        H = pk.normalization_H(alpha, box)
+    modes = pk.ModeSampler(alpha, box, seed=9).batch(8)
+    forces = pk.rb_force_estimate(s, box, alpha, soe8, modes, H)
+
+    def energy(pos):
+        m = pk.make_system(s.charge, s.mass, pos, box)
+        return (pk.rb_energy_estimate(m, box, alpha, soe8, modes, H, c_q=0.0)
+                + pk.zero_mode_energy_soe(m, box, alpha, soe8) + pk.slab_energy_forces(m, box)[0])
+
+    grad = _numerical_gradient(energy, s.pos)
+    np.testing.assert_allclose(forces, -grad, rtol=0, atol=1e-5 * np.max(np.abs(forces)))
+
+
+# --------------------------------------------------------------- short range
+def test_short_range_known_answers_and_errors(pk):
+    box = pk.BoxGeometry(100.0, 100.0, 10.0)
+    s = pk.make_system([1.0, -1.0], np.ones(2), [[1.0, 1.0, 1.0], [4.0, 5.0, 1.0]], box)
+    u, f = pk.short_range_energy_forces(s, box, 0.1, 40.0)
+    assert u == pytest.approx(-erfc(0.5) / 5.0, rel=1e-13)
+    np.testing.assert_allclose(f[0], -f[1], rtol=1e-14)
+    empty = pk.make_system(np.zeros(0), np.zeros(0), np.zeros((0, 3)), box)
+    u0, f0 = pk.short_range_energy_forces(empty, box, 1.0, 3.0)
+    assert u0 == 0.0 and f0.shape == (0, 3)
+    dup = pk.make_system([1.0, 1.0], np.ones(2), [[1, 1, 1], [1, 1, 1]], box)
+    with pytest.raises(ValueError, match="coincident"):
+        pk.short_range_energy_forces(dup, box, 1.0, 3.0)
+    with pytest.raises(ValueError, match="half the in-plane"):
+        pk.short_range_energy_forces(s, pk.BoxGeometry(10.0, 10.0, 10.0), 1.0, 5.5)
+
+
+def test_short_range_dense_walls_matches_oracle(pk):
+    # cfg3-like wall layers: ~10x mean density in thin z layers (load imbalance)
+    from oracle import oracle as O
+    from paper_2403_01521_b200.configs import make_workload
+    wl = make_workload("cfg3")
+    u, f = pk.short_range_energy_forces(wl.system, wl.box, wl.alpha, wl.params().r_c)
+    g = load_golden("cfg3")
+    assert u == pytest.approx(float(g["u_s_alone"]), rel=1e-10)
+    idx = g["sample_idx"]
+    np.testing.assert_allclose(f[idx], g["f_short"], rtol=0,
+                               atol=1e-9 * np.max(np.abs(g["f_short"])))
+
+
+# --------------------------------------------------------------- sampler
+def test_sampler_statistics(pk):
+    box = pk.BoxGeometry(100.0, 100.0, 10.0)
+    smp = pk.ModeSampler(0.3, box, seed=11)
+    n_draw = 20000
+    rec = smp.batch_indices(n_draw)
+    assert not np.any((rec[:, 0] == 0) & (rec[:, 1] == 0))
+    assert smp.acceptance_rate > 0.9
+    ax = smp.axx
+    mmax = 30
+    grid = np.arange(-mmax, mmax + 1)
+    wx = np.exp(-(ax * grid) ** 2)
+    weight = np.outer(wx, wx)
+    weight[mmax, mmax] = 0.0
+    counts = np.zeros_like(weight)
+    inside = (np.abs(rec[:, 0]) <= mmax) & (np.abs(rec[:, 1]) <= mmax)
+    np.add.at(counts, (rec[inside, 0] + mmax, rec[inside, 1] + mmax), 1.0)
+    expected = n_draw * weight / weight.sum()
+    keep = expected >= 5.0
+    obs = np.append(counts[keep], n_draw - counts[keep].sum())
+    exp = np.append(expected[keep], n_draw - expected[keep].sum())
+    _, p = chisquare(obs, exp * obs.sum() / exp.sum())
+    assert p > 1e-3
+    # the reference chain's own draws follow the same law (different RNG stream)
+    g = load_golden("units")
+    ref = g["sampler_idx_a03_L100_seed11"]
+    for arr in (rec, ref):
+        assert abs(np.mean(np.abs(arr[:, 0])) - np.mean(np.abs(ref[:, 0]))) < 0.25
+
+
+def test_sampler_determinism_and_scaling(pk):
+    box = pk.BoxGeometry(80.0, 120.0, 10.0)
+    a = pk.ModeSampler(0.25, box, seed=4).batch_indices(300)
+    b = pk.ModeSampler(0.25, box, seed=4).batch_indices(300)
+    c = pk.ModeSampler(0.25, box, seed=5).batch_indices(300)
+    np.testing.assert_array_equal(a, b)
+    assert np.any(a != c)
+    kb = pk.ModeSampler(0.25, box, seed=4).batch(300)
+    np.testing.assert_array_equal(kb[:, 0], 2 * np.pi * a[:, 0] / box.lx)
+    np.testing.assert_array_equal(kb[:, 1], 2 * np.pi * a[:, 1] / box.ly)
+    np.testing.assert_array_equal(kb[:, 2], np.hypot(kb[:, 0], kb[:, 1]))
+    with pytest.raises(ValueError, match="thin"):
+        pk.ModeSampler(0.3, box, thin=0)
+    with pytest.raises(ValueError, match="batch size"):
+        pk.metropolis_batch(pk.ModeSampler(0.3, box, seed=5), 0)
+
+
+def test_rb_estimator_unbiased_and_variance_scaling(pk):
+    box = pk.BoxGeometry(10.0, 10.0, 5.0)
+    s = _slab_system(pk, 25, box, 61)
+    params = pk.make_ewald_params(0.8, 4.0, box)
+    soe8 = pk.build_soe_contour(8)
+    est = pk.run_many_batches(s, box, params, soe8, n_batches=3000, P=16, seed=2)
+    truth = pk.total_energy_soe(s, box, params, soe8).total
+    d = pk.variance_diagnostics(est)
+    assert abs(d["mean"] - truth) <= 3.0 * d["stderr"]
+    s2 = _slab_system(pk, 25, box, 62)
+    e16 = pk.run_many_batches(s2, box, params, soe8, n_batches=4000, P=16, seed=3)
+    e64 = pk.run_many_batches(s2, box, params, soe8, n_batches=4000, P=64, seed=4)
+    ratio = np.var(e64, ddof=1) / np.var(e16, ddof=1)
+    assert 0.2 <= ratio <= 0.32
+
+
+def test_single_particle_rb_estimate_is_charge_constant(pk):
+    box = pk.BoxGeometry(10.0, 10.0, 5.0)
+    s = pk.make_system([1.0], [1.0], [[2.0, 3.0, 2.5]], box)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        H = pk.normalization_H(0.8, box)
+    c_q = pk.charge_term_sum(0.8, box, 1.0)
+    smp = pk.ModeSampler(0.8, box, seed=6)
+    soe8 = pk.build_soe_contour(8)
+    assert all(pk.rb_energy_estimate(s, box, 0.8, soe8, smp.batch(16), H) == c_q
+               for _ in range(3))
+
+
+# --------------------------------------------------------------- device evaluator
+def test_graph_replay_and_shard_sum_equal_single_eval(pk):
+    import torch
+    from paper_2403_01521_b200.configs import make_workload
+    from paper_2403_01521_b200.engine import DeviceEvaluator
+    wl = make_workload("small_2000")
+    soe = pk.build_soe_contour(wl.m)
+    g = load_golden("small_2000")
+    kw = dict(P=wl.P, H=float(g["H"]), c_q=float(g["c_q"]), modes=g["modes"])
+    ev = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, **kw)
+    ev.step()
+    e1, f1 = ev.energy.clone(), ev.forces.clone()
+    ev.capture()
+    ev.step()
+    torch.cuda.synchronize()
+    assert torch.equal(e1, ev.energy) and torch.equal(f1, ev.forces)
+    # two shards evaluated one after the other on this GPU, summed by hand
+    tot = torch.zeros_like(ev.packed)
+    for r in range(2):
+        evr = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, rank=r, world=1, **kw)
+        evr.rank, evr.world, evr.reduce = r, 2, False   # shard, no collective
+        from paper_2403_01521_b200.sharding import mode_slice
+        evr.t0, evr.t1 = mode_slice(evr.P, r, 2)
+        evr.step()
+        tot += evr.packed
+    torch.cuda.synchronize()
+    e, f = tot[3 * wl.n:].cpu().numpy(), tot[:3 * wl.n].view(wl.n, 3).cpu().numpy()
+    for val, key in zip(e, ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps")):
+        assert val == pytest.approx(float(g[key]), rel=1e-10), key
+    np.testing.assert_allclose(f, g["forces"], rtol=0, atol=1e-9 * float(g["fmax"]))

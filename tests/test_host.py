@@ -1,0 +1,144 @@
+"""CPU: host-side logic of the drop-in API (per-run setup; no device needed).
+
+Mirrors the reference's own known-answer / relational tests for the same
+functions (pkg/tests/test_core.py, test_soe.py, test_rbse2d.py) and pins the
+host outputs against the reference's values frozen in tests/golden.
+"""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from helpers import load_golden
+import paper_2403_01521_b200 as pk
+from paper_2403_01521_b200 import soe as soe_mod
+from paper_2403_01521_b200.configs import make_workload
+from paper_2403_01521_b200.rbse2d import _axis_logq
+
+H_BRUTE_03_100 = 285.47889756541156   # reference tests/test_rbse2d.py:28
+Q0_PROPOSAL = 0.05902784737600369     # erf(pi/60)
+PROPOSAL_STD = 6.7523723711782955
+
+
+def test_box_geometry_validation_and_area():
+    b = pk.BoxGeometry(2.0, 3.0, 4.0)
+    assert b.area == 6.0 and b.volume == 24.0
+    for dims in [(0, 1, 1), (1, -1, 1), (1, 1, 0)]:
+        with pytest.raises(ValueError, match="positive"):
+            pk.BoxGeometry(*dims)
+    with pytest.raises(ValueError, match="finite"):
+        pk.BoxGeometry(1, 1, 1, sigma_top=float("nan"))
+
+
+def test_make_system_wraps_xy_and_accepts_box_in_fourth_slot():
+    box = pk.BoxGeometry(10.0, 10.0, 5.0)
+    pos = np.array([[12.0, -3.0, 1.0], [5.0, 5.0, 5.0]])
+    s1 = pk.make_system([1.0, -1.0], [1.0, 1.0], pos, box=box)
+    s2 = pk.make_system([1.0, -1.0], [1.0, 1.0], pos, box)  # reference tests' call form
+    np.testing.assert_array_equal(s1.pos, s2.pos)
+    np.testing.assert_allclose(s1.pos[0], [2.0, 7.0, 1.0])
+    with pytest.raises(ValueError, match="lie in"):
+        pk.make_system([1.0], [1.0], [[1.0, 1.0, 6.0]], box)
+    with pytest.raises(ValueError, match="shapes"):
+        pk.make_system([1.0, 2.0], [1.0], [[1.0, 1.0, 1.0]])
+    with pytest.raises(ValueError, match="positive"):
+        pk.make_system([1.0], [0.0], [[1.0, 1.0, 1.0]])
+
+
+def test_kmodes_match_reference_full_mode_set():
+    g = load_golden("cfg1")
+    wl = make_workload("cfg1")
+    km = wl.params().kmodes
+    assert km.shape == (792, 3)
+    np.testing.assert_array_equal(km, g["modes"])
+    # closed under k -> -k and excludes the origin
+    s = {(round(a, 12), round(b, 12)) for a, b, _ in km}
+    assert all((round(-a, 12), round(-b, 12)) in s for a, b, _ in km)
+    assert not np.any(km[:, 2] == 0)
+
+
+def test_ewald_params_and_alpha_laws():
+    box = pk.BoxGeometry(100.0, 100.0, 100.0)
+    assert pk.choose_alpha(1000, box, mode="linear") == pytest.approx(0.1, rel=1e-12)
+    p = pk.make_ewald_params(0.5, 4.0, box)
+    assert p.r_c == 8.0 and p.k_c == 4.0
+    with pytest.raises(ValueError, match="alpha must be positive"):
+        pk.make_ewald_params(0.0, 4.0, box)
+    with pytest.raises(ValueError):
+        pk.choose_alpha(10, box, mode="nope")
+
+
+@pytest.mark.parametrize("m", [8, 16, 24])
+def test_soe_contour_bitwise_equal_to_reference(m):
+    g = load_golden({8: "units", 16: "cfg2", 24: "cfg3"}[m]) if m != 8 else None
+    soe = pk.build_soe_contour(m)
+    assert soe_mod.is_conjugate_paired(soe)
+    if g is not None:
+        np.testing.assert_array_equal(soe.w, g["soe_w"])
+        np.testing.assert_array_equal(soe.s, g["soe_s"])
+    assert soe.eps_certified <= soe_mod.ACHIEVED_EPS[m] * 1.5
+
+
+def test_soe_table_roundtrip(tmp_path):
+    soe = pk.build_soe_contour(8)
+    path = tmp_path / "t.csv"
+    pk.save_soe_table(path, soe)
+    back = pk.load_soe_table(path)
+    np.testing.assert_array_equal(back.w, soe.w)
+    np.testing.assert_array_equal(back.s, soe.s)
+
+
+def test_normalization_H_and_charge_term_match_reference_table():
+    g = load_golden("units")
+    for a, lx, ly, Hr, cqr in g["H_cq_table"]:
+        box = pk.BoxGeometry(lx, ly, 10.0)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            assert pk.normalization_H(a, box) == pytest.approx(Hr, rel=1e-14)
+        assert pk.charge_term_sum(a, box, 50.0) == pytest.approx(cqr, rel=1e-14)
+    assert pk.normalization_H(0.3, pk.BoxGeometry(100.0, 100.0, 10.0)) == pytest.approx(
+        H_BRUTE_03_100, rel=1e-9)
+    with pytest.warns(UserWarning, match="Fourier modes"):
+        pk.normalization_H(0.01, pk.BoxGeometry(100.0, 100.0, 10.0))
+    with pytest.raises(ValueError, match="positive"):
+        pk.normalization_H(0.0, pk.BoxGeometry(100.0, 100.0, 10.0))
+
+
+def test_proposal_constants():
+    ax = math.pi / (0.3 * 100.0)
+    assert 1.0 / (ax * math.sqrt(2.0)) == pytest.approx(PROPOSAL_STD, rel=1e-12)
+    assert math.exp(_axis_logq(0, ax)) == pytest.approx(Q0_PROPOSAL, rel=1e-12)
+    total = sum(math.exp(_axis_logq(m, ax)) for m in range(-60, 61))
+    assert total == pytest.approx(1.0, abs=1e-12)
+
+
+def test_variance_diagnostics_and_csv(tmp_path):
+    d = pk.variance_diagnostics(np.full(10, 2.5))
+    assert d["mean"] == 2.5 and d["stderr"] == 0.0
+    with pytest.raises(ValueError, match="two batches"):
+        pk.variance_diagnostics(np.array([1.0]))
+    est = np.random.default_rng(5).normal(size=20)
+    path = tmp_path / "diag.csv"
+    pk.write_diagnostics_csv(path, est)
+    lines = path.read_text().strip().split("\n")
+    assert lines[0] == "batch_index,estimate,running_mean,running_stderr"
+    assert len(lines) == 21
+
+
+def test_neutrality():
+    box = pk.BoxGeometry(10.0, 10.0, 5.0)
+    s = pk.make_system([1.0, -1.0], [1.0, 1.0], [[1, 1, 1], [2, 2, 2]], box)
+    assert pk.validate_neutrality(s, box)[0]
+    s = pk.make_system([1.0], [1.0], [[1, 1, 1]], box)
+    assert not pk.validate_neutrality(s, box)[0]
+
+
+def test_workload_generators_are_neutral_and_regenerate():
+    for name in ("cfg1", "cfg2", "cfg3", "small_600"):
+        wl = make_workload(name)
+        assert abs(wl.system.charge.sum()) < 1e-9
+        assert wl.system.pos[:, 2].min() >= 0 and wl.system.pos[:, 2].max() <= wl.box.lz
+        wl2 = make_workload(name)
+        np.testing.assert_array_equal(wl.system.pos, wl2.system.pos)
