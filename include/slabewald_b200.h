@@ -52,7 +52,9 @@ enum {
 /* device status word bits (written by kernels, read by the host after sync) */
 enum {
   SLAB_STATUS_COINCIDENT = 1, /* d2 < 1e-24 pair: ewald2d.py:207-209,301-302 */
-  SLAB_STATUS_SINGULAR = 2    /* |b_l - k| < 2e-6 k: soewald2d.py:118-121 (analytic branch) */
+  SLAB_STATUS_SINGULAR = 2,   /* |b_l - k| < 2e-6 k: soewald2d.py:118-121 (analytic branch) */
+  SLAB_STATUS_NBR_OVERFLOW = 4 /* a short-range neighbour row exceeded its capacity: results
+                                  are invalid; raise it (slab_ctx_neighbor_capacity) and rerun */
 };
 
 typedef struct SlabBox {
@@ -110,6 +112,11 @@ int slab_ctx_create(SlabCtx** out);
 int slab_ctx_destroy(SlabCtx* ctx);
 const char* slab_last_error(void);
 const char* slab_version(void);
+
+/* Short-range neighbour rows: grow-only minimum capacity, and the longest row
+ * seen by the last short-range run (synchronous read) for SLAB_STATUS_NBR_OVERFLOW. */
+int slab_ctx_neighbor_capacity(SlabCtx* ctx, int capacity);
+int slab_ctx_last_max_neighbors(SlabCtx* ctx, int* out);
 
 /* core.py:203-208: stable ascending-z permutation; z read as d_z[i*stride]. */
 int slab_sort_by_z(SlabCtx* ctx, const double* d_z, int64_t stride, int64_t n, int64_t* d_perm,

@@ -21,11 +21,13 @@ SLAB_ERR_UNSUPPORTED = 3
 SLAB_ERR_NOMEM = 4
 SLAB_STATUS_COINCIDENT = 1
 SLAB_STATUS_SINGULAR = 2
+SLAB_STATUS_NBR_OVERFLOW = 4
 
 EXPORTED = (
     "slab_ctx_create", "slab_ctx_destroy", "slab_last_error", "slab_version",
     "slab_sort_by_z", "slab_fourier_sweep", "slab_zero_mode_sweep", "slab_short_range",
     "slab_sample_modes", "slab_evaluate", "slab_recursive_pair_sum", "slab_fp64_peak",
+    "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors",
 )
 
 
@@ -100,6 +102,8 @@ def load():
     lib.slab_evaluate.argtypes = [vp, ctypes.POINTER(SlabEvalArgs), vp]
     lib.slab_recursive_pair_sum.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, vp, vp]
     lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
+    lib.slab_ctx_neighbor_capacity.argtypes = [vp, cint]
+    lib.slab_ctx_last_max_neighbors.argtypes = [vp, ctypes.POINTER(cint)]
 
     for name in EXPORTED:
         if name not in ("slab_last_error", "slab_version"):

@@ -36,6 +36,8 @@ struct SlabCtx {
   int* status = nullptr;
   double* sampler_scratch = nullptr;
   int64_t sampler_cap = 0;
+  int kcap_min = 0;        // learned short-range neighbour-row capacity (grow-only)
+  int* d_maxnn = nullptr;  // longest neighbour row of the last short-range run
 };
 
 namespace {
@@ -57,6 +59,8 @@ int ensure_arena(SlabCtx* c, size_t bytes) {
   if (c->small == nullptr) {
     CK(cudaMalloc(&c->small, 1024 * sizeof(double)));
     CK(cudaMalloc(&c->status, 16 * sizeof(int)));
+    CK(cudaMalloc(&c->d_maxnn, sizeof(int)));
+    CK(cudaMemset(c->d_maxnn, 0, sizeof(int)));
   }
   if (bytes <= c->arena_bytes) return SLAB_OK;
   if (c->arena) {
@@ -185,7 +189,21 @@ int slab_ctx_destroy(SlabCtx* ctx) {
   if (ctx->small) cudaFree(ctx->small);
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->sampler_scratch) cudaFree(ctx->sampler_scratch);
+  if (ctx->d_maxnn) cudaFree(ctx->d_maxnn);
   delete ctx;
+  return SLAB_OK;
+}
+
+int slab_ctx_neighbor_capacity(SlabCtx* ctx, int capacity) {
+  if (!ctx || capacity < 0) return fail(SLAB_ERR_ARG, "bad capacity");
+  if (capacity > ctx->kcap_min) ctx->kcap_min = (capacity + 7) / 8 * 8;
+  return SLAB_OK;
+}
+
+int slab_ctx_last_max_neighbors(SlabCtx* ctx, int* out) {
+  if (!ctx || !out) return fail(SLAB_ERR_ARG, "bad arguments");
+  *out = 0;
+  if (ctx->d_maxnn) CK(cudaMemcpy(out, ctx->d_maxnn, sizeof(int), cudaMemcpyDeviceToHost));
   return SLAB_OK;
 }
 
@@ -274,10 +292,12 @@ int slab_short_range(SlabCtx* ctx, const double* d_pos, const double* d_charge, 
   if (!(alpha > 0) || !(r_c > 0)) return fail(SLAB_ERR_ARG, "alpha and r_c must be positive");
   cudaStream_t st = (cudaStream_t)stream;
   auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, r_c);
+  if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;
   int rc = ensure_arena(ctx, slab::short_work_bytes(sp) + 1024);
   if (rc) return rc;
+  CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
   CK(slab::short_run(sp, ctx->arena, d_pos, d_charge, box.lx, box.ly, box.lz, alpha, r_c,
-                     d_forces, d_energy, d_status, 0, n, st));
+                     d_forces, d_energy, d_status, 0, n, ctx->d_maxnn, st));
   return SLAB_OK;
 }
 
@@ -331,6 +351,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh);
   auto zp = slab::zero_plan(n, sh.mh);
   auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, a->r_c);
+  if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;
   const size_t N = (size_t)(n > 0 ? n : 1);
   size_t bytes = sorted_bytes(n, sh.mh, fp, zp, true) + pad(24 * N) +
                  (a->skip_short_range ? 0 : pad(slab::short_work_bytes(sp))) + 8192;
@@ -349,6 +370,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
 
   CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
   CK(cudaMemsetAsync(ctx->small, 0, 8 * sizeof(double), st));
+  CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
   int32_t* perm = nullptr;
   if (n > 0) {
     CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm));
@@ -361,7 +383,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (!a->skip_short_range) {
     const int64_t h0 = n * srank / scount, h1 = n * (srank + 1) / scount;
     CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
-                       a->r_c, fshort, u_s, ctx->status, h0, h1, st));
+                       a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, st));
   }
   const bool forces = a->want_forces && n > 0;
   if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, st));

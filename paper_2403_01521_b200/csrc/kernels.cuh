@@ -97,13 +97,14 @@ struct ShortPlan {
   int64_t ncell;
   int jsplit;     // brute path: j-range splits
   int64_t nblk;   // energy partial count
+  int kcap;       // neighbour-row capacity (multiple of 8)
 };
 ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc);
 size_t short_work_bytes(const ShortPlan& p);
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
                       double* energy_out, int* status, int64_t home_begin, int64_t home_end,
-                      cudaStream_t st);
+                      int* maxnn_out, cudaStream_t st);
 
 // ---------------------------------------------------------------- assemble.cu
 cudaError_t assemble_forces(int64_t n, const int32_t* perm, const double* qs,

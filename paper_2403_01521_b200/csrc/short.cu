@@ -45,12 +45,12 @@ __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi,
     flag = 1;
     return;
   }
-  const double d = sqrt(d2);
+  const double inv_d = rsqrt(d2);  // one MUFU.RSQ64H + Newton instead of sqrt and a divide
+  const double d = d2 * inv_d;
   const double qq = qi * qj;
   const double x = alpha * d;
   double e, g;  // erfc(x) and the force Gaussian e^{-x^2} share one exp
   erfc_gauss(x, etab, &e, &g);
-  const double inv_d = 1.0 / d;
   acc.e = fma(qq * e, inv_d, acc.e);
   const double fmag = qq * (e * inv_d + c * g) * (inv_d * inv_d);
   acc.fx = fma(fmag, dx, acc.fx);
@@ -99,83 +99,115 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
 }
 
 constexpr int kSRThreads = 128;
-constexpr int kQ = 32;  // per-thread queue of screened candidates (16 KB per block)
+constexpr int kStage = 8;  // neighbour indices staged per thread = one 32-byte sector
 
-__global__ void __launch_bounds__(kSRThreads) short_cells_kernel(
-    const double4* __restrict__ cp, const float4* __restrict__ cpf,
-    const int32_t* __restrict__ order, const uint32_t* __restrict__ skey,
+// Pass 1: neighbour rows.  One thread per home particle (cell-sorted: a warp
+// scans the same 27 cells, so candidate loads are broadcasts), conservative
+// fp32 distance screen, hits staged 8 at a time in shared memory and written
+// as full 32-byte sectors into the particle's row nbr[(a - a_begin) * kcap + k].
+__global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
+    const float4* __restrict__ cpf, const uint32_t* __restrict__ skey,
     const int32_t* __restrict__ start, int64_t a_begin, int64_t a_end, int ncx, int ncy, int ncz,
-    double lx, double ly, double alpha, double rc2, float rc2f, double* __restrict__ forces,
-    double* __restrict__ eblk, int* __restrict__ status) {
-  extern __shared__ int32_t queue_raw[];
-  int32_t (*queue)[kSRThreads] = reinterpret_cast<int32_t (*)[kSRThreads]>(queue_raw);
-  __shared__ double etab[SLAB_ERFCX_NINT * kErfcxStride];
-  load_erfcx_table(etab);
-  __syncthreads();
-  const int tid = threadIdx.x;
-  const int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + tid;
-  const bool active = a < a_end;
-  const double c = kTwoOverSqrtPi * alpha;
-  const double ilx = 1.0 / lx, ily = 1.0 / ly;
-  const float lxf = (float)lx, lyf = (float)ly, ilxf = 1.0f / lxf, ilyf = 1.0f / lyf;
-  const float4 pf = active ? cpf[a] : make_float4(0.f, 0.f, 0.f, 0.f);
-  const double4 pd = active ? cp[a] : make_double4(0.0, 0.0, 0.0, 0.0);
-  const int cid = active ? (int)skey[a] : 0;
+    float lxf, float lyf, float rc2f, int kcap, int32_t* __restrict__ nbr,
+    int32_t* __restrict__ nn, int* __restrict__ maxnn, int* __restrict__ status) {
+  __shared__ int4 stage[kSRThreads][kStage / 4];
+  const int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x;
+  if (a >= a_end) return;
+  const int cid = (int)skey[a];
   const int cz = cid % ncz, cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
-  PairAcc acc{0.0, 0.0, 0.0, 0.0};
-  int flag = 0, cnt = 0;
-  auto drain = [&]() {
-    const int m = __reduce_max_sync(0xffffffffu, cnt);
-    for (int k = 0; k < m; ++k) {
-      if (k < cnt) {
-        const double4 pj = cp[queue[k][tid]];
-        pair_accumulate(pd.x, pd.y, pd.z, pd.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
-                        rc2, c, etab, acc, flag);
-      }
-    }
-    cnt = 0;
-  };
+  const float4 pi = cpf[a];
+  const float ilx = 1.0f / lxf, ily = 1.0f / lyf;
+  int32_t* st = reinterpret_cast<int32_t*>(stage[threadIdx.x]);
+  int32_t* row = nbr + (a - a_begin) * (int64_t)kcap;
+  int cnt = 0;
   for (int off = 0; off < 27; ++off) {
     const int dxc = off / 9 - 1, dyc = (off / 3) % 3 - 1, dzc = off % 3 - 1;
     const int nz = cz + dzc;
-    int b0 = 0, len = 0;
-    if (active && nz >= 0 && nz < ncz) {
-      const int nx = (cx + dxc + ncx) % ncx, ny = (cy + dyc + ncy) % ncy;
-      const int nid = (nx * ncy + ny) * ncz + nz;
-      b0 = start[nid];
-      len = start[nid + 1] - b0;
-    }
-    const int maxlen = __reduce_max_sync(0xffffffffu, len);
-    for (int it = 0; it < maxlen; ++it) {
-      if (it < len) {
-        const int jj = b0 + it;
-        const float4 pj = cpf[jj];
-        float dx = pf.x - pj.x, dy = pf.y - pj.y;
-        const float dz = pf.z - pj.z;
-        dx -= lxf * rintf(dx * ilxf);
-        dy -= lyf * rintf(dy * ilyf);
-        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        if (d2 <= rc2f && jj != a) queue[cnt++][tid] = jj;
+    if (nz < 0 || nz >= ncz) continue;
+    const int nx = (cx + dxc + ncx) % ncx, ny = (cy + dyc + ncy) % ncy;
+    const int nid = (nx * ncy + ny) * ncz + nz;
+    const int b0 = start[nid], b1 = start[nid + 1];
+#pragma unroll 4
+    for (int jj = b0; jj < b1; ++jj) {
+      const float4 pj = cpf[jj];
+      float dx = pi.x - pj.x, dy = pi.y - pj.y;
+      const float dz = pi.z - pj.z;
+      dx -= lxf * rintf(dx * ilx);
+      dy -= lyf * rintf(dy * ily);
+      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      if (d2 <= rc2f && jj != a) {
+        st[cnt & (kStage - 1)] = jj;
+        ++cnt;
+        if ((cnt & (kStage - 1)) == 0 && cnt <= kcap) {
+          int4* dst = reinterpret_cast<int4*>(row + cnt - kStage);
+          dst[0] = stage[threadIdx.x][0];
+          dst[1] = stage[threadIdx.x][1];
+        }
       }
-      if (__any_sync(0xffffffffu, cnt == kQ)) drain();
     }
   }
-  drain();
-  if (active) {
+  const int tail = cnt & (kStage - 1);
+  if (cnt <= kcap)
+    for (int k = 0; k < tail; ++k) row[cnt - tail + k] = st[k];
+  nn[a - a_begin] = cnt < kcap ? cnt : kcap;
+  if (cnt > kcap) {
+    atomicOr(status, SLAB_STATUS_NBR_OVERFLOW_DEV);
+    atomicMax(maxnn, cnt);
+  }
+}
+
+// Pass 2: one thread per home particle over its own row (rows have ~equal
+// length, so the fp64 pair work runs on nearly full warps); four neighbours in
+// flight per iteration.  Each force is owned by one thread: deterministic.
+__global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
+    const double4* __restrict__ cp, const int32_t* __restrict__ order,
+    const int32_t* __restrict__ nbr, const int32_t* __restrict__ nn, int64_t a_begin,
+    int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2,
+    double* __restrict__ forces, double* __restrict__ eblk, int* __restrict__ status) {
+  __shared__ double etab[SLAB_ERFCX_NINT * kErfcxStride];
+  __shared__ double red[kSRThreads];
+  load_erfcx_table(etab);
+  __syncthreads();
+  const int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x;
+  const double c = kTwoOverSqrtPi * alpha;
+  const double ilx = 1.0 / lx, ily = 1.0 / ly;
+  PairAcc acc{0.0, 0.0, 0.0, 0.0};
+  int flag = 0;
+  if (a < a_end) {
+    const double4 pi = cp[a];
+    const int cnt = nn[a - a_begin];
+    const int32_t* row = nbr + (a - a_begin) * (int64_t)kcap;
+    int k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+      const int4 j4 = *reinterpret_cast<const int4*>(row + k);
+      const double4 p0 = cp[j4.x], p1 = cp[j4.y], p2 = cp[j4.z], p3 = cp[j4.w];
+      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p0.x, p0.y, p0.z, p0.w, lx, ly, ilx, ily, alpha,
+                      rc2, c, etab, acc, flag);
+      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p1.x, p1.y, p1.z, p1.w, lx, ly, ilx, ily, alpha,
+                      rc2, c, etab, acc, flag);
+      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p2.x, p2.y, p2.z, p2.w, lx, ly, ilx, ily, alpha,
+                      rc2, c, etab, acc, flag);
+      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p3.x, p3.y, p3.z, p3.w, lx, ly, ilx, ily, alpha,
+                      rc2, c, etab, acc, flag);
+    }
+    for (; k < cnt; ++k) {
+      const double4 pj = cp[row[k]];
+      pair_accumulate(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
+                      rc2, c, etab, acc, flag);
+    }
     const int64_t i = order[a];
     forces[3 * i + 0] = acc.fx;
     forces[3 * i + 1] = acc.fy;
     forces[3 * i + 2] = acc.fz;
   }
   if (flag) atomicOr(status, SLAB_STATUS_COINCIDENT_DEV);
-  __shared__ double red[kSRThreads];
-  red[tid] = acc.e;
+  red[threadIdx.x] = acc.e;
   __syncthreads();
-  for (int s = kSRThreads / 2; s > 0; s >>= 1) {
-    if (tid < s) red[tid] += red[tid + s];
+  for (int w = kSRThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (tid == 0) eblk[blockIdx.x] = red[0];
+  if (threadIdx.x == 0) eblk[blockIdx.x] = red[0];
 }
 
 // all pairs (ncx < 3 or ncy < 3): grid (i tiles, j splits)
@@ -259,6 +291,12 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc) {
   p.jsplit = p.brute ? (js < 1 ? 1 : (js > 64 ? 64 : js)) : 1;
   p.nblk = p.brute ? (int64_t)p.jsplit * (nbx > 0 ? nbx : 1)
                    : (n + kSRThreads - 1) / kSRThreads;
+  // neighbour-row capacity: 1.6x the mean-density sphere count + slack, rounded to
+  // whole 32-byte sectors; grown by the caller after an overflow report
+  const double dens = n / (lx * ly * lz);
+  int64_t kc = (int64_t)(1.6 * 4.18879 * rc * rc * rc * dens) + 96;
+  if (kc > n + 8) kc = n + 8;
+  p.kcap = (int)((kc + kStage - 1) / kStage * kStage);
   return p;
 }
 
@@ -274,6 +312,8 @@ size_t short_work_bytes(const ShortPlan& p) {
     b += align256(sizeof(int32_t) * radix_hist_entries(p.n));
     b += align256(sizeof(int32_t) * (p.ncell + 1));
     b += align256(sizeof(double4) * n) + align256(sizeof(float4) * n);
+    b += align256(sizeof(int32_t) * n * (size_t)p.kcap) + align256(sizeof(int32_t) * n);
+    b += align256(sizeof(int));
   }
   return b + 256;
 }
@@ -281,7 +321,7 @@ size_t short_work_bytes(const ShortPlan& p) {
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
                       double* energy_out, int* status, int64_t h0, int64_t h1,
-                      cudaStream_t st) {
+                      int* maxnn_out, cudaStream_t st) {
   const int64_t n = p.n;
   if (n < 2 || h1 <= h0) {
     cudaMemsetAsync(energy_out, 0, sizeof(double), st);
@@ -322,6 +362,12 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     double4* cp = reinterpret_cast<double4*>(w);
     w += align256(sizeof(double4) * n);
     float4* cpf = reinterpret_cast<float4*>(w);
+    w += align256(sizeof(float4) * n);
+    int32_t* nbr = reinterpret_cast<int32_t*>(w);
+    w += align256(sizeof(int32_t) * n * (size_t)p.kcap);
+    int32_t* nn = reinterpret_cast<int32_t*>(w);
+    w += align256(sizeof(int32_t) * n);
+    int* maxnn = maxnn_out;
     cell_index_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, n, lx, ly, lz, p.ncx,
                                                                   p.ncy, p.ncz, k0, v0);
     int bits = 8;
@@ -337,16 +383,12 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     // conservative fp32 screen: positions rounded to fp32 move d2 by < 1e-2 for
     // |r| <= 1e3; the exact fp64 test is applied to every survivor
     const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(short_cells_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(int32_t) * kQ * kSRThreads));
-      attr = true;
-    }
     const int64_t nblk = (nh + kSRThreads - 1) / kSRThreads;
-    short_cells_kernel<<<(unsigned)nblk, kSRThreads, sizeof(int32_t) * kQ * kSRThreads, st>>>(
-        cp, cpf, order, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, lx, ly, alpha, rc2, rc2f, forces,
-        eblk, status);
+    nbr_build_kernel<<<(unsigned)nblk, kSRThreads, 0, st>>>(
+        cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, rc2f, p.kcap, nbr, nn,
+        maxnn, status);
+    pair_list_kernel<<<(unsigned)nblk, kSRThreads, 0, st>>>(cp, order, nbr, nn, h0, h1, p.kcap, lx,
+                                                            ly, alpha, rc2, forces, eblk, status);
     half_sum_kernel<<<1, 1024, 0, st>>>(eblk, nblk, energy_out);
   }
   return cudaGetLastError();

@@ -58,6 +58,18 @@ class Engine:
         with torch.cuda.device(self.device):
             check(self.lib.slab_ctx_create(ctypes.byref(self.ctx)), "slab_ctx_create")
 
+    def handle_overflow(self, status: int) -> bool:
+        """After a synchronised run: if a short-range neighbour row overflowed, grow the
+        capacity to the longest row seen and report that the evaluation must be rerun."""
+        if not int(status) & _native.SLAB_STATUS_NBR_OVERFLOW:
+            return False
+        need = ctypes.c_int(0)
+        check(self.lib.slab_ctx_last_max_neighbors(self.ctx, ctypes.byref(need)),
+              "slab_ctx_last_max_neighbors")
+        check(self.lib.slab_ctx_neighbor_capacity(self.ctx, int(need.value * 1.1) + 16),
+              "slab_ctx_neighbor_capacity")
+        return True
+
     def _stream(self):
         torch = _torch()
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -108,6 +120,13 @@ class Engine:
 
     # -- sub-paths ----------------------------------------------------------
     def short_range(self, pos, charge, box, alpha, r_c):
+        """Synchronous: (energy, forces, status), rerun once after a capacity overflow."""
+        while True:
+            out = self._short_range(pos, charge, box, alpha, r_c)
+            if not self.handle_overflow(int(out[2].cpu().item())):
+                return out
+
+    def _short_range(self, pos, charge, box, alpha, r_c):
         torch = _torch()
         n = charge.numel()
         forces = torch.empty((n, 3), dtype=torch.float64, device=self.device)
@@ -290,10 +309,14 @@ class DeviceEvaluator:
             dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
 
     def warmup(self):
-        """Run one step synchronously (workspace allocation, kernel attributes)."""
+        """Run one step synchronously (workspace allocation, kernel attributes,
+        short-range neighbour capacity)."""
         torch = _torch()
-        self._enqueue()
-        torch.cuda.synchronize(self.eng.device)
+        while True:
+            self._enqueue()
+            torch.cuda.synchronize(self.eng.device)
+            if not self.eng.handle_overflow(int(self.energy[5].item())):
+                return
 
     def capture(self):
         """Record one step as a CUDA graph (single GPU; small systems are launch bound)."""

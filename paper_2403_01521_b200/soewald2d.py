@@ -61,9 +61,12 @@ def device_evaluate(system: ParticleSystem, box: BoxGeometry, alpha: float, r_c:
     modes = np.asarray(modes, dtype=np.float64).reshape(-1, 3)
     mt = to_device(modes) if modes.shape[0] else None
     cv = to_device(commonv) if isinstance(commonv, np.ndarray) else float(commonv)
-    energy, forces = eng.evaluate(pos, q, box, alpha, r_c, soe, mt, cv, charge_const,
-                                  want_forces=want_forces, skip_short_range=skip_short_range)
-    e = energy.cpu().numpy()
+    while True:
+        energy, forces = eng.evaluate(pos, q, box, alpha, r_c, soe, mt, cv, charge_const,
+                                      want_forces=want_forces, skip_short_range=skip_short_range)
+        e = energy.cpu().numpy()
+        if not eng.handle_overflow(int(e[5])):
+            break
     raise_on_status(int(e[5]))
     return e, (forces.cpu().numpy() if want_forces else None)
 
