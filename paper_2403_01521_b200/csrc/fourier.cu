@@ -140,7 +140,7 @@ __global__ void mode_table_kernel(const double* __restrict__ modes,
 // phase 1: chunk aggregates
 // ---------------------------------------------------------------------------
 template <int MH>
-__global__ void __launch_bounds__(256) fourier_aggregate_kernel(
+__global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
     int ipg, BVec b, double2* __restrict__ carry) {
@@ -221,9 +221,12 @@ __global__ void __launch_bounds__(256) fourier_aggregate_kernel(
 // ---------------------------------------------------------------------------
 // phase 2: carry scan over chunks (in place: aggregates -> carried-in states)
 // ---------------------------------------------------------------------------
-// One warp per chain (item, component): lane l composes a contiguous block of
-// chunks, a shuffle scan composes the lane blocks, then each lane rewrites its
-// block with the exclusive carries.  Affine map per chunk: T -> D T + X.
+// One 128-thread block per chain (item, component): thread t composes a
+// contiguous block of ~nch/128 chunks, a shuffle + shared-memory scan composes
+// the thread blocks, then each thread rewrites its block with the exclusive
+// carries.  Affine map per chunk: T -> D T + X.
+constexpr int kCarryThreads = 128;
+
 __device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, int l, int mh,
                                           double k, const double2* __restrict__ Df,
                                           const double2* __restrict__ Db,
@@ -237,14 +240,22 @@ __device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, in
   return C2{d.x, d.y};
 }
 
-__global__ void __launch_bounds__(128) fourier_carry_kernel(
+struct AffC {
+  C2 D, X;
+};
+// apply a first, then b
+__device__ __forceinline__ AffC acompose(const AffC& a, const AffC& b) {
+  const C2 x = cmul(b.D, a.X);
+  return AffC{cmul(b.D, a.D), C2{x.re + b.X.re, x.im + b.X.im}};
+}
+
+__global__ void __launch_bounds__(kCarryThreads) fourier_carry_kernel(
     double2* __restrict__ carry, int nch, int P, int mh, const double* __restrict__ modetab,
     const double2* __restrict__ Df, const double2* __restrict__ Db,
     const double* __restrict__ zbound) {
+  __shared__ AffC wagg[kCarryThreads / 32];
   const int nitems = 2 * P, nc = ncomp_of(mh);
-  const int chain = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (chain >= nitems * nc) return;  // whole warp exits together
+  const int chain = blockIdx.x;
   const int item = chain % nitems, comp = chain / nitems;
   const bool fwd = item < P;
   const int t = fwd ? item : item - P;
@@ -253,33 +264,46 @@ __global__ void __launch_bounds__(128) fourier_carry_kernel(
   const double k = modetab[(size_t)t * mode_stride(mh) + 2];
   const size_t cstride = (size_t)nc * nitems;
   double2* base = carry + (size_t)comp * nitems + item;
-  const int per = (nch + 31) / 32;
-  const int s0 = lane * per, s1 = min(nch, s0 + per);
-  // pass 1: compose this lane's block
-  C2 D{1.0, 0.0}, X{0.0, 0.0};
-  for (int s = s0; s < s1; ++s) {
-    const int c = fwd ? s : nch - 1 - s;
-    const double2 x = base[(size_t)c * cstride];
-    const C2 d = carry_decay(isg, fwd, c, nch, l, mh, k, Df, Db, zbound);
-    const C2 nx = cmul(d, X);
-    X = C2{nx.re + x.x, nx.im + x.y};
-    D = cmul(d, D);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (nch + kCarryThreads - 1) / kCarryThreads;
+  const int s0 = tid * per, s1 = min(nch, s0 + per);
+  constexpr int B = 8;
+  // pass 1: compose this thread's block (loads batched ahead)
+  AffC M{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  for (int sb = s0; sb < s1; sb += B) {
+    double2 xs[B];
+    C2 ds[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int s = sb + j;
+      if (s < s1) {
+        const int c = fwd ? s : nch - 1 - s;
+        xs[j] = base[(size_t)c * cstride];
+        ds[j] = carry_decay(isg, fwd, c, nch, l, mh, k, Df, Db, zbound);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (sb + j < s1) M = acompose(M, AffC{ds[j], C2{xs[j].x, xs[j].y}});
   }
-  // inclusive scan of lane maps (earlier lanes applied first)
+  // inclusive scan over threads (earlier threads applied first)
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const double dr = __shfl_up_sync(0xffffffffu, D.re, o), di = __shfl_up_sync(0xffffffffu, D.im, o);
-    const double xr = __shfl_up_sync(0xffffffffu, X.re, o), xi = __shfl_up_sync(0xffffffffu, X.im, o);
-    if (lane >= o) {
-      const C2 nx = cmul(D, C2{xr, xi});
-      X = C2{nx.re + X.re, nx.im + X.im};
-      D = cmul(D, C2{dr, di});
-    }
+    AffC u;
+    u.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, o), __shfl_up_sync(0xffffffffu, M.D.im, o)};
+    u.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, o), __shfl_up_sync(0xffffffffu, M.X.im, o)};
+    if (lane >= o) M = acompose(u, M);
   }
-  C2 T{__shfl_up_sync(0xffffffffu, X.re, 1), __shfl_up_sync(0xffffffffu, X.im, 1)};
-  if (lane == 0) T = C2{0.0, 0.0};
-  // pass 2: rewrite the block with exclusive carries (loads batched ahead of stores)
-  constexpr int B = 8;
+  if (lane == 31) wagg[warp] = M;
+  __syncthreads();
+  AffC pre{C2{1.0, 0.0}, C2{0.0, 0.0}};  // all earlier warps
+  for (int w = 0; w < warp; ++w) pre = acompose(pre, wagg[w]);
+  AffC excl;  // exclusive within the warp
+  excl.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, 1), __shfl_up_sync(0xffffffffu, M.D.im, 1)};
+  excl.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, 1), __shfl_up_sync(0xffffffffu, M.X.im, 1)};
+  if (lane == 0) excl = AffC{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  C2 T = acompose(pre, excl).X;  // carried state entering this thread's block (T0 = 0)
+  // pass 2: rewrite the block with exclusive carries
   for (int sb = s0; sb < s1; sb += B) {
     double2 xs[B];
     C2 ds[B];
@@ -446,28 +470,36 @@ __global__ void __launch_bounds__(256, 2) fourier_sweep_kernel(
       if (slot == kSB - 1 || i == len - 1) {
         __syncwarp();
         const int nslot = slot + 1, ibase = i - slot;
-        if (lane < 3 * nslot) {
-          const int s = lane / 3, comp = lane - 3 * s;
-          const double* row = st + (s * 3 + comp) * kStageStride;
-          double sf = 0.0, sb = 0.0;
+        const int nrow = 3 * nslot;
+        // two lanes per (particle, component) row, 16 columns each, then one shuffle
+        const int r = lane % (3 * kSB), half = lane / (3 * kSB);
+        double sf = 0.0, sb = 0.0;
+        if (r < nrow && half < 2) {
+          const double* row = st + r * kStageStride + 16 * half;
           if (bmask == 0u || fmask == 0u) {  // single-direction warp (all but one)
             double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
+            for (int j = 0; j < 16; j += 2) {
               acc0 += row[j];
               acc1 += row[j + 1];
             }
             (bmask == 0u ? sf : sb) = acc0 + acc1;
           } else {
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
               const double v = row[j];
-              if ((fmask >> j) & 1u) sf += v;
-              if ((bmask >> j) & 1u) sb += v;
+              const int col = 16 * half + j;
+              if ((fmask >> col) & 1u) sf += v;
+              if ((bmask >> col) & 1u) sb += v;
             }
           }
-          if (fmask) fbuf_f[(a0 + ibase + s) * 3 + comp] = sf;
-          if (bmask) fbuf_b[(a0 + len - 1 - (ibase + s)) * 3 + comp] = sb;
+        }
+        sf += __shfl_down_sync(0xffffffffu, sf, 3 * kSB);
+        sb += __shfl_down_sync(0xffffffffu, sb, 3 * kSB);
+        if (lane < nrow) {
+          const int sl = lane / 3, comp = lane - 3 * sl;
+          if (fmask) fbuf_f[(a0 + ibase + sl) * 3 + comp] = sf;
+          if (bmask) fbuf_b[(a0 + len - 1 - (ibase + sl)) * 3 + comp] = sb;
         }
         __syncwarp();
       }
@@ -617,6 +649,11 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
                          (int)agg_smem(kMaxR, MH));
     cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sweep_smem(kMaxR, MH, 8));
+    // prefer the largest shared-memory carveout so two CTAs fit per SM
+    cudaFuncSetAttribute(fourier_aggregate_kernel<MH>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         100);
     attr_done = true;
   }
   dim3 grid(p.nch, p.ngroups);
@@ -626,8 +663,7 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
   else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {
-    const int nthr = 32 * 2 * p.P * ncomp_of(MH);
-    fourier_carry_kernel<<<(nthr + 127) / 128, 128, 0, st>>>(
+    fourier_carry_kernel<<<2 * p.P * ncomp_of(MH), kCarryThreads, 0, st>>>(
         w.carry, p.nch, p.P, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH, w.zbound);
   }
   fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
