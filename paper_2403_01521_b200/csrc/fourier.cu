@@ -171,12 +171,17 @@ __global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
   }
   __syncthreads();
 
+  // Lane layout: lanes 0-15 forward, 16-31 backward items of the SAME 16 modes
+  // (mode = g * mpg + 16 * warp + lane % 16), so a lane and its partner lane^16
+  // need identical phases: each computes the sincos of one particle of a pair and
+  // they swap with one shuffle (half the sincos work).  `ipg` = modes per group.
   const int nitems = 2 * P;
-  const int item = g * ipg + threadIdx.x;
-  const int gend = min(nitems, (g + 1) * ipg);
-  const bool active = item < gend;
-  const bool fwd = item < P;
-  const int t = active ? (fwd ? item : item - P) : 0;
+  const int lane = threadIdx.x & 31;
+  const int t_raw = g * ipg + 16 * (threadIdx.x >> 5) + (lane & 15);
+  const bool active = t_raw < min(P, (g + 1) * ipg);
+  const bool fwd = lane < 16;
+  const int t = active ? t_raw : 0;
+  const int item = fwd ? t : P + t;
   const double* mt = modetab + (size_t)t * mode_stride(MH);
   const double kx = mt[0], ky = mt[1], k = mt[2];
   const double sigma = fwd ? 1.0 : -1.0;
@@ -186,11 +191,7 @@ __global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
 #pragma unroll
   for (int l = 0; l < MH; ++l) Racc[l] = Iacc[l] = C2{0.0, 0.0};
   C2 gacc{0.0, 0.0};
-#pragma unroll 2
-  for (int i = 0; i < len; ++i) {
-    const double th = __dadd_rn(__dmul_rn(kx, sx[i]), __dmul_rn(ky, sy[i]));
-    double sn, cs;
-    sincos_fast(th, &sn, &cs);
+  auto accumulate = [&](int i, double cs, double sn) {
     const double q = sq[i];
     const double ur = q * cs, ui = -sigma * q * sn;
     const double dist = fwd ? (z_end - sz[i]) : (sz[i] - z_start);
@@ -205,6 +206,16 @@ __global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
       Iacc[l].re = fma(ui, wl.x, Iacc[l].re);
       Iacc[l].im = fma(ui, wl.y, Iacc[l].im);
     }
+  };
+  for (int i = 0; i < len; i += 2) {
+    const int mine = min(i + (fwd ? 0 : 1), len - 1);
+    const double th = __dadd_rn(__dmul_rn(kx, sx[mine]), __dmul_rn(ky, sy[mine]));
+    double sn, cs;
+    sincos_fast(th, &sn, &cs);
+    const double cs_o = __shfl_xor_sync(0xffffffffu, cs, 16);
+    const double sn_o = __shfl_xor_sync(0xffffffffu, sn, 16);
+    accumulate(i, fwd ? cs : cs_o, fwd ? sn : sn_o);
+    if (i + 1 < len) accumulate(i + 1, fwd ? cs_o : cs, fwd ? sn_o : sn);
   }
   if (active) {
     const int nc = ncomp_of(MH);
@@ -600,6 +611,11 @@ FourierPlan fourier_plan(int64_t n, int P, int mh) {
   const int g_of_p = P / p.ipg;  // group containing item P (first backward item)
   const bool mixed = P < nitems && ((P - g_of_p * p.ipg) % 32) != 0;
   p.nbuf = p.ngroups * p.warps + (mixed ? 1 : 0);
+  p.agg_groups = (P + 127) / 128;
+  if (p.agg_groups < 1) p.agg_groups = 1;
+  p.agg_mpg = (P + p.agg_groups - 1) / p.agg_groups;
+  p.agg_warps = (p.agg_mpg + 15) / 16;
+  if (p.agg_warps < 1) p.agg_warps = 1;
   return p;
 }
 
@@ -658,8 +674,8 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
   }
   dim3 grid(p.nch, p.ngroups);
   if (p.nch > 1)
-    fourier_aggregate_kernel<MH><<<grid, p.warps * 32, p.smem_agg, st>>>(
-        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, p.ipg, b, w.carry);
+    fourier_aggregate_kernel<MH><<<dim3(p.nch, p.agg_groups), p.agg_warps * 32, p.smem_agg, st>>>(
+        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, p.agg_mpg, b, w.carry);
   else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {

@@ -52,6 +52,7 @@ struct FourierPlan {
   int ipg;        // items per group
   int warps;      // warps per CTA
   int nbuf;       // partial force buffers (per group x warp, + 1 if a warp mixes directions)
+  int agg_groups, agg_mpg, agg_warps;  // aggregate kernel: modes per group, 16 modes per warp
   size_t smem_agg, smem_sweep;
 };
 FourierPlan fourier_plan(int64_t n, int P, int mh);
