@@ -116,7 +116,6 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
   const int cid = (int)skey[a];
   const int cz = cid % ncz, cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
   const float4 pi = cpf[a];
-  const float ilx = 1.0f / lxf, ily = 1.0f / lyf;
   int32_t* st = reinterpret_cast<int32_t*>(stage[threadIdx.x]);
   int32_t* row = nbr + (a - a_begin) * (int64_t)kcap;
   int cnt = 0;
@@ -124,18 +123,24 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
     const int dxc = off / 9 - 1, dyc = (off / 3) % 3 - 1, dzc = off % 3 - 1;
     const int nz = cz + dzc;
     if (nz < 0 || nz >= ncz) continue;
-    const int nx = (cx + dxc + ncx) % ncx, ny = (cy + dyc + ncy) % ncy;
+    const int ux = cx + dxc, uy = cy + dyc;
+    const int nx = (ux + ncx) % ncx, ny = (uy + ncy) % ncy;
     const int nid = (nx * ncy + ny) * ncz + nz;
     const int b0 = start[nid], b1 = start[nid + 1];
+    // periodic image of the neighbour cell folded into the home position once per
+    // cell (ncx, ncy >= 3: the three neighbours per axis are distinct cells and any
+    // pair within r_c is found in its minimum image) -- a conservative superset
+    // screen; the exact reference minimum image is applied in pair_list_kernel
+    const float px = pi.x + (ux < 0 ? lxf : (ux >= ncx ? -lxf : 0.0f));
+    const float py = pi.y + (uy < 0 ? lyf : (uy >= ncy ? -lyf : 0.0f));
+    const float pz = pi.z;
+    const bool home = off == 13;
 #pragma unroll 4
     for (int jj = b0; jj < b1; ++jj) {
       const float4 pj = cpf[jj];
-      float dx = pi.x - pj.x, dy = pi.y - pj.y;
-      const float dz = pi.z - pj.z;
-      dx -= lxf * rintf(dx * ilx);
-      dy -= lyf * rintf(dy * ily);
+      const float dx = px - pj.x, dy = py - pj.y, dz = pz - pj.z;
       const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      if (d2 <= rc2f && jj != a) {
+      if (d2 <= rc2f && (!home || jj != a)) {
         st[cnt & (kStage - 1)] = jj;
         ++cnt;
         if ((cnt & (kStage - 1)) == 0 && cnt <= kcap) {
