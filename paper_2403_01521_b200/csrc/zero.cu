@@ -103,76 +103,78 @@ __device__ __forceinline__ ZMap zshfl_up(const ZMap& m, int o) {
   return r;
 }
 
-// in place: aggregates -> carried-in states.  One warp per (dir, chain), chain
-// = SOE pair l < mh, or mh for the (S0, S1) prefix sums.
-__global__ void __launch_bounds__(64) zero_carry_kernel(int nch, int mh,
-                                                        const double* __restrict__ zdz,
-                                                        const double2* __restrict__ zD,
-                                                        double2* __restrict__ zagg) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= 2 * (mh + 1)) return;
+// in place: aggregates -> carried-in states.  One 256-thread block per
+// (dir, chain), chain = SOE pair l < mh, or mh for the (S0, S1) prefix sums:
+// thread blocks of chunks composed serially, then a shuffle + shared-memory scan.
+constexpr int kZCarryThreads = 256;
+
+__global__ void __launch_bounds__(kZCarryThreads) zero_carry_kernel(
+    int nch, int mh, const double* __restrict__ zdz, const double2* __restrict__ zD,
+    double2* __restrict__ zagg) {
+  __shared__ ZMap wagg[kZCarryThreads / 32];
+  const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int dir = w / (mh + 1), l = w % (mh + 1);
   const size_t rec = 2 * mh + 1;
-  const int per = (nch + 31) / 32;
-  const int s0 = lane * per, s1 = min(nch, s0 + per);
-  if (l == mh) {  // plain prefix (fwd) / suffix (bwd) sums of q and q z
-    double a0 = 0.0, a1 = 0.0;
-    for (int s = s0; s < s1; ++s) {
-      const int c = dir == 0 ? s : nch - 1 - s;
-      const double2 x = zagg[((size_t)c * 2 + dir) * rec + 2 * mh];
-      a0 += x.x;
-      a1 += x.y;
-    }
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double u0 = __shfl_up_sync(0xffffffffu, a0, o), u1 = __shfl_up_sync(0xffffffffu, a1, o);
-      if (lane >= o) {
-        a0 += u0;
-        a1 += u1;
-      }
-    }
-    double S0 = __shfl_up_sync(0xffffffffu, a0, 1), S1 = __shfl_up_sync(0xffffffffu, a1, 1);
-    if (lane == 0) S0 = S1 = 0.0;
-    for (int s = s0; s < s1; ++s) {
-      const int c = dir == 0 ? s : nch - 1 - s;
-      double2* p = zagg + ((size_t)c * 2 + dir) * rec + 2 * mh;
-      const double2 x = *p;
-      *p = make_double2(S0, S1);
-      S0 += x.x;
-      S1 += x.y;
-    }
-    return;
-  }
-  ZMap M{C2{1.0, 0.0}, C2{0.0, 0.0}, C2{0.0, 0.0}, 0.0};
-  for (int s = s0; s < s1; ++s) {
-    const int c = dir == 0 ? s : nch - 1 - s;
+  const int per = (nch + kZCarryThreads - 1) / kZCarryThreads;
+  const int s0 = tid * per, s1 = min(nch, s0 + per);
+  const ZMap ident{C2{1.0, 0.0}, C2{0.0, 0.0}, C2{0.0, 0.0}, 0.0};
+  // the (S0, S1) chain is the same machinery with D = 1, dz = 0: X_A = S0, X_B = S1
+  const bool sums = l == mh;
+  auto element = [&](int c) {
     const double2* p = zagg + ((size_t)c * 2 + dir) * rec;
+    if (sums) return ZMap{C2{1.0, 0.0}, C2{p[2 * mh].x, 0.0}, C2{p[2 * mh].y, 0.0}, 0.0};
     const double2 d = zD[((size_t)dir * nch + c) * mh + l];
-    ZMap e{C2{d.x, d.y}, C2{p[l].x, p[l].y}, C2{p[mh + l].x, p[mh + l].y},
-           zdz[(size_t)dir * nch + c]};
-    M = zcompose(M, e);
+    return ZMap{C2{d.x, d.y}, C2{p[l].x, p[l].y}, C2{p[mh + l].x, p[mh + l].y},
+                zdz[(size_t)dir * nch + c]};
+  };
+  ZMap M = ident;
+  for (int sb = s0; sb < s1; sb += 8) {
+    ZMap es[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (sb + j < s1) es[j] = element(dir == 0 ? sb + j : nch - 1 - (sb + j));
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (sb + j < s1) M = zcompose(M, es[j]);
   }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const ZMap u = zshfl_up(M, o);
     if (lane >= o) M = zcompose(u, M);
   }
-  const ZMap prev = zshfl_up(M, 1);
-  C2 TA = lane ? prev.XA : C2{0.0, 0.0};
-  C2 TB = lane ? prev.XB : C2{0.0, 0.0};
-  for (int s = s0; s < s1; ++s) {
-    const int c = dir == 0 ? s : nch - 1 - s;
-    double2* p = zagg + ((size_t)c * 2 + dir) * rec;
-    const double2 XA = p[l], XB = p[mh + l];
-    p[l] = make_double2(TA.re, TA.im);
-    p[mh + l] = make_double2(TB.re, TB.im);
-    const double2 d = zD[((size_t)dir * nch + c) * mh + l];
-    const double dz = zdz[(size_t)dir * nch + c];
-    const C2 D{d.x, d.y};
-    const C2 nb = cmul(D, C2{fma(dz, TA.re, TB.re), fma(dz, TA.im, TB.im)});
-    const C2 na = cmul(D, TA);
-    TA = C2{na.re + XA.x, na.im + XA.y};
-    TB = C2{nb.re + XB.x, nb.im + XB.y};
+  if (lane == 31) wagg[warp] = M;
+  __syncthreads();
+  ZMap pre = ident;
+  for (int q = 0; q < warp; ++q) pre = zcompose(pre, wagg[q]);
+  ZMap ex = zshfl_up(M, 1);
+  if (lane == 0) ex = ident;
+  const ZMap in = zcompose(pre, ex);
+  C2 TA = in.XA, TB = in.XB;
+  constexpr int B = 8;  // loads of a batch issued ahead of its stores
+  for (int sb = s0; sb < s1; sb += B) {
+    ZMap es[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (sb + j < s1) es[j] = element(dir == 0 ? sb + j : nch - 1 - (sb + j));
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      if (sb + j >= s1) break;
+      const int c = dir == 0 ? sb + j : nch - 1 - (sb + j);
+      const ZMap& e = es[j];
+      double2* p = zagg + ((size_t)c * 2 + dir) * rec;
+      if (sums) {
+        p[2 * mh] = make_double2(TA.re, TB.re);
+        TA.re += e.XA.re;
+        TB.re += e.XB.re;
+      } else {
+        p[l] = make_double2(TA.re, TA.im);
+        p[mh + l] = make_double2(TB.re, TB.im);
+        const C2 nb = cmul(e.D, C2{fma(e.dz, TA.re, TB.re), fma(e.dz, TA.im, TB.im)});
+        const C2 na = cmul(e.D, TA);
+        TA = C2{na.re + e.XA.re, na.im + e.XA.im};
+        TB = C2{nb.re + e.XB.re, nb.im + e.XB.im};
+      }
+    }
   }
 }
 
@@ -271,7 +273,7 @@ ZeroPlan zero_plan(int64_t n, int mh) {
   p.n = n;
   p.mh = mh;
   int R = 32;
-  while (R * 2 <= 256 && (int64_t)R * 2 * 4096 <= n) R *= 2;
+  while (R * 2 <= 128 && (int64_t)R * 2 * 8192 <= n) R *= 2;
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
   return p;
@@ -300,8 +302,7 @@ static void zero_launch(const ZeroPlan& p, double* work, const double* zs, const
   zero_aggregate_kernel<MH><<<(nthr + 63) / 64, 64, 0, st>>>(zs, qs, dtab, p.n, p.R, p.nch, zagg);
   const int nd = 2 * p.nch * MH;
   zero_chunk_decay_kernel<<<(nd + 255) / 256, 256, 0, st>>>(zs, p.n, p.R, p.nch, MH, b, zdz, zD);
-  const int nwarp_thr = 32 * 2 * (MH + 1);
-  zero_carry_kernel<<<(nwarp_thr + 63) / 64, 64, 0, st>>>(p.nch, MH, zdz, zD, zagg);
+  zero_carry_kernel<<<2 * (MH + 1), kZCarryThreads, 0, st>>>(p.nch, MH, zdz, zD, zagg);
   zero_sweep_kernel<MH><<<(nthr + 63) / 64, 64, 0, st>>>(zs, qs, dtab, p.n, p.R, p.nch, zagg, zc,
                                                          want_forces, fzf, fzb, zep);
   zero_energy_kernel<<<3, 256, 0, st>>>(zep, p.nch, tsum);
