@@ -53,8 +53,9 @@ enum {
 enum {
   SLAB_STATUS_COINCIDENT = 1, /* d2 < 1e-24 pair: ewald2d.py:207-209,301-302 */
   SLAB_STATUS_SINGULAR = 2,   /* |b_l - k| < 2e-6 k: soewald2d.py:118-121 (analytic branch) */
-  SLAB_STATUS_NBR_OVERFLOW = 4 /* a short-range neighbour row exceeded its capacity: results
-                                  are invalid; raise it (slab_ctx_neighbor_capacity) and rerun */
+  SLAB_STATUS_NBR_OVERFLOW = 4, /* a short-range neighbour row exceeded its capacity: results
+                                   are invalid; raise it (slab_ctx_neighbor_capacity) and rerun */
+  SLAB_STATUS_NONFINITE = 8     /* a z coordinate is not finite (core.py:206-207): results invalid */
 };
 
 typedef struct SlabBox {

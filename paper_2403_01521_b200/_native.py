@@ -22,6 +22,7 @@ SLAB_ERR_NOMEM = 4
 SLAB_STATUS_COINCIDENT = 1
 SLAB_STATUS_SINGULAR = 2
 SLAB_STATUS_NBR_OVERFLOW = 4
+SLAB_STATUS_NONFINITE = 8
 
 EXPORTED = (
     "slab_ctx_create", "slab_ctx_destroy", "slab_last_error", "slab_version",

@@ -373,7 +373,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
   int32_t* perm = nullptr;
   if (n > 0) {
-    CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm));
+    CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm, ctx->status));
     CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm, st));
   }
   const int scount = a->shard_count > 1 ? a->shard_count : 1;

@@ -15,7 +15,7 @@ struct SortWork {
 };
 int64_t radix_hist_entries(int64_t n);
 cudaError_t sort_by_z_device(const double* z, int64_t stride, int64_t n, SortWork& w,
-                             cudaStream_t st, int32_t** perm_out);
+                             cudaStream_t st, int32_t** perm_out, int* status = nullptr);
 template <typename K>
 cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_alt,
                              int32_t* hist, int64_t n, int key_bits, cudaStream_t st,

@@ -21,11 +21,15 @@ constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per tile
 
 __global__ void zkey_init_kernel(const double* __restrict__ z, int64_t stride, int64_t n,
-                                 uint64_t* __restrict__ keys, int32_t* __restrict__ idx) {
+                                 uint64_t* __restrict__ keys, int32_t* __restrict__ idx,
+                                 int* __restrict__ status) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) {
-    keys[i] = z_key(z[i * stride]);
+    const double zi = z[i * stride];
+    keys[i] = z_key(zi);
     idx[i] = (int32_t)i;
+    // core.py:206-207 rejects non-finite z; reported through the status word
+    if (status && !isfinite(zi)) atomicOr(status, SLAB_STATUS_NONFINITE_DEV);
   }
 }
 
@@ -197,9 +201,10 @@ int64_t radix_hist_entries(int64_t n) {
 }
 
 cudaError_t sort_by_z_device(const double* z, int64_t stride, int64_t n, SortWork& w,
-                             cudaStream_t st, int32_t** perm_out) {
+                             cudaStream_t st, int32_t** perm_out, int* status) {
   if (n > 0)
-    zkey_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(z, stride, n, w.k0, w.v0);
+    zkey_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(z, stride, n, w.k0, w.v0,
+                                                                  status);
   uint64_t* kout;
   return radix_sort_pairs<uint64_t>(w.k0, w.v0, w.k1, w.v1, w.hist, n, 64, st, &kout, perm_out);
 }

@@ -202,6 +202,21 @@ def to_device(a, dtype=None, device=None):
 _pinned_keepalive: list = []
 
 
+def host_result(energy, forces=None):
+    """Device energy (8,) and forces (n,3) -> numpy, through page-locked buffers from
+    torch's caching host allocator (one synchronisation, DMA-speed copies).  The
+    returned arrays own their buffers (freed back to the cache when dropped)."""
+    torch = _torch()
+    e_h = torch.empty(energy.shape, dtype=energy.dtype, pin_memory=True)
+    e_h.copy_(energy, non_blocking=True)
+    f_h = None
+    if forces is not None:
+        f_h = torch.empty(forces.shape, dtype=forces.dtype, pin_memory=True)
+        f_h.copy_(forces, non_blocking=True)
+    torch.cuda.current_stream(energy.device).synchronize()
+    return e_h.numpy(), (f_h.numpy() if f_h is not None else None)
+
+
 def pinned_like(a) -> np.ndarray:
     """A numpy array backed by pinned (page-locked) host memory, filled with `a`
     (the backing torch buffer is kept alive for the life of the process)."""

@@ -46,7 +46,9 @@ def check_short_range_cutoff(box: BoxGeometry, r_c: float) -> None:
 
 
 def raise_on_status(status: int) -> None:
-    from ._native import SLAB_STATUS_COINCIDENT, SLAB_STATUS_SINGULAR
+    from ._native import SLAB_STATUS_COINCIDENT, SLAB_STATUS_NONFINITE, SLAB_STATUS_SINGULAR
+    if status & SLAB_STATUS_NONFINITE:  # checked first, like sort_by_z (core.py:206-207)
+        raise ValueError("z coordinates must be finite")
     if status & SLAB_STATUS_COINCIDENT:
         raise ValueError("coincident particles: short-range energy is singular")
     if status & SLAB_STATUS_SINGULAR:

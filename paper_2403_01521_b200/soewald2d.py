@@ -51,8 +51,7 @@ def device_evaluate(system: ParticleSystem, box: BoxGeometry, alpha: float, r_c:
                     soe: SOEApprox, modes, commonv, charge_const: float, want_forces=True,
                     skip_short_range=False):
     """One ``slab_evaluate`` call on host arrays; returns (energy[8], forces or None)."""
-    from .engine import get_engine, to_device
-    _check_finite_z(system)
+    from .engine import get_engine, host_result, to_device
     if not skip_short_range:
         check_short_range_cutoff(box, r_c)
     eng = get_engine()
@@ -64,11 +63,11 @@ def device_evaluate(system: ParticleSystem, box: BoxGeometry, alpha: float, r_c:
     while True:
         energy, forces = eng.evaluate(pos, q, box, alpha, r_c, soe, mt, cv, charge_const,
                                       want_forces=want_forces, skip_short_range=skip_short_range)
-        e = energy.cpu().numpy()
+        e, f = host_result(energy, forces if want_forces else None)  # one sync, pinned D2H
         if not eng.handle_overflow(int(e[5])):
             break
-    raise_on_status(int(e[5]))
-    return e, (forces.cpu().numpy() if want_forces else None)
+    raise_on_status(int(e[5]))  # includes the non-finite-z check done on device
+    return e, f
 
 
 def _breakdown(e) -> EnergyBreakdown:

@@ -322,6 +322,26 @@ def test_single_particle_rb_estimate_is_charge_constant(pk):
                for _ in range(3))
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_z_rejected_by_device_status(pk, bad):
+    """core.py:206-207 via the device status word (no host scan on the eval path)."""
+    box = pk.BoxGeometry(10.0, 10.0, 5.0)
+    s = _slab_system(pk, 20, box, 71)
+    pos = s.pos.copy()
+    pos[7, 2] = bad
+    s = pk.make_system(s.charge, np.ones(s.n), pos)  # no box: make_system would reject inf
+    params = pk.make_ewald_params(0.8, 4.0, box)
+    soe8 = pk.build_soe_contour(8)
+    smp = pk.ModeSampler(0.8, box, seed=1)
+    with pytest.raises(ValueError, match="finite"):
+        pk.rb_energy_forces(s, box, params, soe8, smp, 8)
+    with pytest.raises(ValueError, match="finite"):
+        pk.soe_energy_forces(s, box, params, soe8)
+    # the context recovers (status word reset per evaluation)
+    good = _slab_system(pk, 20, box, 71)
+    pk.soe_energy_forces(good, box, params, soe8)
+
+
 # --------------------------------------------------------------- device evaluator
 def test_graph_replay_and_shard_sum_equal_single_eval(pk):
     import torch
