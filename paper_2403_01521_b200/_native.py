@@ -12,7 +12,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libslabewald_b200.so")
+# SLAB_B200_LIB: alternative build of the same library (kernel-variant A/B timing)
+LIB_PATH = os.environ.get("SLAB_B200_LIB") or os.path.join(HERE, "_lib", "libslabewald_b200.so")
 
 SLAB_OK = 0
 SLAB_ERR_ARG = 1

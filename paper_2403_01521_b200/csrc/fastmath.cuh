@@ -11,8 +11,8 @@
 //                   degree-15/16 Taylor on |r| <= pi/4.
 //   erfc_gauss(x)   erfc(x) and e^{-x^2} for x >= 0 sharing one exp: e^{-x^2}
 //                   with the exact x^2 = hi + lo split, erfc = erfcx * e^{-x^2}
-//                   with erfcx from a piecewise degree-14 table on [0, 6)
-//                   (erfcx_table.cuh, rel. err 2e-16), libdevice beyond.
+//                   with erfcx from a piecewise degree-9 table on [0, 6)
+//                   (erfcx_table.cuh, 48 rows, rel. err 2e-16), libdevice beyond.
 // Parity is still checked end to end against the reference (1e-10 / 1e-9).
 #pragma once
 #include <cuda_runtime.h>
@@ -22,7 +22,7 @@
 namespace slab {
 
 __device__ __forceinline__ double exp_neg(double t) {
-  // branch-free: t >= 700 (and +inf) returns 0 through the final select
+  // t >= 700 (and +inf) returns 0
   const bool tiny = !(t < 700.0);
   t = tiny ? 0.0 : t;
   const double kL2e = 1.4426950408889634;
@@ -45,8 +45,8 @@ __device__ __forceinline__ double exp_neg(double t) {
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const long long e = (long long)((int)n + 1023) << 52;
-  return tiny ? 0.0 : p * __longlong_as_double(e);
+  const long long e = tiny ? 0ll : (long long)((int)n + 1023) << 52;
+  return p * __longlong_as_double(e);  // zero exponent factor: no branch around the polynomial
 }
 
 // Branch-free.  The FMA reduction keeps ~1 ulp in r for |th| up to ~1e15 (the
@@ -82,9 +82,81 @@ __device__ __forceinline__ void sincos_fast(double th, double* s, double* c) {
   *c = ((q + 1) & 2) ? -cc : cc;
 }
 
-// tab: shared-memory copy of kErfcxCoef with row stride 17 (bank-conflict free)
-constexpr int kErfcxStride = 17;
+// *_cb variants: the same polynomials with the constants in the constant bank.
+// sm_100a DFMA takes no c[][] operand, so they are fetched with LDCU.128 into
+// uniform registers (two constants per load instead of four UMOVs per literal
+// pair).  Faster where registers are plentiful (fourier_aggregate: 1.59 ->
+// 1.41 ms at cfg4); slower in the 128-register sweep, where the extra live
+// values spill (4.75 -> 6.0 ms) -- hence both forms.
+static __constant__ double kFmExp[16] = {
+    1.6059043836821613e-10,  // 1/13!
+    2.08767569878681e-09,  2.505210838544172e-08, 2.755731922398589e-07,
+    2.7557319223985893e-06, 2.48015873015873e-05, 0.0001984126984126984,
+    0.001388888888888889,  0.008333333333333333,  0.041666666666666664,
+    0.16666666666666666,   0.5,                   1.0,
+    1.0,
+    6.93147180369123816490e-01,  // [14] ln2 hi (32 significant bits)
+    1.90821492927058770002e-10,  // [15] ln2 lo
+};
+static __constant__ double kFmSin[8] = {
+    -7.647163731819816e-13,  // -1/15!
+    1.6059043836821613e-10, -2.505210838544172e-08, 2.7557319223985893e-06,
+    -0.0001984126984126984, 0.008333333333333333,   -0.16666666666666666,
+    0.6366197723675814,      // [7] 2/pi
+};
+static __constant__ double kFmCos[12] = {
+    4.779477332387385e-14,  // 1/16!
+    -1.1470745597729725e-11, 2.08767569878681e-09, -2.755731922398589e-07,
+    2.48015873015873e-05,    -0.001388888888888889, 0.041666666666666664,
+    -0.5,                    1.0,
+    -1.5707963267948966,     // [9..11] -pi/2 split in three
+    -6.123233995736766e-17,  1.4973849048591698e-33,
+};
 
+__device__ __forceinline__ double exp_neg_cb(double t) {
+  // branch-free: t >= 700 (and +inf) returns 0 by zeroing the exponent factor
+  const bool tiny = !(t < 700.0);
+  t = tiny ? 0.0 : t;
+  const double n = rint(-t * 1.4426950408889634);  // in [-1010, 0]
+  double r = fma(n, -kFmExp[14], -t);
+  r = fma(n, -kFmExp[15], r);
+  double p = kFmExp[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) p = fma(p, r, kFmExp[i]);
+  const long long e = tiny ? 0ll : (long long)((int)n + 1023) << 52;
+  return p * __longlong_as_double(e);
+}
+
+// Branch-free.  The FMA reduction keeps ~1 ulp in r for |th| up to ~1e15 (the
+// products n*P_i are exact inside the FMAs, th - n*P1 is exact by Sterbenz and
+// pi/2 - (P1+P2+P3) ~ 1e-49); physical phases are |th| < 1e4.
+__device__ __forceinline__ void sincos_fast_cb(double th, double* s, double* c) {
+  const double n = rint(th * kFmSin[7]);
+  double r = fma(n, kFmCos[9], th);
+  r = fma(n, kFmCos[10], r);
+  r = fma(n, kFmCos[11], r);
+  const double z = r * r;
+  double ps = kFmSin[0];
+#pragma unroll
+  for (int i = 1; i < 7; ++i) ps = fma(ps, z, kFmSin[i]);
+  const double sr = fma(ps * z, r, r);
+  double pc = kFmCos[0];
+#pragma unroll
+  for (int i = 1; i < 9; ++i) pc = fma(pc, z, kFmCos[i]);
+  const double cr = pc;
+  const int q = ((int)(long long)n) & 3;
+  const double ss = (q & 1) ? cr : sr;
+  const double cc = (q & 1) ? sr : cr;
+  *s = (q & 2) ? -ss : ss;
+  *c = ((q + 1) & 2) ? -cc : cc;
+}
+
+// tab: shared-memory copy of kErfcxCoef, coefficient-major (tab[k * NINT + i]):
+// the lanes of a warp evaluate different intervals i, and with consecutive
+// intervals in consecutive 8-byte words only rows 16 apart share a bank (pair
+// distances put x = alpha r in ~20 adjacent rows).  Interval-major rows read as
+// 16-byte pairs measured 5% slower on the pair kernel (8 lanes per LDS.128
+// phase over 8 bank groups collide).
 __device__ __forceinline__ void erfc_gauss(double x, const double* __restrict__ tab,
                                            double* erfc_out, double* g_out) {
   const double hi = x * x;
@@ -92,13 +164,13 @@ __device__ __forceinline__ void erfc_gauss(double x, const double* __restrict__ 
   double g = exp_neg(hi);
   g = fma(-lo, g, g);  // e^{-(hi+lo)} = e^{-hi} (1 - lo)
   double ex;
-  if (x < 6.0) {
-    const int i = (int)(x * 2.0);
-    const double u = fma(4.0, x, -(double)(2 * i + 1));
-    const double* cf = tab + i * kErfcxStride;
-    ex = cf[SLAB_ERFCX_NCOEF - 1];
+  if (x < SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W) {
+    const int i = (int)(x * SLAB_ERFCX_INV_W);
+    const double u = fma(2.0 * SLAB_ERFCX_INV_W, x, -(double)(2 * i + 1));
+    const double* cf = tab + i;
+    ex = cf[(SLAB_ERFCX_NCOEF - 1) * SLAB_ERFCX_NINT];
 #pragma unroll
-    for (int k = SLAB_ERFCX_NCOEF - 2; k >= 0; --k) ex = fma(ex, u, cf[k]);
+    for (int k = SLAB_ERFCX_NCOEF - 2; k >= 0; --k) ex = fma(ex, u, cf[k * SLAB_ERFCX_NINT]);
   } else {
     ex = erfcx(x);
   }
@@ -106,10 +178,12 @@ __device__ __forceinline__ void erfc_gauss(double x, const double* __restrict__ 
   *g_out = g;
 }
 
+constexpr int kErfcxTabSize = SLAB_ERFCX_NINT * SLAB_ERFCX_NCOEF;
+
 __device__ __forceinline__ void load_erfcx_table(double* tab) {
-  for (int e = threadIdx.x; e < SLAB_ERFCX_NINT * SLAB_ERFCX_NCOEF; e += blockDim.x) {
+  for (int e = threadIdx.x; e < kErfcxTabSize; e += blockDim.x) {
     const int i = e / SLAB_ERFCX_NCOEF, k = e - i * SLAB_ERFCX_NCOEF;
-    tab[i * kErfcxStride + k] = kErfcxCoef[e];
+    tab[k * SLAB_ERFCX_NINT + i] = kErfcxCoef[e];
   }
 }
 

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
     const double q = sq[i];
     const double ur = q * cs, ui = -sigma * q * sn;
     const double dist = fwd ? (z_end - sz[i]) : (sz[i] - z_start);
-    const double wk = exp_neg(k * dist);
+    const double wk = exp_neg_cb(k * dist);
     gacc.re = fma(ur, wk, gacc.re);
     gacc.im = fma(ui, wk, gacc.im);
 #pragma unroll
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
     const int mine = min(i + (fwd ? 0 : 1), len - 1);
     const double th = __dadd_rn(__dmul_rn(kx, sx[mine]), __dmul_rn(ky, sy[mine]));
     double sn, cs;
-    sincos_fast(th, &sn, &cs);
+    sincos_fast_cb(th, &sn, &cs);
     const double cs_o = __shfl_xor_sync(0xffffffffu, cs, 16);
     const double sn_o = __shfl_xor_sync(0xffffffffu, sn, 16);
     accumulate(i, fwd ? cs : cs_o, fwd ? sn : sn_o);

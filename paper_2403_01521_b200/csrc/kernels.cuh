@@ -99,6 +99,7 @@ struct ShortPlan {
   int jsplit;     // brute path: j-range splits
   int64_t nblk;   // energy partial count
   int kcap;       // neighbour-row capacity (multiple of 8)
+  int span;       // cell search span: 1 (edge >= r_c) or 2 (edge >= r_c/2)
 };
 ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc);
 size_t short_work_bytes(const ShortPlan& p);

@@ -17,6 +17,8 @@
 // lanes whose candidate happens to be in range).  Each force is accumulated by
 // exactly one thread over the full shell: deterministic, no atomics;
 // u_s = 1/2 of the full-shell sum.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -99,61 +101,85 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
 }
 
 constexpr int kSRThreads = 128;
-constexpr int kStage = 8;  // neighbour indices staged per thread = one 32-byte sector
+constexpr int kRing = 16;  // staged neighbour indices per thread (two 32-byte sectors)
 
-// Pass 1: neighbour rows.  One thread per home particle (cell-sorted: a warp
-// scans the same 27 cells, so candidate loads are broadcasts), conservative
-// fp32 distance screen, hits staged 8 at a time in shared memory and written
-// as full 32-byte sectors into the particle's row nbr[(a - a_begin) * kcap + k].
+// Pass 1: neighbour rows.  One thread per home particle in cell order.  Cells
+// are ordered z-fastest, so the 2S+1 z-neighbours of one (x, y) column are one
+// contiguous range: (2S+1)^2 ranges per particle.  S = 2 on cells of edge
+// >= r_c/2 (search volume 25 * 5 / 8 = 15.6 r_c^3 instead of 27 r_c^3 with
+// S = 1 on cells >= r_c).  Conservative fp32 distance screen; hits go to a
+// per-thread ring in shared memory (slot-major: conflict-free) and are written
+// as whole 32-byte sectors into the row nbr[(a - a_begin) * kcap + k].
+template <int S>
 __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
     const float4* __restrict__ cpf, const uint32_t* __restrict__ skey,
     const int32_t* __restrict__ start, int64_t a_begin, int64_t a_end, int ncx, int ncy, int ncz,
     float lxf, float lyf, float rc2f, int kcap, int32_t* __restrict__ nbr,
     int32_t* __restrict__ nn, int* __restrict__ maxnn, int* __restrict__ status) {
-  __shared__ int4 stage[kSRThreads][kStage / 4];
+  __shared__ int32_t ring[kRing][kSRThreads];
   const int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x;
   if (a >= a_end) return;
   const int cid = (int)skey[a];
   const int cz = cid % ncz, cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
   const float4 pi = cpf[a];
-  int32_t* st = reinterpret_cast<int32_t*>(stage[threadIdx.x]);
+  const int self = (int)a;
+  int32_t* st = &ring[0][threadIdx.x];
   int32_t* row = nbr + (a - a_begin) * (int64_t)kcap;
-  int cnt = 0;
-  for (int off = 0; off < 27; ++off) {
-    const int dxc = off / 9 - 1, dyc = (off / 3) % 3 - 1, dzc = off % 3 - 1;
-    const int nz = cz + dzc;
-    if (nz < 0 || nz >= ncz) continue;
-    const int ux = cx + dxc, uy = cy + dyc;
-    const int nx = (ux + ncx) % ncx, ny = (uy + ncy) % ncy;
-    const int nid = (nx * ncy + ny) * ncz + nz;
-    const int b0 = start[nid], b1 = start[nid + 1];
-    // periodic image of the neighbour cell folded into the home position once per
-    // cell (ncx, ncy >= 3: the three neighbours per axis are distinct cells and any
-    // pair within r_c is found in its minimum image) -- a conservative superset
-    // screen; the exact reference minimum image is applied in pair_list_kernel
+  int cnt = 0, done = 0;  // hits found / hits already written to the row
+  const int zlo = cz - S < 0 ? 0 : cz - S;
+  const int zhi = cz + S >= ncz ? ncz - 1 : cz + S;
+  auto flush8 = [&]() {
+    if (done + 8 <= kcap) {
+      const int s0 = done & (kRing - 1);
+      const int4 v0 = make_int4(st[(s0 + 0) * kSRThreads], st[(s0 + 1) * kSRThreads],
+                                st[(s0 + 2) * kSRThreads], st[(s0 + 3) * kSRThreads]);
+      const int4 v1 = make_int4(st[(s0 + 4) * kSRThreads], st[(s0 + 5) * kSRThreads],
+                                st[(s0 + 6) * kSRThreads], st[(s0 + 7) * kSRThreads]);
+      int4* dst = reinterpret_cast<int4*>(row + done);
+      dst[0] = v0;
+      dst[1] = v1;
+    }
+    done += 8;
+  };
+  auto test = [&](int jj, const float4& pj, float px, float py) {
+    const float dx = px - pj.x, dy = py - pj.y, dz = pi.z - pj.z;
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const bool hit = d2 <= rc2f && jj != self;
+    if (hit) st[(cnt & (kRing - 1)) * kSRThreads] = jj;
+    cnt += hit ? 1 : 0;
+  };
+#pragma unroll 1
+  for (int ox = -S; ox <= S; ++ox) {
+    // periodic image of the neighbour column folded into the home position (the
+    // 2S+1 columns per axis are distinct cells: ncx, ncy >= 2S+1), a conservative
+    // superset screen; the exact reference minimum image is applied in pair_list_kernel
+    const int ux = cx + ox;
+    const int nx = ux < 0 ? ux + ncx : (ux >= ncx ? ux - ncx : ux);
     const float px = pi.x + (ux < 0 ? lxf : (ux >= ncx ? -lxf : 0.0f));
-    const float py = pi.y + (uy < 0 ? lyf : (uy >= ncy ? -lyf : 0.0f));
-    const float pz = pi.z;
-    const bool home = off == 13;
-#pragma unroll 4
-    for (int jj = b0; jj < b1; ++jj) {
-      const float4 pj = cpf[jj];
-      const float dx = px - pj.x, dy = py - pj.y, dz = pz - pj.z;
-      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      if (d2 <= rc2f && (!home || jj != a)) {
-        st[cnt & (kStage - 1)] = jj;
-        ++cnt;
-        if ((cnt & (kStage - 1)) == 0 && cnt <= kcap) {
-          int4* dst = reinterpret_cast<int4*>(row + cnt - kStage);
-          dst[0] = stage[threadIdx.x][0];
-          dst[1] = stage[threadIdx.x][1];
-        }
+#pragma unroll 1
+    for (int oy = -S; oy <= S; ++oy) {
+      const int uy = cy + oy;
+      const int ny = uy < 0 ? uy + ncy : (uy >= ncy ? uy - ncy : uy);
+      const float py = pi.y + (uy < 0 ? lyf : (uy >= ncy ? -lyf : 0.0f));
+      const int col = (nx * ncy + ny) * ncz;
+      const int b1 = start[col + zhi + 1];
+      int jj = start[col + zlo];
+      for (; jj + 4 <= b1; jj += 4) {
+        const float4 p0 = cpf[jj], p1 = cpf[jj + 1], p2 = cpf[jj + 2], p3 = cpf[jj + 3];
+        test(jj, p0, px, py);
+        test(jj + 1, p1, px, py);
+        test(jj + 2, p2, px, py);
+        test(jj + 3, p3, px, py);
+        if (cnt - done >= 8) flush8();  // pending <= 7 + 4 < kRing
+      }
+      for (; jj < b1; ++jj) {
+        test(jj, cpf[jj], px, py);
+        if (cnt - done >= 8) flush8();
       }
     }
   }
-  const int tail = cnt & (kStage - 1);
   if (cnt <= kcap)
-    for (int k = 0; k < tail; ++k) row[cnt - tail + k] = st[k];
+    for (int k = done; k < cnt; ++k) row[k] = st[(k & (kRing - 1)) * kSRThreads];
   nn[a - a_begin] = cnt < kcap ? cnt : kcap;
   if (cnt > kcap) {
     atomicOr(status, SLAB_STATUS_NBR_OVERFLOW_DEV);
@@ -163,13 +189,15 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
 
 // Pass 2: one thread per home particle over its own row (rows have ~equal
 // length, so the fp64 pair work runs on nearly full warps); four neighbours in
-// flight per iteration.  Each force is owned by one thread: deterministic.
+// flight per iteration (measured: 2 or 8 in flight, a generic unrolled loop, or
+// a min-blocks launch bound are all 5-20% slower).  Each force is owned by one
+// thread: deterministic.
 __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     const double4* __restrict__ cp, const int32_t* __restrict__ order,
     const int32_t* __restrict__ nbr, const int32_t* __restrict__ nn, int64_t a_begin,
     int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2,
     double* __restrict__ forces, double* __restrict__ eblk, int* __restrict__ status) {
-  __shared__ double etab[SLAB_ERFCX_NINT * kErfcxStride];
+  __shared__ double etab[kErfcxTabSize];
   __shared__ double red[kSRThreads];
   load_erfcx_table(etab);
   __syncthreads();
@@ -220,7 +248,7 @@ __global__ void __launch_bounds__(128) brute_pair_kernel(
     const double* __restrict__ pos, const double* __restrict__ q, int64_t n, int64_t i_begin,
     int64_t i_end, int jsplit, double lx, double ly, double alpha, double rc2,
     double* __restrict__ fbuf, double* __restrict__ eblk, int* __restrict__ status) {
-  __shared__ double etab[SLAB_ERFCX_NINT * kErfcxStride];
+  __shared__ double etab[kErfcxTabSize];
   load_erfcx_table(etab);
   __syncthreads();
   const int64_t i = i_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -286,7 +314,20 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc) {
   ncy = ncy < 1 ? 1 : ncy;
   ncz = ncz < 1 ? 1 : ncz;
   p.brute = (ncx < 3 || ncy < 3);
-  if (p.brute) ncx = ncy = ncz = 1;
+  p.span = 1;
+  if (p.brute) {
+    ncx = ncy = ncz = 1;
+  } else {
+    // half-edge cells (edge >= r_c/2, search span 2): ncx, ncy >= 6 >= 2*2+1 here
+    const char* env = getenv("SLAB_SHORT_SPAN");  // tuning knob: 1 = cells of edge >= r_c
+    if (!(env && env[0] == '1')) {
+      p.span = 2;
+      ncx = (int)(2.0 * lx / rc);
+      ncy = (int)(2.0 * ly / rc);
+      ncz = (int)(2.0 * lz / rc);
+      ncz = ncz < 1 ? 1 : ncz;
+    }
+  }
   p.ncx = ncx;
   p.ncy = ncy;
   p.ncz = ncz;
@@ -301,7 +342,7 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc) {
   const double dens = n / (lx * ly * lz);
   int64_t kc = (int64_t)(1.6 * 4.18879 * rc * rc * rc * dens) + 96;
   if (kc > n + 8) kc = n + 8;
-  p.kcap = (int)((kc + kStage - 1) / kStage * kStage);
+  p.kcap = (int)((kc + 7) / 8 * 8);  // whole 32-byte sectors
   return p;
 }
 
@@ -389,9 +430,14 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     // |r| <= 1e3; the exact fp64 test is applied to every survivor
     const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);
     const int64_t nblk = (nh + kSRThreads - 1) / kSRThreads;
-    nbr_build_kernel<<<(unsigned)nblk, kSRThreads, 0, st>>>(
-        cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, rc2f, p.kcap, nbr, nn,
-        maxnn, status);
+    if (p.span == 2)
+      nbr_build_kernel<2><<<(unsigned)nblk, kSRThreads, 0, st>>>(
+          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, rc2f, p.kcap, nbr,
+          nn, maxnn, status);
+    else
+      nbr_build_kernel<1><<<(unsigned)nblk, kSRThreads, 0, st>>>(
+          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, rc2f, p.kcap, nbr,
+          nn, maxnn, status);
     pair_list_kernel<<<(unsigned)nblk, kSRThreads, 0, st>>>(cp, order, nbr, nn, h0, h1, p.kcap, lx,
                                                             ly, alpha, rc2, forces, eblk, status);
     half_sum_kernel<<<1, 1024, 0, st>>>(eblk, nblk, energy_out);
