@@ -33,7 +33,16 @@
 
 namespace slab {
 
-constexpr int kSB = 4;          // force staging batch (particles)
+#ifndef SLAB_SWEEP_SB
+#define SLAB_SWEEP_SB 4
+#endif
+#ifndef SLAB_SWEEP_PIPE
+#define SLAB_SWEEP_PIPE 0  // 1: next particle's sincos/exp issued one iteration ahead (measured 2.5% slower since exp_neg went branch-free)
+#endif
+#ifndef SLAB_AGG_MMA
+#define SLAB_AGG_MMA 1  // phase 1 on DMMA (0: DFMA lane-per-item kernel)
+#endif
+constexpr int kSB = SLAB_SWEEP_SB;  // force staging batch (particles)
 constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
 constexpr int kMaxR = 256;
 
@@ -226,6 +235,164 @@ __global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
       out[(size_t)(MH + l) * nitems] = make_double2(Iacc[l].re, Iacc[l].im);
     }
     out[(size_t)(2 * MH) * nitems] = make_double2(gacc.re, gacc.im);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase 1 on the FP64 tensor cores (DMMA m8n8k4)
+// ---------------------------------------------------------------------------
+// For chunk c the pair aggregates are a GEMM over the chunk's particles j:
+//   X[row][col] = sum_j U[row][j] W[j][col]
+// rows (mode t, part s): U = q cos(theta) (s = 0, the R recurrence) or
+//   -q sin(theta) (s = 1, I);
+// cols (direction, pair l, re/im): the k-independent weights
+//   W^f_l(j) = e^{-b_l (z_end - z_j)},  W^b_l(j) = e^{-b_l (z_j - z_start)}.
+// A warp owns an m-tile of 8 modes.  Per 4-particle k-step each lane computes
+// ONE sincos -- for (mode lane>>2, particle lane&3), exactly its A-fragment
+// slot -- which feeds both the cos and the sin fragment, then issues 2 x NT
+// DMMAs against NT B fragments read from the shared weight table (column-major,
+// K stride R+4: conflict-free).  DMMA and DFMA share the FP64 pipe on B200
+// (measured: 37 TF/s DMMA alone, 33 TF/s mixed), so the gain is issue
+// efficiency: one instruction per 256 FMAs.  The k-dependent e^{-k dist}
+// aggregates (the kappa g term) stay on DFMA, four lanes per mode, reduced by
+// shuffles.  Carry layout identical to fourier_aggregate_kernel.
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__host__ __device__ constexpr int mma_mhp(int mh) { return (mh + 3) / 4 * 4; }
+static size_t agg_mma_smem(int R, int mh) {
+  return sizeof(double) * ((size_t)4 * mma_mhp(mh) * (R + 4) + 4 * (size_t)R);
+}
+
+#ifndef SLAB_AGG_MMA_MAXW
+#define SLAB_AGG_MMA_MAXW 13  // m-tiles (warps) per CTA: P <= 104 in one CTA per chunk
+#endif
+#ifndef SLAB_AGG_MMA_CB
+#define SLAB_AGG_MMA_CB 1  // constant-bank polynomial coefficients in the main loop
+#endif
+template <int MH>
+__global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, 2) fourier_aggregate_mma_kernel(
+    const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
+    const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
+    int tiles_per_cta, BVec b, double2* __restrict__ carry) {
+  constexpr int MHP = mma_mhp(MH);  // pairs padded to whole n-tiles of 4 pairs
+  constexpr int NT = MHP / 2;       // n-tiles: 2 directions x MHP/4
+  constexpr int NCOL = 8 * NT;      // (dir, l, re/im) columns
+  extern __shared__ double4 smem4[];
+  const int RP = R + 4;
+  double* wt = reinterpret_cast<double*>(smem4);  // [NCOL][RP]
+  double* sx = wt + (size_t)NCOL * RP;
+  double* sy = sx + R;
+  double* sz = sy + R;
+  double* sq = sz + R;
+  const int c = blockIdx.x;
+  const int64_t a0 = (int64_t)c * R;
+  const int len = (int)(a0 + R < n ? R : n - a0);
+  const double z_end = zs[a0 + len - 1], z_start = zs[a0];
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    sx[i] = xs[a0 + i];
+    sy[i] = ys[a0 + i];
+    sz[i] = zs[a0 + i];
+    sq[i] = qs[a0 + i];
+  }
+  // weights, column (dir * MHP + l) * 2 + e
+  for (int e = threadIdx.x; e < R * MHP * 2; e += blockDim.x) {
+    const int j = e % R, rest = e / R;
+    const int l = rest % MHP, dir = rest / MHP;
+    double wr = 0.0, wi = 0.0;
+    if (j < len && l < MH) {
+      const double z = zs[a0 + j];
+      const double dist = dir == 0 ? z_end - z : z - z_start;
+      const double e = exp_neg_cb(b.re[l] * dist);
+      double sn, cs;
+      sincos_fast_cb(b.im[l] * dist, &sn, &cs);
+      wr = e * cs;
+      wi = -e * sn;
+    }
+    const int col = (dir * MHP + l) * 2;
+    wt[col * RP + j] = wr;
+    wt[(col + 1) * RP + j] = wi;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.y * tiles_per_cta + warp;
+  if (tile * 8 >= P) return;  // no barrier below
+  const int kk = lane & 3, nn = lane >> 2;
+  const int t = tile * 8 + nn;
+  const bool tv = t < P;
+  const double* mt = modetab + (size_t)(tv ? t : 0) * mode_stride(MH);
+  const double kx = mt[0], ky = mt[1], k = mt[2];
+  double acc[2][NT][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int u = 0; u < NT; ++u) acc[s][u][0] = acc[s][u][1] = 0.0;
+  double gfr = 0.0, gfi = 0.0, gbr = 0.0, gbi = 0.0;
+  const double* wk = wt + nn * RP + kk;
+  const bool span_ok = k * (z_end - z_start) < 600.0;
+  const double ekspan = exp_neg(k * (z_end - z_start));
+  for (int k0 = 0; k0 < len; k0 += 4) {
+    const int j = k0 + kk;
+    double ur = 0.0, ui = 0.0;
+    if (tv && j < len) {
+      const double th = __dadd_rn(__dmul_rn(kx, sx[j]), __dmul_rn(ky, sy[j]));
+      double sn, cs;
+      const double q = sq[j], z = sz[j];
+#if SLAB_AGG_MMA_CB
+      sincos_fast_cb(th, &sn, &cs);
+      // e^{-k (z - z_start)} = e^{-k (z_end - z_start)} / e^{-k (z_end - z)} (one exp
+      // and a reciprocal instead of two exps) while both factors stay normal
+      const double wf = exp_neg_cb(k * (z_end - z));
+      const double wb = span_ok ? ekspan / wf : exp_neg_cb(k * (z - z_start));
+#else
+      sincos_fast(th, &sn, &cs);
+      const double wf = exp_neg(k * (z_end - z)), wb = exp_neg(k * (z - z_start));
+#endif
+      ur = q * cs;
+      ui = -q * sn;
+      gfr = fma(ur, wf, gfr);
+      gfi = fma(ui, wf, gfi);
+      gbr = fma(ur, wb, gbr);
+      gbi = fma(-ui, wb, gbi);
+    }
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+      const double bf = wk[(size_t)u * 8 * RP + k0];
+      dmma_8x8x4(acc[0][u][0], acc[0][u][1], ur, bf);
+      dmma_8x8x4(acc[1][u][0], acc[1][u][1], ui, bf);
+    }
+  }
+  // g aggregates: the four lanes of a mode hold disjoint particle subsets
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    gfr += __shfl_xor_sync(0xffffffffu, gfr, o);
+    gfi += __shfl_xor_sync(0xffffffffu, gfi, o);
+    gbr += __shfl_xor_sync(0xffffffffu, gbr, o);
+    gbi += __shfl_xor_sync(0xffffffffu, gbi, o);
+  }
+  if (!tv) return;
+  const int nitems = 2 * P, nc = ncomp_of(MH);
+  double2* out = carry + (size_t)c * nc * nitems;
+  // accumulator (row t, cols 2kk, 2kk+1 of n-tile u) = (re, im) of pair l
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int dir = u / (MHP / 4);
+    const int l = (u % (MHP / 4)) * 4 + kk;
+    if (l < MH) {
+      const int item = dir == 0 ? t : P + t;
+      const double sgn = dir == 0 ? 1.0 : -1.0;  // backward I input is +q sin = -ui
+      out[(size_t)l * nitems + item] = make_double2(acc[0][u][0], acc[0][u][1]);
+      out[(size_t)(MH + l) * nitems + item] =
+          make_double2(sgn * acc[1][u][0], sgn * acc[1][u][1]);
+    }
+  }
+  if (kk == 0) {
+    out[(size_t)(2 * MH) * nitems + t] = make_double2(gfr, gfi);
+    out[(size_t)(2 * MH) * nitems + P + t] = make_double2(gbr, gbi);
   }
 }
 
@@ -441,10 +608,16 @@ __global__ void __launch_bounds__(256, 2) fourier_sweep_kernel(
     q_ = sq[ia];
   };
   double cs, sn, dk, q;
+#if SLAB_SWEEP_PIPE
   phase(0, cs, sn, dk, q);
+#endif
   for (int i = 0; i < len; ++i) {
+#if SLAB_SWEEP_PIPE
     double cs_n, sn_n, dk_n, q_n;
     phase(i + 1 < len ? i + 1 : i, cs_n, sn_n, dk_n, q_n);
+#else
+    phase(i, cs, sn, dk, q);
+#endif
     const int ia = fwd ? i : len - 1 - i;
     const int id = fwd ? ia : ia + 1;
     // S_a = T_{a-1} * d_a  (forward) / T'_{a+1} * d_{a+1} (backward)
@@ -527,10 +700,12 @@ __global__ void __launch_bounds__(256, 2) fourier_sweep_kernel(
     }
     gk.re += ur;
     gk.im += ui;
+#if SLAB_SWEEP_PIPE
     cs = cs_n;
     sn = sn_n;
     dk = dk_n;
     q = q_n;
+#endif
   }
   if (active && fwd) epart[(size_t)c * P + t] = E;
 }
@@ -665,6 +840,10 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
                          (int)agg_smem(kMaxR, MH));
     cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sweep_smem(kMaxR, MH, 8));
+    cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)agg_mma_smem(kMaxR, MH));
+    cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     // prefer the largest shared-memory carveout so two CTAs fit per SM
     cudaFuncSetAttribute(fourier_aggregate_kernel<MH>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -673,10 +852,18 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
     attr_done = true;
   }
   dim3 grid(p.nch, p.ngroups);
-  if (p.nch > 1)
+  if (p.nch > 1) {
+#if SLAB_AGG_MMA
+    const int tiles = (p.P + 7) / 8;
+    const int ngy = (tiles + SLAB_AGG_MMA_MAXW - 1) / SLAB_AGG_MMA_MAXW;
+    const int tpc = (tiles + ngy - 1) / ngy;
+    fourier_aggregate_mma_kernel<MH><<<dim3(p.nch, ngy), tpc * 32, agg_mma_smem(p.R, MH), st>>>(
+        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry);
+#else
     fourier_aggregate_kernel<MH><<<dim3(p.nch, p.agg_groups), p.agg_warps * 32, p.smem_agg, st>>>(
         xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, p.agg_mpg, b, w.carry);
-  else
+#endif
+  } else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {
     fourier_carry_kernel<<<2 * p.P * ncomp_of(MH), kCarryThreads, 0, st>>>(

@@ -60,6 +60,40 @@ __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi,
   acc.fz = fma(fmag, dz, acc.fz);
 }
 
+// Branch-free form of pair_accumulate for the neighbour-list kernel: list
+// entries already passed the conservative screen, so nearly every pair is in
+// range and the out-of-range / coincident ones are masked (charge product 0,
+// finite stand-in distance) instead of branched around.  Without the early
+// returns the four pairs in flight become independent dependency chains the
+// scheduler can interleave.  Masked pairs add exact zeros.
+__device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, double zi, double qi,
+                                                       double xj, double yj, double zj, double qj,
+                                                       double lx, double ly, double ilx, double ily,
+                                                       double alpha, double rc2, double c,
+                                                       const double* __restrict__ etab,
+                                                       PairAcc& acc, int& flag) {
+  double dx = __dsub_rn(xi, xj), dy = __dsub_rn(yi, yj);
+  const double dz = __dsub_rn(zi, zj);
+  dx = __dsub_rn(dx, __dmul_rn(lx, rint(__dmul_rn(dx, ilx))));
+  dy = __dsub_rn(dy, __dmul_rn(ly, rint(__dmul_rn(dy, ily))));
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const bool in = d2 <= rc2;
+  const bool coincident = d2 < 1e-24;
+  flag |= (in && coincident) ? 1 : 0;
+  const bool use = in && !coincident;
+  const double d2u = use ? d2 : rc2;
+  const double inv_d = rsqrt(d2u);
+  const double d = d2u * inv_d;
+  const double qq = use ? qi * qj : 0.0;
+  double e, g;
+  erfc_gauss(alpha * d, etab, &e, &g);
+  acc.e = fma(qq * e, inv_d, acc.e);
+  const double fmag = qq * (e * inv_d + c * g) * (inv_d * inv_d);
+  acc.fx = fma(fmag, dx, acc.fx);
+  acc.fy = fma(fmag, dy, acc.fy);
+  acc.fz = fma(fmag, dz, acc.fz);
+}
+
 // ewald2d.py:126-138
 __global__ void cell_index_kernel(const double* __restrict__ pos, int64_t n, double lx, double ly,
                                   double lz, int ncx, int ncy, int ncz, uint32_t* __restrict__ key,
@@ -101,6 +135,14 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
 }
 
 constexpr int kSRThreads = 128;
+#ifndef SLAB_PAIR_MASKED
+#define SLAB_PAIR_MASKED 1
+#endif
+#if SLAB_PAIR_MASKED
+#define PAIR_FN pair_accumulate_masked
+#else
+#define PAIR_FN pair_accumulate
+#endif
 constexpr int kRing = 16;  // staged neighbour indices per thread (two 32-byte sectors)
 
 // Pass 1: neighbour rows.  One thread per home particle in cell order.  Cells
@@ -214,18 +256,18 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     for (; k + 4 <= cnt; k += 4) {
       const int4 j4 = *reinterpret_cast<const int4*>(row + k);
       const double4 p0 = cp[j4.x], p1 = cp[j4.y], p2 = cp[j4.z], p3 = cp[j4.w];
-      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p0.x, p0.y, p0.z, p0.w, lx, ly, ilx, ily, alpha,
+      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p0.x, p0.y, p0.z, p0.w, lx, ly, ilx, ily, alpha,
                       rc2, c, etab, acc, flag);
-      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p1.x, p1.y, p1.z, p1.w, lx, ly, ilx, ily, alpha,
+      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p1.x, p1.y, p1.z, p1.w, lx, ly, ilx, ily, alpha,
                       rc2, c, etab, acc, flag);
-      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p2.x, p2.y, p2.z, p2.w, lx, ly, ilx, ily, alpha,
+      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p2.x, p2.y, p2.z, p2.w, lx, ly, ilx, ily, alpha,
                       rc2, c, etab, acc, flag);
-      pair_accumulate(pi.x, pi.y, pi.z, pi.w, p3.x, p3.y, p3.z, p3.w, lx, ly, ilx, ily, alpha,
+      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p3.x, p3.y, p3.z, p3.w, lx, ly, ilx, ily, alpha,
                       rc2, c, etab, acc, flag);
     }
     for (; k < cnt; ++k) {
       const double4 pj = cp[row[k]];
-      pair_accumulate(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
+      PAIR_FN(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
                       rc2, c, etab, acc, flag);
     }
     const int64_t i = order[a];
