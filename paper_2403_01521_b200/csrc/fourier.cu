@@ -42,7 +42,12 @@ namespace slab {
 #ifndef SLAB_AGG_MMA
 #define SLAB_AGG_MMA 1  // phase 1 on DMMA (0: DFMA lane-per-item kernel)
 #endif
-constexpr int kSB = SLAB_SWEEP_SB;  // force staging batch (particles)
+constexpr int kSB = SLAB_SWEEP_SB;
+#ifndef SLAB_SWEEP_MAXT
+#define SLAB_SWEEP_MAXT 256
+#endif
+// sweep CTA size cap: 2 CTAs/SM at 65536 / (2 * cap) registers per thread
+constexpr int kSweepMaxThreads = SLAB_SWEEP_MAXT;  // force staging batch (particles)
 constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
 constexpr int kMaxR = 256;
 
@@ -399,11 +404,18 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, 2) fourier_aggregate_m
 // ---------------------------------------------------------------------------
 // phase 2: carry scan over chunks (in place: aggregates -> carried-in states)
 // ---------------------------------------------------------------------------
-// One 128-thread block per chain (item, component): thread t composes a
-// contiguous block of ~nch/128 chunks, a shuffle + shared-memory scan composes
-// the thread blocks, then each thread rewrites its block with the exclusive
-// carries.  Affine map per chunk: T -> D T + X.
-constexpr int kCarryThreads = 128;
+// Lanes are 32 consecutive items of one component (contiguous in the carry
+// array, so every load / store is a 512-byte coalesced row) and each warp of a
+// CTA owns one contiguous segment of chunks.  Pass 1 composes the segment's
+// affine maps T -> D T + X, the segments are composed across warps through
+// shared memory, pass 2 rewrites the segment with the exclusive carries.
+#ifndef SLAB_CARRY_SEGS
+#define SLAB_CARRY_SEGS 32
+#endif
+#ifndef SLAB_CARRY_BATCH
+#define SLAB_CARRY_BATCH 4
+#endif
+constexpr int kCarrySegs = SLAB_CARRY_SEGS;  // warps per CTA
 
 __device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, int l, int mh,
                                           double k, const double2* __restrict__ Df,
@@ -427,14 +439,17 @@ __device__ __forceinline__ AffC acompose(const AffC& a, const AffC& b) {
   return AffC{cmul(b.D, a.D), C2{x.re + b.X.re, x.im + b.X.im}};
 }
 
-__global__ void __launch_bounds__(kCarryThreads) fourier_carry_kernel(
+__global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_kernel(
     double2* __restrict__ carry, int nch, int P, int mh, const double* __restrict__ modetab,
     const double2* __restrict__ Df, const double2* __restrict__ Db,
     const double* __restrict__ zbound) {
-  __shared__ AffC wagg[kCarryThreads / 32];
+  __shared__ AffC segm[kCarrySegs][32];
   const int nitems = 2 * P, nc = ncomp_of(mh);
-  const int chain = blockIdx.x;
-  const int item = chain % nitems, comp = chain / nitems;
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int comp = blockIdx.y;
+  const int item_raw = blockIdx.x * 32 + lane;
+  const bool valid = item_raw < nitems;
+  const int item = valid ? item_raw : nitems - 1;
   const bool fwd = item < P;
   const int t = fwd ? item : item - P;
   const bool isg = comp == 2 * mh;
@@ -442,11 +457,10 @@ __global__ void __launch_bounds__(kCarryThreads) fourier_carry_kernel(
   const double k = modetab[(size_t)t * mode_stride(mh) + 2];
   const size_t cstride = (size_t)nc * nitems;
   double2* base = carry + (size_t)comp * nitems + item;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (nch + kCarryThreads - 1) / kCarryThreads;
-  const int s0 = tid * per, s1 = min(nch, s0 + per);
-  constexpr int B = 8;
-  // pass 1: compose this thread's block (loads batched ahead)
+  const int per = (nch + kCarrySegs - 1) / kCarrySegs;
+  const int s0 = seg * per, s1 = min(nch, s0 + per);
+  constexpr int B = SLAB_CARRY_BATCH;
+  // pass 1: compose this segment (loads batched ahead of the dependent chain)
   AffC M{C2{1.0, 0.0}, C2{0.0, 0.0}};
   for (int sb = s0; sb < s1; sb += B) {
     double2 xs[B];
@@ -464,24 +478,14 @@ __global__ void __launch_bounds__(kCarryThreads) fourier_carry_kernel(
     for (int j = 0; j < B; ++j)
       if (sb + j < s1) M = acompose(M, AffC{ds[j], C2{xs[j].x, xs[j].y}});
   }
-  // inclusive scan over threads (earlier threads applied first)
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    AffC u;
-    u.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, o), __shfl_up_sync(0xffffffffu, M.D.im, o)};
-    u.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, o), __shfl_up_sync(0xffffffffu, M.X.im, o)};
-    if (lane >= o) M = acompose(u, M);
-  }
-  if (lane == 31) wagg[warp] = M;
+  segm[seg][lane] = M;
   __syncthreads();
-  AffC pre{C2{1.0, 0.0}, C2{0.0, 0.0}};  // all earlier warps
-  for (int w = 0; w < warp; ++w) pre = acompose(pre, wagg[w]);
-  AffC excl;  // exclusive within the warp
-  excl.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, 1), __shfl_up_sync(0xffffffffu, M.D.im, 1)};
-  excl.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, 1), __shfl_up_sync(0xffffffffu, M.X.im, 1)};
-  if (lane == 0) excl = AffC{C2{1.0, 0.0}, C2{0.0, 0.0}};
-  C2 T = acompose(pre, excl).X;  // carried state entering this thread's block (T0 = 0)
-  // pass 2: rewrite the block with exclusive carries
+  // carried state entering this segment: earlier segments applied in order (T0 = 0)
+  AffC pre{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  for (int w = 0; w < seg; ++w) pre = acompose(pre, segm[w][lane]);
+  C2 T = pre.X;
+  if (!valid) return;
+  // pass 2: rewrite the segment with exclusive carries
   for (int sb = s0; sb < s1; sb += B) {
     double2 xs[B];
     C2 ds[B];
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(kCarryThreads) fourier_carry_kernel(
 // (forward and backward lanes to separate buffers), reduced in fixed order
 // afterwards: deterministic, no atomics.
 template <int MH>
-__global__ void __launch_bounds__(256, 2) fourier_sweep_kernel(
+__global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
     const double* __restrict__ modetab, int P, int ipg, BVec b, const double2* __restrict__ carry,
@@ -768,7 +772,7 @@ FourierPlan fourier_plan(int64_t n, int P, int mh) {
   p.P = P;
   p.mh = mh;
   const int nitems = 2 * P;
-  p.ngroups = (nitems + 255) / 256;
+  p.ngroups = (nitems + kSweepMaxThreads - 1) / kSweepMaxThreads;
   if (p.ngroups < 1) p.ngroups = 1;
   p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
   p.warps = (p.ipg + 31) / 32;
@@ -866,7 +870,7 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
   } else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {
-    fourier_carry_kernel<<<2 * p.P * ncomp_of(MH), kCarryThreads, 0, st>>>(
+    fourier_carry_kernel<<<dim3((2 * p.P + 31) / 32, ncomp_of(MH)), 32 * kCarrySegs, 0, st>>>(
         w.carry, p.nch, p.P, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH, w.zbound);
   }
   fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
