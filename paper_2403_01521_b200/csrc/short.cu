@@ -146,30 +146,30 @@ constexpr int kSRThreads = 128;
 constexpr int kRing = 16;  // staged neighbour indices per thread (two 32-byte sectors)
 
 // Pass 1: neighbour rows.  One thread per home particle in cell order.  Cells
-// are ordered z-fastest, so the 2S+1 z-neighbours of one (x, y) column are one
-// contiguous range: (2S+1)^2 ranges per particle.  S = 2 on cells of edge
-// >= r_c/2 (search volume 25 * 5 / 8 = 15.6 r_c^3 instead of 27 r_c^3 with
-// S = 1 on cells >= r_c).  Conservative fp32 distance screen; hits go to a
+// are ordered z-fastest, so the z cells of one (x, y) column are one contiguous
+// range: at most (2S+1)^2 ranges per particle, each trimmed to the z extent the
+// r_c sphere has over that column (corner columns often drop out).  S = 2 on
+// cells of edge >= r_c/2: mean search volume ~10.5 r_c^3, against 15.6 r_c^3
+// for untrimmed 5-cell columns and 27 r_c^3 for S = 1 on cells >= r_c.  Conservative fp32 distance screen; hits go to a
 // per-thread ring in shared memory (slot-major: conflict-free) and are written
 // as whole 32-byte sectors into the row nbr[(a - a_begin) * kcap + k].
 template <int S>
 __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
     const float4* __restrict__ cpf, const uint32_t* __restrict__ skey,
     const int32_t* __restrict__ start, int64_t a_begin, int64_t a_end, int ncx, int ncy, int ncz,
-    float lxf, float lyf, float rc2f, int kcap, int32_t* __restrict__ nbr,
+    float lxf, float lyf, float lzf, float rc2f, int kcap, int32_t* __restrict__ nbr,
     int32_t* __restrict__ nn, int* __restrict__ maxnn, int* __restrict__ status) {
   __shared__ int32_t ring[kRing][kSRThreads];
   const int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x;
   if (a >= a_end) return;
   const int cid = (int)skey[a];
-  const int cz = cid % ncz, cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
+  const int cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
   const float4 pi = cpf[a];
   const int self = (int)a;
   int32_t* st = &ring[0][threadIdx.x];
   int32_t* row = nbr + (a - a_begin) * (int64_t)kcap;
   int cnt = 0, done = 0;  // hits found / hits already written to the row
-  const int zlo = cz - S < 0 ? 0 : cz - S;
-  const int zhi = cz + S >= ncz ? ncz - 1 : cz + S;
+  const float ex = lxf / ncx, ey = lyf / ncy, izc = ncz / lzf;
   auto flush8 = [&]() {
     if (done + 8 <= kcap) {
       const int s0 = done & (kRing - 1);
@@ -203,9 +203,24 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
       const int uy = cy + oy;
       const int ny = uy < 0 ? uy + ncy : (uy >= ncy ? uy - ncy : uy);
       const float py = pi.y + (uy < 0 ? lyf : (uy >= ncy ? -lyf : 0.0f));
+      // trim the column to the part of the r_c sphere it can hold: skip it when
+      // its xy rectangle is out of reach, else scan only the z cells within
+      // h = sqrt(rc2f - d_xy^2) of the home height (a superset of every pair:
+      // rc2f is inflated, the cell bounds are widened by 1e-3 cells)
+      const float dxr = fmaxf(0.0f, fmaxf(nx * ex - px, px - (nx + 1) * ex));
+      const float dyr = fmaxf(0.0f, fmaxf(ny * ey - py, py - (ny + 1) * ey));
+      const float dxy2 = fmaf(dxr, dxr, dyr * dyr);
+      if (dxy2 > rc2f) continue;
+      const float h = sqrtf(rc2f - dxy2);
+      int zlo = (int)floorf((pi.z - h) * izc - 1e-3f);
+      int zhi = (int)floorf((pi.z + h) * izc + 1e-3f);
+      zlo = zlo < 0 ? 0 : (zlo >= ncz ? ncz - 1 : zlo);
+      zhi = zhi < 0 ? 0 : (zhi >= ncz ? ncz - 1 : zhi);
       const int col = (nx * ncy + ny) * ncz;
       const int b1 = start[col + zhi + 1];
       int jj = start[col + zlo];
+      // (scanning the warp-union of the lanes' ranges instead -- broadcast
+      // loads, no idle lanes -- measured 1.51 ms against 1.13 ms per lane)
       for (; jj + 4 <= b1; jj += 4) {
         const float4 p0 = cpf[jj], p1 = cpf[jj + 1], p2 = cpf[jj + 2], p3 = cpf[jj + 3];
         test(jj, p0, px, py);
@@ -474,11 +489,11 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     const int64_t nblk = (nh + kSRThreads - 1) / kSRThreads;
     if (p.span == 2)
       nbr_build_kernel<2><<<(unsigned)nblk, kSRThreads, 0, st>>>(
-          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, rc2f, p.kcap, nbr,
+          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
     else
       nbr_build_kernel<1><<<(unsigned)nblk, kSRThreads, 0, st>>>(
-          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, rc2f, p.kcap, nbr,
+          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
     pair_list_kernel<<<(unsigned)nblk, kSRThreads, 0, st>>>(cp, order, nbr, nn, h0, h1, p.kcap, lx,
                                                             ly, alpha, rc2, forces, eblk, status);
