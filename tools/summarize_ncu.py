@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (committed evidence).
 
-    python tools/summarize_ncu.py <round_tag> <launches.csv> <full.ncu-rep>
+    python tools/summarize_ncu.py <round_tag> <launches.csv> <full.ncu-rep> [more.ncu-rep ...]
 
 Writes profiles/ncu_<tag>_launches.md (per-kernel share of one step from the
 cold-cache serialised launch list) and profiles/ncu_<tag>_summary.json (per-kernel
@@ -61,7 +61,7 @@ def full_metrics(rep):
         "launch__block_size": "block",
     }
     scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "usecond": 1e-3,
-             "msecond": 1.0, "nsecond": 1e-6}
+             "msecond": 1.0, "nsecond": 1e-6, "us": 1e-3, "ms": 1.0, "ns": 1e-6}
     res = []
     for r in data:
         d = {"kernel": short(r[hdr.index("Kernel Name")])}
@@ -80,8 +80,10 @@ def full_metrics(rep):
 
 
 def main():
-    tag, lpath, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+    tag, lpath, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     tot, cnt = launches(lpath)
+    # not part of the evaluation step: bench.py's live DFMA peak probe, torch fills
+    extra = {k: tot.pop(k) for k in list(tot) if k.startswith("dfma_peak") or k.startswith("at::")}
     grand = sum(tot.values())
     lines = [f"# ncu launch list, round {tag}", "",
              "`ncu --metrics gpu__time_duration.sum --clock-control none` over "
@@ -92,14 +94,16 @@ def main():
         lines.append(f"| {k} | {cnt[k]} | {v / 1e6:.3f} | {100 * v / grand:.1f}% |")
     scan = sum(v for k, v in tot.items() if any(k.startswith(s) for s in SCAN))
     lines += ["", f"SOE-scan kernels (3-phase Fourier scan + k=0 mode + tables): "
-              f"{100 * scan / grand:.1f}% of device time."]
+              f"{100 * scan / grand:.1f}% of device time.", "",
+              "Excluded (outside the evaluation step): " +
+              ", ".join(f"{k} ({v / 1e6:.3f} ms)" for k, v in extra.items())]
     with open(os.path.join(REPO, "profiles", f"ncu_{tag}_launches.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    full = full_metrics(rep)
+    full = [d for rep in reps for d in full_metrics(rep)]
     per_kernel = defaultdict(list)
     for d in full:
         per_kernel[d["kernel"]].append(d)
-    summary = {"round": tag, "source": os.path.basename(rep), "kernels": {}}
+    summary = {"round": tag, "source": [os.path.basename(r) for r in reps], "kernels": {}}
     scan_bytes = 0.0
     for k, ds in per_kernel.items():
         d = ds[-1]
