@@ -591,6 +591,7 @@ __global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
     gk = C2{gg.x, gg.y};
   }
   __syncthreads();
+  if ((fmask | bmask) == 0u) return;  // no items in this warp (its buffer is skipped)
 
   // partial force buffers: one per (group, warp); the single warp that holds
   // both directions sends its backward lanes to the extra buffer G*W
@@ -745,12 +746,23 @@ __global__ void kahan_modes_kernel(const double* __restrict__ se, int P, double*
 }
 
 // forces_sorted += sum of the per-warp partial buffers (fixed order)
+// Buffer b < ngroups * nwarps belongs to warp b % nwarps of item group
+// b / nwarps and is written only if that warp holds items; buffer
+// ngroups * nwarps (when nbuf exceeds the grid) is the mixed warp's backward one.
 __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int nbuf,
+                                            int ngroups, int nwarps, int ipg, int nitems,
                                             int64_t n3, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n3) return;
   double v = 0.0;
-  for (int b = 0; b < nbuf; ++b) v += fpart[(size_t)b * n3 + e];
+  for (int b = 0; b < nbuf; ++b) {
+    if (b < ngroups * nwarps) {
+      const int g = b / nwarps, w = b - g * nwarps;
+      const int cnt = min(nitems, (g + 1) * ipg) - g * ipg;
+      if (32 * w >= cnt) continue;
+    }
+    v += fpart[(size_t)b * n3 + e];
+  }
   out[e] += v;
 }
 
@@ -906,8 +918,8 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
   kahan_modes_kernel<<<1, 1, 0, st>>>(se, p.P, energy_out);
   if (want_forces) {
     const int64_t n3 = p.n * 3;
-    fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(w.fpart, p.nbuf,
-                                                                              n3, forces_sorted);
+    fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(
+        w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, 2 * p.P, n3, forces_sorted);
   }
   return cudaGetLastError();
 }

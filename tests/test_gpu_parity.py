@@ -107,3 +107,16 @@ def test_short_range_matches_reference():
         assert abs(u - float(g["u_s_alone"])) <= E_TOL * abs(float(g["u_s_alone"]))
         fm = np.max(np.abs(g["f_short"]))
         assert np.max(np.abs(f - g["f_short"])) <= F_TOL * fm
+
+
+def test_workspace_reuse_after_larger_problem():
+    """The context arena is reused across evaluations without clearing: a larger
+    problem first (dense walls: neighbour-capacity growth, arena refilled), then
+    a full-mode evaluation whose last item group leaves a warp without items
+    (its force buffer must not be summed)."""
+    import paper_2403_01521_b200 as pk
+    from paper_2403_01521_b200.configs import make_workload
+    wl3 = make_workload("cfg3")
+    pk.short_range_energy_forces(wl3.system, wl3.box, wl3.alpha, wl3.params().r_c)
+    g, wl, bd, f = _run("cfg1")
+    _check(g, bd, f)
