@@ -241,7 +241,7 @@ int slab_fourier_sweep(SlabCtx* ctx, const double* d_x, const double* d_y, const
   int rc = prepare_soe(soe, alpha, sh);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  auto fp = slab::fourier_plan(n, (int)nmode, sh.mh);
+  auto fp = slab::fourier_plan(n, (int)nmode, sh.mh, (want_forces && d_forces_sorted) ? 2 : 1);
   auto zp = slab::zero_plan(n, sh.mh);
   rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, false) + 4096);
   if (rc) return rc;
@@ -348,7 +348,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const SlabBox& box = a->box;
   const double area = box.lx * box.ly;
-  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh);
+  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, (a->want_forces && n > 0) ? 2 : 1);
   auto zp = slab::zero_plan(n, sh.mh);
   auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, a->r_c);
   if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;

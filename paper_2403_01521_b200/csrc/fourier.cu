@@ -39,9 +39,6 @@ namespace slab {
 #ifndef SLAB_SWEEP_PIPE
 #define SLAB_SWEEP_PIPE 0  // 1: next particle's sincos/exp issued one iteration ahead (measured 2.5% slower since exp_neg went branch-free)
 #endif
-#ifndef SLAB_AGG_MMA
-#define SLAB_AGG_MMA 1  // phase 1 on DMMA (0: DFMA lane-per-item kernel)
-#endif
 constexpr int kSB = SLAB_SWEEP_SB;
 #ifndef SLAB_SWEEP_MAXT
 #define SLAB_SWEEP_MAXT 256
@@ -148,99 +145,6 @@ __global__ void mode_table_kernel(const double* __restrict__ modes,
   r[6] = singular;
   r[7] = 0.0;
   if (singular) atomicOr(status, SLAB_STATUS_SINGULAR_DEV);
-}
-
-// ---------------------------------------------------------------------------
-// phase 1: chunk aggregates
-// ---------------------------------------------------------------------------
-template <int MH>
-__global__ void __launch_bounds__(256, 2) fourier_aggregate_kernel(
-    const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
-    const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
-    int ipg, BVec b, double2* __restrict__ carry) {
-  extern __shared__ double4 smem4[];
-  double* sx = reinterpret_cast<double*>(smem4);
-  double* sy = sx + R;
-  double* sz = sy + R;
-  double* sq = sz + R;
-  double2* sw = reinterpret_cast<double2*>(sq + R);  // [2][R][MH]: forward, backward weights
-  const int c = blockIdx.x, g = blockIdx.y;
-  const int64_t a0 = (int64_t)c * R;
-  const int len = (int)(a0 + R < n ? R : n - a0);
-  const double z_end = zs[a0 + len - 1], z_start = zs[a0];
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    sx[i] = xs[a0 + i];
-    sy[i] = ys[a0 + i];
-    sz[i] = zs[a0 + i];
-    sq[i] = qs[a0 + i];
-  }
-  for (int e = threadIdx.x; e < len * MH; e += blockDim.x) {
-    const int i = e / MH, l = e - i * MH;
-    const double z = zs[a0 + i];
-    const double df = z_end - z, db = z - z_start;
-    C2 wf = cexp_neg(b.re[l] * df, b.im[l] * df);
-    C2 wb = cexp_neg(b.re[l] * db, b.im[l] * db);
-    sw[e] = make_double2(wf.re, wf.im);
-    sw[R * MH + e] = make_double2(wb.re, wb.im);
-  }
-  __syncthreads();
-
-  // Lane layout: lanes 0-15 forward, 16-31 backward items of the SAME 16 modes
-  // (mode = g * mpg + 16 * warp + lane % 16), so a lane and its partner lane^16
-  // need identical phases: each computes the sincos of one particle of a pair and
-  // they swap with one shuffle (half the sincos work).  `ipg` = modes per group.
-  const int nitems = 2 * P;
-  const int lane = threadIdx.x & 31;
-  const int t_raw = g * ipg + 16 * (threadIdx.x >> 5) + (lane & 15);
-  const bool active = t_raw < min(P, (g + 1) * ipg);
-  const bool fwd = lane < 16;
-  const int t = active ? t_raw : 0;
-  const int item = fwd ? t : P + t;
-  const double* mt = modetab + (size_t)t * mode_stride(MH);
-  const double kx = mt[0], ky = mt[1], k = mt[2];
-  const double sigma = fwd ? 1.0 : -1.0;
-  const double2* W = sw + (fwd ? 0 : R * MH);
-
-  C2 Racc[MH], Iacc[MH];
-#pragma unroll
-  for (int l = 0; l < MH; ++l) Racc[l] = Iacc[l] = C2{0.0, 0.0};
-  C2 gacc{0.0, 0.0};
-  auto accumulate = [&](int i, double cs, double sn) {
-    const double q = sq[i];
-    const double ur = q * cs, ui = -sigma * q * sn;
-    const double dist = fwd ? (z_end - sz[i]) : (sz[i] - z_start);
-    const double wk = exp_neg_cb(k * dist);
-    gacc.re = fma(ur, wk, gacc.re);
-    gacc.im = fma(ui, wk, gacc.im);
-#pragma unroll
-    for (int l = 0; l < MH; ++l) {
-      const double2 wl = W[i * MH + l];
-      Racc[l].re = fma(ur, wl.x, Racc[l].re);
-      Racc[l].im = fma(ur, wl.y, Racc[l].im);
-      Iacc[l].re = fma(ui, wl.x, Iacc[l].re);
-      Iacc[l].im = fma(ui, wl.y, Iacc[l].im);
-    }
-  };
-  for (int i = 0; i < len; i += 2) {
-    const int mine = min(i + (fwd ? 0 : 1), len - 1);
-    const double th = __dadd_rn(__dmul_rn(kx, sx[mine]), __dmul_rn(ky, sy[mine]));
-    double sn, cs;
-    sincos_fast_cb(th, &sn, &cs);
-    const double cs_o = __shfl_xor_sync(0xffffffffu, cs, 16);
-    const double sn_o = __shfl_xor_sync(0xffffffffu, sn, 16);
-    accumulate(i, fwd ? cs : cs_o, fwd ? sn : sn_o);
-    if (i + 1 < len) accumulate(i + 1, fwd ? cs_o : cs, fwd ? sn_o : sn);
-  }
-  if (active) {
-    const int nc = ncomp_of(MH);
-    double2* out = carry + (size_t)c * nc * nitems + item;
-#pragma unroll
-    for (int l = 0; l < MH; ++l) {
-      out[(size_t)l * nitems] = make_double2(Racc[l].re, Racc[l].im);
-      out[(size_t)(MH + l) * nitems] = make_double2(Iacc[l].re, Iacc[l].im);
-    }
-    out[(size_t)(2 * MH) * nitems] = make_double2(gacc.re, gacc.im);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -440,16 +344,16 @@ __device__ __forceinline__ AffC acompose(const AffC& a, const AffC& b) {
 }
 
 __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_kernel(
-    double2* __restrict__ carry, int nch, int P, int mh, const double* __restrict__ modetab,
-    const double2* __restrict__ Df, const double2* __restrict__ Db,
-    const double* __restrict__ zbound) {
+    double2* __restrict__ carry, int nch, int P, int items, int mh,
+    const double* __restrict__ modetab, const double2* __restrict__ Df,
+    const double2* __restrict__ Db, const double* __restrict__ zbound) {
   __shared__ AffC segm[kCarrySegs][32];
   const int nitems = 2 * P, nc = ncomp_of(mh);
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
   const int comp = blockIdx.y;
   const int item_raw = blockIdx.x * 32 + lane;
-  const bool valid = item_raw < nitems;
-  const int item = valid ? item_raw : nitems - 1;
+  const bool valid = item_raw < items;
+  const int item = valid ? item_raw : items - 1;
   const bool fwd = item < P;
   const int t = fwd ? item : item - P;
   const bool isg = comp == 2 * mh;
@@ -529,8 +433,9 @@ template <int MH>
 __global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
-    const double* __restrict__ modetab, int P, int ipg, BVec b, const double2* __restrict__ carry,
-    double* __restrict__ epart, double* __restrict__ fpart, int want_forces) {
+    const double* __restrict__ modetab, int P, int items, int ipg, BVec b,
+    const double2* __restrict__ carry, double* __restrict__ epart, double* __restrict__ fpart,
+    int want_forces) {
   extern __shared__ double4 smem4[];
   const int nwarps = blockDim.x >> 5;
   double2* sC = reinterpret_cast<double2*>(smem4);         // [MH][blockDim]
@@ -560,7 +465,7 @@ __global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nitems = 2 * P;
   const int item = g * ipg + threadIdx.x;
-  const int gend = min(nitems, (g + 1) * ipg);
+  const int gend = min(items, (g + 1) * ipg);
   const bool active = item < gend;
   const bool fwd = item < P;
   const int t = active ? (fwd ? item : item - P) : 0;
@@ -774,16 +679,17 @@ static size_t sweep_smem(int R, int mh, int warps) {
          sizeof(double) * (3 * (size_t)R + R + 2) +
          sizeof(double) * (size_t)warps * kSB * 3 * kStageStride;
 }
-static size_t agg_smem(int R, int mh) {
-  return sizeof(double) * 4 * (size_t)R + sizeof(double2) * 2 * (size_t)R * mh;
-}
 
-FourierPlan fourier_plan(int64_t n, int P, int mh) {
+FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs) {
   FourierPlan p{};
   p.n = n;
   p.P = P;
   p.mh = mh;
-  const int nitems = 2 * P;
+  // energy-only evaluations need only the forward sweep (the reference's energy
+  // is the forward sum, soewald2d.py:138-170; the backward sweep only adds the
+  // j-side forces, 172-202): active items = dirs * P, carry layout stays 2P
+  p.items = (dirs == 1 ? 1 : 2) * P;
+  const int nitems = p.items;
   p.ngroups = (nitems + kSweepMaxThreads - 1) / kSweepMaxThreads;
   if (p.ngroups < 1) p.ngroups = 1;
   p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
@@ -795,18 +701,12 @@ FourierPlan fourier_plan(int64_t n, int P, int mh) {
   while (R * 2 <= rf && R * 2 <= kMaxR) R *= 2;
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
-  p.smem_agg = agg_smem(R, mh);
   p.smem_sweep = sweep_smem(R, mh, p.warps);
   // one partial force buffer per (group, warp) + one for the backward lanes of
   // the (at most one) warp that holds both directions
   const int g_of_p = P / p.ipg;  // group containing item P (first backward item)
   const bool mixed = P < nitems && ((P - g_of_p * p.ipg) % 32) != 0;
   p.nbuf = p.ngroups * p.warps + (mixed ? 1 : 0);
-  p.agg_groups = (P + 127) / 128;
-  if (p.agg_groups < 1) p.agg_groups = 1;
-  p.agg_mpg = (P + p.agg_groups - 1) / p.agg_groups;
-  p.agg_warps = (p.agg_mpg + 15) / 16;
-  if (p.agg_warps < 1) p.agg_warps = 1;
   return p;
 }
 
@@ -852,42 +752,34 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
                           cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(fourier_aggregate_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)agg_smem(kMaxR, MH));
+    // largest shared-memory carveout so two CTAs of each fit per SM
     cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sweep_smem(kMaxR, MH, 8));
+    cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         100);
     cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)agg_mma_smem(kMaxR, MH));
     cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    // prefer the largest shared-memory carveout so two CTAs fit per SM
-    cudaFuncSetAttribute(fourier_aggregate_kernel<MH>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         100);
     attr_done = true;
   }
   dim3 grid(p.nch, p.ngroups);
   if (p.nch > 1) {
-#if SLAB_AGG_MMA
     const int tiles = (p.P + 7) / 8;
     const int ngy = (tiles + SLAB_AGG_MMA_MAXW - 1) / SLAB_AGG_MMA_MAXW;
     const int tpc = (tiles + ngy - 1) / ngy;
     fourier_aggregate_mma_kernel<MH><<<dim3(p.nch, ngy), tpc * 32, agg_mma_smem(p.R, MH), st>>>(
         xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry);
-#else
-    fourier_aggregate_kernel<MH><<<dim3(p.nch, p.agg_groups), p.agg_warps * 32, p.smem_agg, st>>>(
-        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, p.agg_mpg, b, w.carry);
-#endif
   } else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {
-    fourier_carry_kernel<<<dim3((2 * p.P + 31) / 32, ncomp_of(MH)), 32 * kCarrySegs, 0, st>>>(
-        w.carry, p.nch, p.P, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH, w.zbound);
+    fourier_carry_kernel<<<dim3((p.items + 31) / 32, ncomp_of(MH)), 32 * kCarrySegs, 0, st>>>(
+        w.carry, p.nch, p.P, p.items, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH,
+        w.zbound);
   }
   fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
-      xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.ipg, b, w.carry, w.epart, w.fpart,
-      want_forces);
+      xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
+      w.fpart, want_forces);
   return cudaGetLastError();
 }
 
@@ -919,7 +811,7 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
   if (want_forces) {
     const int64_t n3 = p.n * 3;
     fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(
-        w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, 2 * p.P, n3, forces_sorted);
+        w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted);
   }
   return cudaGetLastError();
 }

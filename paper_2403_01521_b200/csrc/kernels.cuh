@@ -52,10 +52,10 @@ struct FourierPlan {
   int ipg;        // items per group
   int warps;      // warps per CTA
   int nbuf;       // partial force buffers (per group x warp, + 1 if a warp mixes directions)
-  int agg_groups, agg_mpg, agg_warps;  // aggregate kernel: modes per group, 16 modes per warp
-  size_t smem_agg, smem_sweep;
+  int items;      // active (mode, direction) items: 2P, or P for energy-only (forward)
+  size_t smem_sweep;
 };
-FourierPlan fourier_plan(int64_t n, int P, int mh);
+FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2);
 // bytes of device workspace the plan needs (carry, chunk decays, mode table, partials)
 struct FourierWork {
   double* modetab;   // P * mode_stride
