@@ -158,6 +158,17 @@ int slab_sample_modes(SlabCtx* ctx, int64_t* d_state, uint64_t seed, double alph
  * slab, assembly, scatter to input order). */
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* args, void* stream);
 
+/* rbse2d.py:320-330 _rb_batch_energy_kernel (the body of run_many_batches):
+ * for b < nbatch, d_out[b] = Kahan-combined forward-sweep energy of modes
+ * d_modes[b*P .. (b+1)*P) (rows kx, ky, |k|), commonv = commonv_scalar for every
+ * mode, no charge constant.  Particles in input order (pos AoS, charge): sorted
+ * once, decay table once, modes swept in groups on device.  ORs status bits
+ * (SINGULAR, NONFINITE) into d_status. */
+int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                        SlabSOE soe, double alpha, double area, const double* d_modes,
+                        int64_t nbatch, int64_t P, double commonv_scalar, double* d_out,
+                        int* d_status, void* stream);
+
 /* Recursion of soewald2d.py:42-64 recursive_pair_sum on sorted z:
  * out[a] = sum_{j<a} q_j exp(-i theta_j - beta (z_a - z_j)), complex interleaved. */
 int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,

@@ -29,7 +29,7 @@ EXPORTED = (
     "slab_ctx_create", "slab_ctx_destroy", "slab_last_error", "slab_version",
     "slab_sort_by_z", "slab_fourier_sweep", "slab_zero_mode_sweep", "slab_short_range",
     "slab_sample_modes", "slab_evaluate", "slab_recursive_pair_sum", "slab_fp64_peak",
-    "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors",
+    "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors", "slab_batch_energies",
 )
 
 
@@ -103,6 +103,8 @@ def load():
                                       vp, vp]
     lib.slab_evaluate.argtypes = [vp, ctypes.POINTER(SlabEvalArgs), vp]
     lib.slab_recursive_pair_sum.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, vp, vp]
+    lib.slab_batch_energies.argtypes = [vp, vp, vp, i64, SlabSOE, dbl, dbl, vp, i64, i64, dbl, vp,
+                                        vp, vp]
     lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
     lib.slab_ctx_neighbor_capacity.argtypes = [vp, cint]
     lib.slab_ctx_last_max_neighbors.argtypes = [vp, ctypes.POINTER(cint)]

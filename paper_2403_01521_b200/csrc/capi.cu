@@ -321,6 +321,50 @@ int slab_sample_modes(SlabCtx* ctx, int64_t* d_state, uint64_t seed, double alph
   return SLAB_OK;
 }
 
+int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                        SlabSOE soe, double alpha, double area, const double* d_modes,
+                        int64_t nbatch, int64_t P, double commonv_scalar, double* d_out,
+                        int* d_status, void* stream) {
+  if (!ctx || n < 0 || nbatch < 0 || P < 1 || !d_out || !d_status ||
+      (n > 0 && (!d_pos || !d_charge)) || (nbatch > 0 && !d_modes))
+    return fail(SLAB_ERR_ARG, "bad batch-energy arguments");
+  if (n > INT32_MAX) return fail(SLAB_ERR_ARG, "n exceeds int32 indexing");
+  if (!(alpha > 0)) return fail(SLAB_ERR_ARG, "alpha must be positive");
+  SOEHost sh;
+  int rc = prepare_soe(soe, alpha, sh);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nbatch == 0) return SLAB_OK;
+  if (n < 2) {
+    CK(cudaMemsetAsync(d_out, 0, sizeof(double) * nbatch, st));
+    return SLAB_OK;
+  }
+  // batches per launch: ~4096 modes keeps the carries modest and the grid full
+  int64_t per = 4096 / P;
+  per = per < 1 ? 1 : (per > nbatch ? nbatch : per);
+  auto fp = slab::fourier_plan(n, (int)(per * P), sh.mh, 1);
+  auto zp = slab::zero_plan(n, sh.mh);
+  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, true) + 8192);
+  if (rc) return rc;
+  Carver cv{(char*)ctx->arena};
+  SortedWork w{};
+  carve_sorted(cv, n, sh.mh, fp, zp, true, w);
+  slab::FourierWork fw;
+  slab::fourier_work_carve(fp, w.fwork, fw);
+  int32_t* perm = nullptr;
+  CK(slab::sort_by_z_device(d_pos + 2, 3, n, w.sw, st, &perm, d_status));
+  CK(slab::gather_sorted(d_pos, d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, nullptr, st));
+  CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
+  for (int64_t b0 = 0; b0 < nbatch; b0 += per) {
+    const int64_t nb = nbatch - b0 < per ? nbatch - b0 : per;
+    auto fpb = slab::fourier_plan(n, (int)(nb * P), sh.mh, 1);
+    CK(slab::fourier_run(fpb, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, d_modes + 3 * b0 * P, nullptr,
+                         commonv_scalar, area, sh.b, sh.w, 0, d_out + b0, d_status, nullptr, st,
+                         (int)P));
+  }
+  return SLAB_OK;
+}
+
 int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,
                             const double* d_z, int64_t n, double beta_re, double beta_im,
                             double* d_out, void* stream) {

@@ -638,16 +638,20 @@ __global__ void __launch_bounds__(256) fourier_mode_energy_kernel(
   if (threadIdx.x == 0) se[t] = modetab[(size_t)t * mode_stride(mh) + 3] * red[0];
 }
 
-__global__ void kahan_modes_kernel(const double* __restrict__ se, int P, double* __restrict__ out) {
-  if (threadIdx.x || blockIdx.x) return;
+// Kahan over modes in mode order exactly like soewald2d.py:204-207, one thread
+// per segment of seg_len consecutive modes (one segment = the whole sum)
+__global__ void kahan_modes_kernel(const double* __restrict__ se, int nseg, int seg_len,
+                                   double* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
   double u = 0.0, comp = 0.0;
-  for (int t = 0; t < P; ++t) {
+  for (int t = s * seg_len; t < (s + 1) * seg_len; ++t) {
     const double y = se[t] - comp;
     const double tt = u + y;
     comp = (tt - u) - y;
     u = tt;
   }
-  out[0] = u;
+  out[s] = u;
 }
 
 // forces_sorted += sum of the per-warp partial buffers (fixed order)
@@ -788,8 +792,9 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
                         const double2* dtab, const double* modes, const double* commonv,
                         double commonv_scalar, double area, const BVec& b, const WVec& wv,
                         int want_forces, double* energy_out, int* status, double* forces_sorted,
-                        cudaStream_t st) {
+                        cudaStream_t st, int seg_len) {
   if (p.P <= 0 || p.n < 2) return cudaSuccess;
+  if (seg_len <= 0 || p.P % seg_len != 0) seg_len = p.P;
   mode_table_kernel<<<(p.P + 127) / 128, 128, 0, st>>>(modes, commonv, commonv_scalar, p.P, p.mh,
                                                        area, b, wv, w.modetab, status);
   const int nb = p.nch * p.mh;
@@ -807,7 +812,8 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
   if (e != cudaSuccess) return e;
   double* se = w.epart + (size_t)p.nch * p.P;  // P scratch doubles after the partials
   fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.nch, p.P, p.mh, w.modetab, se);
-  kahan_modes_kernel<<<1, 1, 0, st>>>(se, p.P, energy_out);
+  const int nseg = p.P / seg_len;
+  kahan_modes_kernel<<<(nseg + 127) / 128, 128, 0, st>>>(se, nseg, seg_len, energy_out);
   if (want_forces) {
     const int64_t n3 = p.n * 3;
     fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(

@@ -74,7 +74,7 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
                         const double2* dtab, const double* modes, const double* commonv,
                         double commonv_scalar, double area, const BVec& b, const WVec& wv,
                         int want_forces, double* energy_out, int* status, double* forces_sorted,
-                        cudaStream_t st);
+                        cudaStream_t st, int seg_len = 0);  // seg_len > 0: energy per segment
 
 // ---------------------------------------------------------------- zero.cu
 struct ZeroPlan {

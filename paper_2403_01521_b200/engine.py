@@ -170,6 +170,19 @@ class Engine:
             int(thin), int(burn_in), int(P), _ptr(modes), _ptr(idx), self._stream()),
             "slab_sample_modes")
 
+    def batch_energies(self, pos, charge, soe, alpha, area, modes, nbatch, P, commonv):
+        """Forward-sweep energies of nbatch consecutive P-mode batches (device (nbatch,)
+        tensor) and the status word (device int32)."""
+        torch = _torch()
+        out = torch.empty(nbatch, dtype=torch.float64, device=self.device)
+        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        pack = _SOEPack(soe)
+        check(self.lib.slab_batch_energies(
+            self.ctx, _ptr(pos), _ptr(charge), charge.numel(), pack.struct, float(alpha),
+            float(area), _ptr(modes), int(nbatch), int(P), float(commonv), _ptr(out),
+            _ptr(status), self._stream()), "slab_batch_energies")
+        return out, status
+
     def recursive_pair_sum(self, q, theta, z, beta):
         torch = _torch()
         out = torch.empty((q.numel(), 2), dtype=torch.float64, device=self.device)

@@ -23,6 +23,7 @@ from scipy.special import erfc
 
 from .core import BoxGeometry, EwaldParams, ParticleSystem, enumerate_kmodes
 from .soe import SOEApprox
+from .ewald2d import raise_on_status
 from .soewald2d import _breakdown, device_evaluate
 
 SQRT_PI = math.sqrt(math.pi)
@@ -207,15 +208,14 @@ def run_many_batches(system: ParticleSystem, box: BoxGeometry, params: EwaldPara
     from .engine import get_engine, to_device
     eng = get_engine()
     pos, q = to_device(system.pos), to_device(system.charge)
-    import torch
-    energies = torch.empty((n_batches, 8), dtype=torch.float64, device=eng.device)
-    cv = _rb_commonv(H, P, alpha)
-    for b in range(n_batches):
-        modes = sampler.batch_device(P)
-        eng.evaluate(pos, q, box, alpha, params.r_c, soe, modes, cv, 0.0, energy=energies[b],
-                     want_forces=False, skip_short_range=True)
-    e = energies.cpu().numpy()
-    return e[:, 1] + u_det
+    # rbse2d.py:346-363: all n_batches * P modes drawn as one chain continuation,
+    # then one batched forward-sweep energy launch sequence (sort and decay
+    # table once; ~4096 modes per device pass)
+    modes = sampler.batch_device(n_batches * P)
+    e, status = eng.batch_energies(pos, q, soe, alpha, box.area, modes, n_batches, P,
+                                   _rb_commonv(H, P, alpha))
+    raise_on_status(int(status.cpu().item()))
+    return e.cpu().numpy() + u_det
 
 
 def variance_diagnostics(estimates: np.ndarray) -> dict:

@@ -372,3 +372,26 @@ def test_graph_replay_and_shard_sum_equal_single_eval(pk):
     for val, key in zip(e, ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps")):
         assert val == pytest.approx(float(g[key]), rel=1e-10), key
     np.testing.assert_allclose(f, g["forces"], rtol=0, atol=1e-9 * float(g["fmax"]))
+
+
+def test_run_many_batches_matches_per_batch_estimates(pk):
+    """Batched forward-sweep energies (slab_batch_energies, several device passes)
+    equal one rb_energy_estimate per batch plus the deterministic terms.  Like the
+    reference (rbse2d.py:346), all n_batches * P modes come from ONE sampler call
+    (chain draws are not invariant under re-batching, there or here)."""
+    box = pk.BoxGeometry(10.0, 10.0, 5.0)
+    s = _slab_system(pk, 25, box, 63)
+    params = pk.make_ewald_params(0.8, 4.0, box)
+    soe8 = pk.build_soe_contour(8)
+    P, nb = 16, 600  # 9600 modes: three 4096-mode passes
+    est = pk.run_many_batches(s, box, params, soe8, n_batches=nb, P=P, seed=21)
+    H = pk.normalization_H(0.8, box)
+    c_q = pk.charge_term_sum(0.8, box, float(np.sum(s.charge ** 2)))
+    bd, _ = pk.soe_energy_forces(s, box, params, soe8)
+    det = bd.u_s + bd.u_l_0 - bd.u_self + bd.u_ps
+    allm = pk.ModeSampler(0.8, box, seed=21).batch(nb * P)
+    for b in range(nb):
+        modes = allm[b * P:(b + 1) * P]
+        if b % 97 == 0 or b == nb - 1:
+            want = pk.rb_energy_estimate(s, box, 0.8, soe8, modes, H, c_q) + det
+            assert est[b] == pytest.approx(want, rel=1e-12, abs=1e-12), b
