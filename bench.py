@@ -250,19 +250,53 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def count_launches(ev, torch):
-    """Kernels of OUR library launched by one step (torch.profiler / CUPTI)."""
+def profile_step(ev, torch):
+    """One step under torch.profiler (CUPTI): (kernel launches of OUR library,
+    {kernel name: device ms}).  Outside the timed region."""
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         ev.step()
         torch.cuda.synchronize()
     n = 0
+    times = {}
     for e in prof.events():
         name = getattr(e, "name", "")
         if "slab::" in name and getattr(e, "device_type", None) is not None:
             if str(e.device_type).endswith("CUDA"):
                 n += 1
-    return n
+                t = getattr(e, "device_time", None)
+                if t is None:
+                    t = getattr(e, "cuda_time", 0.0)
+                key = name.split("(")[0].replace("void ", "").replace("slab::", "")
+                times[key] = times.get(key, 0.0) + t / 1e3
+    return n, times
+
+
+def components(times, n, P, r_c, density):
+    """Per-sub-path device time of one step (SURVEY 8(d) asks for the short range
+    in pairs/s and fp64 terms, the sort in GB/s)."""
+    def pick(pred):
+        return sum(v for k, v in times.items() if pred(k))
+    sr = pick(lambda k: k.startswith(("cell_", "nbr_build", "pair_list", "half_sum",
+                                      "brute_")) or k.endswith("<unsigned int>"))
+    zsort = pick(lambda k: k.startswith(("zkey_init", "gather_sorted", "perm_to")) or
+                 k.endswith("<unsigned long>") or k.startswith(("scan_rows", "add_digit")))
+    scan = pick(lambda k: k.startswith(("fourier_", "zero_", "decay_table", "chunk_bounds",
+                                        "mode_table", "kahan_modes")))
+    pairs = 0.5 * n * (4.0 / 3.0) * np.pi * r_c ** 3 * density  # in-range pairs (mean density)
+    # LSD radix over 64-bit keys: 8 passes x N x (key 8 + value 4 B) read + written
+    sort_bytes = 8 * n * 24
+    return {
+        "note": "device ms per step from one torch.profiler pass (outside the timed region)",
+        "soe_scan_ms": scan,
+        "short_range_ms": sr,
+        "short_range_pairs_per_s": pairs / (sr * 1e-3) if sr else None,
+        "short_range_pairs": pairs, "pairs_basis": "0.5 N (4/3) pi r_c^3 rho (mean density)",
+        "z_sort_ms": zsort,
+        "z_sort_GBps": sort_bytes / (zsort * 1e-3) / 1e9 if zsort else None,
+        "z_sort_bytes": sort_bytes, "hbm_peak_GBps": 6542,
+        "other_ms": sum(times.values()) - scan - sr - zsort,
+    }
 
 
 def scan_flops(n, P, m, world):
@@ -313,7 +347,7 @@ def run_ours(args, rank, world, local):
         ev.capture()
         for _ in range(2):
             ev.step()
-    launches_per_step = count_launches(ev, torch) if rank == 0 else 0
+    launches_per_step, ktimes = profile_step(ev, torch) if rank == 0 else (0, {})
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident, CUDA events, max over ranks ----
@@ -405,6 +439,8 @@ def run_ours(args, rank, world, local):
                      "traffic": load_traffic()},
         "clocks": clk,
         "gpu_launches": launches_per_step * K,
+        "components": components(ktimes, wl.n, wl.P, params.r_c,
+                                 wl.n / (wl.box.lx * wl.box.ly * wl.box.lz)),
         "energy_total": float(e[0] + e[1] + e[2] - e[3] + e[4]),
         "status": status,
         "e2e": e2e,
