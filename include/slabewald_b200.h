@@ -55,7 +55,8 @@ enum {
   SLAB_STATUS_SINGULAR = 2,   /* |b_l - k| < 2e-6 k: soewald2d.py:118-121 (analytic branch) */
   SLAB_STATUS_NBR_OVERFLOW = 4, /* a short-range neighbour row exceeded its capacity: results
                                    are invalid; raise it (slab_ctx_neighbor_capacity) and rerun */
-  SLAB_STATUS_NONFINITE = 8     /* a z coordinate is not finite (core.py:206-207): results invalid */
+  SLAB_STATUS_NONFINITE = 8,    /* a z coordinate is not finite (core.py:206-207): results invalid */
+  SLAB_STATUS_WALL = 16         /* a particle at or beyond a wall (md.py:72) */
 };
 
 typedef struct SlabBox {
@@ -168,6 +169,35 @@ int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charg
                         SlabSOE soe, double alpha, double area, const double* d_modes,
                         int64_t nbatch, int64_t P, double commonv_scalar, double* d_out,
                         int* d_status, void* stream);
+
+/* ---- device-resident MD step (md.py) ---------------------
+ * WCA core of md.py:34-56 (lj_forces: 4 eps[(s/r)^12 - (s/r)^6] + eps below
+ * 2^(1/6) s, minimum image in x, y): ADDS into d_forces (n,3, input order),
+ * d_energy[0] = energy; coincident pairs set SLAB_STATUS_COINCIDENT. */
+int slab_wca(SlabCtx* ctx, const double* d_pos, int64_t n, SlabBox box, double eps, double sigma,
+             double* d_forces, double* d_energy, int* d_status, void* stream);
+/* md.py:59-77 wall_forces: ADDS the wall z-forces, d_energy[0] = energy,
+ * SLAB_STATUS_WALL for a particle at or beyond a wall. */
+int slab_walls(SlabCtx* ctx, const double* d_pos, int64_t n, double lz, double eps, double sigma,
+               double* d_forces, double* d_energy, int* d_status, void* stream);
+/* md.py:180-193 langevin_step (kick, drift, exact OU with Philox4x32-10 noise
+ * keyed by (seed, *d_counter, particle), drift) followed by the xy wrap of
+ * run_simulation (md.py:245-250) accumulating image offsets into d_shift (n,2)
+ * if not NULL; advances *d_counter on device (graph-capturable). */
+int slab_md_langevin(double* d_pos, double* d_vel, const double* d_forces, const double* d_mass,
+                     int64_t n, double dt, double gamma, double temperature, uint64_t seed,
+                     int64_t* d_counter, double* d_shift, double lx, double ly, void* stream);
+/* v += h F / m */
+int slab_md_kick(double* d_vel, const double* d_forces, const double* d_mass, int64_t n,
+                 double h, void* stream);
+/* x += dt v, then the xy wrap (d_shift as above) */
+int slab_md_drift(double* d_pos, const double* d_vel, int64_t n, double dt, double* d_shift,
+                  double lx, double ly, void* stream);
+/* v *= s (Nose-Hoover, md.py:205-217) */
+int slab_md_scale(double* d_vel, int64_t n, double s, void* stream);
+/* d_out[0] = 0.5 sum m v^2 (md.py:176-177), fixed-order reduction */
+int slab_md_kinetic(SlabCtx* ctx, const double* d_vel, const double* d_mass, int64_t n,
+                    double* d_out, void* stream);
 
 /* Recursion of soewald2d.py:42-64 recursive_pair_sum on sorted z:
  * out[a] = sum_{j<a} q_j exp(-i theta_j - beta (z_a - z_j)), complex interleaved. */

@@ -24,12 +24,15 @@ SLAB_STATUS_COINCIDENT = 1
 SLAB_STATUS_SINGULAR = 2
 SLAB_STATUS_NBR_OVERFLOW = 4
 SLAB_STATUS_NONFINITE = 8
+SLAB_STATUS_WALL = 16
 
 EXPORTED = (
     "slab_ctx_create", "slab_ctx_destroy", "slab_last_error", "slab_version",
     "slab_sort_by_z", "slab_fourier_sweep", "slab_zero_mode_sweep", "slab_short_range",
     "slab_sample_modes", "slab_evaluate", "slab_recursive_pair_sum", "slab_fp64_peak",
     "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors", "slab_batch_energies",
+    "slab_wca", "slab_walls", "slab_md_langevin", "slab_md_kick", "slab_md_drift",
+    "slab_md_scale", "slab_md_kinetic",
 )
 
 
@@ -105,6 +108,14 @@ def load():
     lib.slab_recursive_pair_sum.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, vp, vp]
     lib.slab_batch_energies.argtypes = [vp, vp, vp, i64, SlabSOE, dbl, dbl, vp, i64, i64, dbl, vp,
                                         vp, vp]
+    lib.slab_wca.argtypes = [vp, vp, i64, SlabBox, dbl, dbl, vp, vp, vp, vp]
+    lib.slab_walls.argtypes = [vp, vp, i64, dbl, dbl, dbl, vp, vp, vp, vp]
+    lib.slab_md_langevin.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, dbl, ctypes.c_uint64, vp, vp,
+                                     dbl, dbl, vp]
+    lib.slab_md_kick.argtypes = [vp, vp, vp, i64, dbl, vp]
+    lib.slab_md_drift.argtypes = [vp, vp, i64, dbl, vp, dbl, dbl, vp]
+    lib.slab_md_scale.argtypes = [vp, i64, dbl, vp]
+    lib.slab_md_kinetic.argtypes = [vp, vp, vp, i64, vp, vp]
     lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
     lib.slab_ctx_neighbor_capacity.argtypes = [vp, cint]
     lib.slab_ctx_last_max_neighbors.argtypes = [vp, ctypes.POINTER(cint)]

@@ -205,3 +205,33 @@ def sort_by_z(system: ParticleSystem, lz: float) -> np.ndarray:
         raise ValueError("z coordinates must be finite")
     from .engine import device_sort_perm
     return device_sort_perm(np.ascontiguousarray(z), float(lz))
+
+
+# ---------------------------------------------------------------------------
+# particle CSV (reference core.py:305-329): header id,q,m,x,y,z,vx,vy,vz, rows in
+# any order, read back ordered by id; written with 17 significant digits so a
+# save / load round trip is exact.
+# ---------------------------------------------------------------------------
+PARTICLE_CSV_HEADER = "id,q,m,x,y,z,vx,vy,vz"
+
+
+def load_particles(path, box: BoxGeometry | None = None) -> ParticleSystem:
+    import csv
+    with open(path, newline="") as fh:
+        rows = list(csv.reader(fh))
+    if not rows or [c.strip() for c in rows[0]] != PARTICLE_CSV_HEADER.split(","):
+        raise ValueError(f"particle CSV must have header {PARTICLE_CSV_HEADER}")
+    body = [r for r in rows[1:] if r and any(c.strip() for c in r)]
+    a = np.array([[float(c) for c in r] for r in body], dtype=np.float64).reshape(-1, 9)
+    a = a[np.argsort(a[:, 0], kind="stable")]
+    return make_system(a[:, 1], a[:, 2], a[:, 3:6], a[:, 6:9], box=box)
+
+
+def save_particles(path, system: ParticleSystem) -> None:
+    vel = system.vel if system.vel is not None else np.zeros((system.n, 3))
+    lines = [PARTICLE_CSV_HEADER]
+    for i in range(system.n):
+        vals = (system.charge[i], system.mass[i], *system.pos[i], *vel[i])
+        lines.append(str(i) + "," + ",".join(f"{v:.17g}" for v in vals))
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")

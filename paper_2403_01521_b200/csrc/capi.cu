@@ -38,6 +38,8 @@ struct SlabCtx {
   int64_t sampler_cap = 0;
   int kcap_min = 0;        // learned short-range neighbour-row capacity (grow-only)
   int* d_maxnn = nullptr;  // longest neighbour row of the last short-range run
+  double* md_part = nullptr;  // block partials of the O(N) MD reductions
+  int64_t md_part_cap = 0;
 };
 
 namespace {
@@ -190,6 +192,7 @@ int slab_ctx_destroy(SlabCtx* ctx) {
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->sampler_scratch) cudaFree(ctx->sampler_scratch);
   if (ctx->d_maxnn) cudaFree(ctx->d_maxnn);
+  if (ctx->md_part) cudaFree(ctx->md_part);
   delete ctx;
   return SLAB_OK;
 }
@@ -362,6 +365,90 @@ int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charg
                          commonv_scalar, area, sh.b, sh.w, 0, d_out + b0, d_status, nullptr, st,
                          (int)P));
   }
+  return SLAB_OK;
+}
+
+// ---------------------------------------------------------------- MD step (md.cu)
+static int ensure_md_part(SlabCtx* ctx, int64_t n) {
+  const int64_t need = slab::md_partials(n) + 1;
+  if (need <= ctx->md_part_cap) return SLAB_OK;
+  if (ctx->md_part) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaFree(ctx->md_part));
+  }
+  CK(cudaMalloc(&ctx->md_part, sizeof(double) * need));
+  ctx->md_part_cap = need;
+  return SLAB_OK;
+}
+
+int slab_wca(SlabCtx* ctx, const double* d_pos, int64_t n, SlabBox box, double eps, double sigma,
+             double* d_forces, double* d_energy, int* d_status, void* stream) {
+  if (!ctx || n < 0 || !d_energy || !d_status || (n > 0 && (!d_pos || !d_forces)))
+    return fail(SLAB_ERR_ARG, "bad WCA arguments");
+  if (!(sigma > 0) || eps < 0) return fail(SLAB_ERR_ARG, "WCA needs sigma > 0, eps >= 0");
+  if (n > INT32_MAX) return fail(SLAB_ERR_ARG, "n exceeds int32 indexing");
+  cudaStream_t st = (cudaStream_t)stream;
+  const double cut = 1.122462048309373 * sigma;  // WCA_CUT = 2^(1/6), md.py:31
+  auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, cut);
+  if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;
+  int rc = ensure_arena(ctx, slab::short_work_bytes(sp) + 1024);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
+  CK(slab::short_run(sp, ctx->arena, d_pos, d_pos /* charges unused */, box.lx, box.ly, box.lz,
+                     0.0, cut, d_forces, d_energy, d_status, 0, n, ctx->d_maxnn, st, 1, eps,
+                     sigma, 1));
+  return SLAB_OK;
+}
+
+int slab_walls(SlabCtx* ctx, const double* d_pos, int64_t n, double lz, double eps, double sigma,
+               double* d_forces, double* d_energy, int* d_status, void* stream) {
+  if (!ctx || n < 0 || !d_energy || !d_status || (n > 0 && (!d_pos || !d_forces)))
+    return fail(SLAB_ERR_ARG, "bad wall arguments");
+  int rc = ensure_md_part(ctx, n);
+  if (rc) return rc;
+  CK(slab::md_walls(d_pos, n, lz, eps, sigma, d_forces, d_energy, d_status, ctx->md_part, 0,
+                    (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_md_langevin(double* d_pos, double* d_vel, const double* d_forces, const double* d_mass,
+                     int64_t n, double dt, double gamma, double temperature, uint64_t seed,
+                     int64_t* d_counter, double* d_shift, double lx, double ly, void* stream) {
+  if (n < 0 || !d_counter || (n > 0 && (!d_pos || !d_vel || !d_forces || !d_mass)))
+    return fail(SLAB_ERR_ARG, "bad Langevin arguments");
+  CK(slab::md_langevin(d_pos, d_vel, d_forces, d_mass, n, dt, gamma, temperature, seed, d_counter,
+                       d_shift, lx, ly, (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_md_kick(double* d_vel, const double* d_forces, const double* d_mass, int64_t n,
+                 double h, void* stream) {
+  if (n < 0 || (n > 0 && (!d_vel || !d_forces || !d_mass)))
+    return fail(SLAB_ERR_ARG, "bad kick arguments");
+  CK(slab::md_kick(d_vel, d_forces, d_mass, n, h, (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_md_drift(double* d_pos, const double* d_vel, int64_t n, double dt, double* d_shift,
+                  double lx, double ly, void* stream) {
+  if (n < 0 || (n > 0 && (!d_pos || !d_vel))) return fail(SLAB_ERR_ARG, "bad drift arguments");
+  CK(slab::md_drift(d_pos, d_vel, n, dt, d_shift, lx, ly, (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_md_scale(double* d_vel, int64_t n, double s, void* stream) {
+  if (n < 0 || (n > 0 && !d_vel)) return fail(SLAB_ERR_ARG, "bad scale arguments");
+  CK(slab::md_scale(d_vel, n, s, (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_md_kinetic(SlabCtx* ctx, const double* d_vel, const double* d_mass, int64_t n,
+                    double* d_out, void* stream) {
+  if (!ctx || n < 0 || !d_out || (n > 0 && (!d_vel || !d_mass)))
+    return fail(SLAB_ERR_ARG, "bad kinetic-energy arguments");
+  int rc = ensure_md_part(ctx, n);
+  if (rc) return rc;
+  CK(slab::md_kinetic(d_vel, d_mass, n, d_out, ctx->md_part, (cudaStream_t)stream));
   return SLAB_OK;
 }
 

@@ -22,6 +22,7 @@ constexpr int SLAB_STATUS_COINCIDENT_DEV = 1;         // mirrors SLAB_STATUS_* i
 constexpr int SLAB_STATUS_SINGULAR_DEV = 2;
 constexpr int SLAB_STATUS_NBR_OVERFLOW_DEV = 4;
 constexpr int SLAB_STATUS_NONFINITE_DEV = 8;          // a z coordinate is NaN / inf
+constexpr int SLAB_STATUS_WALL_DEV = 16;              // a particle at or beyond a wall (md.py:72)
 
 // Per-mode coefficient record (doubles), built by mode_table_kernel.
 //   [0]=kx [1]=ky [2]=|k| [3]=ck=(pi/A)C_t/k [4]=cz=(pi/A)C_t [5]=kappa (real)

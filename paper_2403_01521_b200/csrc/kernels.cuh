@@ -106,7 +106,25 @@ size_t short_work_bytes(const ShortPlan& p);
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
                       double* energy_out, int* status, int64_t home_begin, int64_t home_end,
-                      int* maxnn_out, cudaStream_t st);
+                      int* maxnn_out, cudaStream_t st, int kind = 0, double lj_eps = 0.0,
+                      double lj_sigma = 0.0,  // kind 1: WCA core instead of erfc Coulomb
+                      int accumulate = 0);    // 1: forces += (full home range only)
+
+// ---------------------------------------------------------------- md.cu
+int64_t md_partials(int64_t n);
+cudaError_t md_langevin(double* pos, double* vel, const double* forces, const double* mass,
+                        int64_t n, double dt, double gamma, double temperature, uint64_t seed,
+                        int64_t* counter, double* shift, double lx, double ly, cudaStream_t st);
+cudaError_t md_kick(double* vel, const double* forces, const double* mass, int64_t n, double h,
+                    cudaStream_t st);
+cudaError_t md_drift(double* pos, const double* vel, int64_t n, double dt, double* shift, double lx,
+                     double ly, cudaStream_t st);
+cudaError_t md_scale(double* vel, int64_t n, double s, cudaStream_t st);
+cudaError_t md_walls(const double* pos, int64_t n, double lz, double eps, double sigma,
+                     double* forces, double* energy, int* status, double* part, int accumulate,
+                     cudaStream_t st);
+cudaError_t md_kinetic(const double* vel, const double* mass, int64_t n, double* out,
+                       double* part, cudaStream_t st);
 
 // ---------------------------------------------------------------- assemble.cu
 cudaError_t assemble_forces(int64_t n, const int32_t* perm, const double* qs,

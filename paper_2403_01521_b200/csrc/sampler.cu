@@ -16,33 +16,9 @@
 // triangular, lane k is final after k rounds; high acceptance converges fast).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "philox.cuh"
 
 namespace slab {
-
-struct Philox {
-  __device__ static uint4 round(uint4 c, uint2 k) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
-    uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
-    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-  }
-  __device__ static uint4 gen(uint64_t seed, uint64_t ctr) {
-    uint4 c = make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), 0x5AB5u, 0x2403u);
-    uint2 k = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-      c = round(c, k);
-      k.x += 0x9E3779B9u;
-      k.y += 0xBB67AE85u;
-    }
-    return c;
-  }
-};
-
-__device__ __forceinline__ double u01_open(uint32_t a, uint32_t b) {
-  // 53-bit uniform in (0, 1]
-  return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6) + 1.0) * (1.0 / 9007199254740992.0);
-}
 
 // rbse2d.py:96-102, tail-stable form (erfc differences) for |m| >= 1
 __device__ __forceinline__ double axis_logq(long long m, double ax) {

@@ -17,6 +17,7 @@
 // lanes whose candidate happens to be in range).  Each force is accumulated by
 // exactly one thread over the full shell: deterministic, no atomics;
 // u_s = 1/2 of the full-shell sum.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -96,6 +97,47 @@ __device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, dou
   acc.fz = fma(fmag, dz, acc.fz);
 }
 
+// WCA core (ewald2d.py:218-221 with shifted_lj = 1, used by md.py:34-56):
+// 4 eps [(s/r)^12 - (s/r)^6] + eps and its force, for d2 <= rc2 = (2^(1/6) s)^2.
+// Same minimum image, cutoff and coincidence rules as the Coulomb term.
+// (Two explicit forms: a shared body with `use ? d2 : rc2` selects after the
+// unmasked early return was miscompiled -- the selects took the masked arm.)
+template <bool kMasked>
+__device__ __forceinline__ void wca_accumulate(double xi, double yi, double zi, double xj,
+                                               double yj, double zj, double lx, double ly,
+                                               double ilx, double ily, double rc2, double eps,
+                                               double sig2, PairAcc& acc, int& flag) {
+  double dx = __dsub_rn(xi, xj), dy = __dsub_rn(yi, yj);
+  const double dz = __dsub_rn(zi, zj);
+  dx = __dsub_rn(dx, __dmul_rn(lx, rint(__dmul_rn(dx, ilx))));
+  dy = __dsub_rn(dy, __dmul_rn(ly, rint(__dmul_rn(dy, ily))));
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const bool in = d2 <= rc2;
+  const bool coincident = d2 < 1e-24;
+  double inv_d2, e;
+  if constexpr (kMasked) {
+    flag |= (in && coincident) ? 1 : 0;
+    const bool use = in && !coincident;
+    inv_d2 = 1.0 / (use ? d2 : rc2);
+    e = use ? eps : 0.0;
+  } else {
+    if (!in) return;
+    if (coincident) {
+      flag = 1;
+      return;
+    }
+    inv_d2 = 1.0 / d2;
+    e = eps;
+  }
+  const double s2 = sig2 * inv_d2;
+  const double s6 = s2 * s2 * s2;
+  acc.e += 4.0 * e * (s6 * s6 - s6) + e;
+  const double fmag = 24.0 * e * (2.0 * s6 * s6 - s6) * inv_d2;
+  acc.fx = fma(fmag, dx, acc.fx);
+  acc.fy = fma(fmag, dy, acc.fy);
+  acc.fz = fma(fmag, dz, acc.fz);
+}
+
 // ewald2d.py:126-138
 __global__ void cell_index_kernel(const double* __restrict__ pos, int64_t n, double lx, double ly,
                                   double lz, int ncx, int ncy, int ncz, uint32_t* __restrict__ key,
@@ -137,14 +179,6 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
 }
 
 constexpr int kSRThreads = 128;
-#ifndef SLAB_PAIR_MASKED
-#define SLAB_PAIR_MASKED 1
-#endif
-#if SLAB_PAIR_MASKED
-#define PAIR_FN pair_accumulate_masked
-#else
-#define PAIR_FN pair_accumulate
-#endif
 constexpr int kRing = 16;  // staged neighbour indices per thread (two 32-byte sectors)
 
 // Pass 1: neighbour rows.  One thread per home particle in cell order.  Cells
@@ -251,19 +285,31 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
 // flight per iteration (measured: 2 or 8 in flight, a generic unrolled loop, or
 // a min-blocks launch bound are all 5-20% slower).  Each force is owned by one
 // thread: deterministic.
+// KIND 0: erfc Coulomb (alpha); KIND 1: WCA core (eps, sig2 = sigma^2).
+template <int KIND>
 __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     const double4* __restrict__ cp, const int32_t* __restrict__ order,
     const int32_t* __restrict__ nbr, const int32_t* __restrict__ nn, int64_t a_begin,
-    int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2,
-    double* __restrict__ forces, double* __restrict__ eblk, int* __restrict__ status) {
-  __shared__ double etab[kErfcxTabSize];
+    int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2, double eps,
+    double sig2, double* __restrict__ forces, double* __restrict__ eblk,
+    int* __restrict__ status, int accumulate) {
+  __shared__ double etab[KIND == 0 ? kErfcxTabSize : 1];
   __shared__ double red[kSRThreads];
-  load_erfcx_table(etab);
+  if constexpr (KIND == 0) load_erfcx_table(etab);
   __syncthreads();
   const double c = kTwoOverSqrtPi * alpha;
   const double ilx = 1.0 / lx, ily = 1.0 / ly;
   PairAcc acc{0.0, 0.0, 0.0, 0.0};
   int flag = 0;
+#define PAIR(pi, pj)                                                                          \
+  do {                                                                                        \
+    if constexpr (KIND == 0)                                                                  \
+      pair_accumulate_masked(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, \
+                             alpha, rc2, c, etab, acc, flag);                                 \
+    else                                                                                      \
+      wca_accumulate<true>(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, lx, ly, ilx, ily, rc2, eps,    \
+                           sig2, acc, flag);                                                  \
+  } while (0)
   // grid-stride over home particles: the smem erfcx fill is paid once per CTA
   for (int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x; a < a_end;
        a += (int64_t)gridDim.x * kSRThreads) {
@@ -275,25 +321,26 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     for (; k + 4 <= cnt; k += 4) {
       const int4 j4 = *reinterpret_cast<const int4*>(row + k);
       const double4 p0 = cp[j4.x], p1 = cp[j4.y], p2 = cp[j4.z], p3 = cp[j4.w];
-      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p0.x, p0.y, p0.z, p0.w, lx, ly, ilx, ily, alpha,
-                      rc2, c, etab, acc, flag);
-      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p1.x, p1.y, p1.z, p1.w, lx, ly, ilx, ily, alpha,
-                      rc2, c, etab, acc, flag);
-      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p2.x, p2.y, p2.z, p2.w, lx, ly, ilx, ily, alpha,
-                      rc2, c, etab, acc, flag);
-      PAIR_FN(pi.x, pi.y, pi.z, pi.w, p3.x, p3.y, p3.z, p3.w, lx, ly, ilx, ily, alpha,
-                      rc2, c, etab, acc, flag);
+      PAIR(pi, p0);
+      PAIR(pi, p1);
+      PAIR(pi, p2);
+      PAIR(pi, p3);
     }
     for (; k < cnt; ++k) {
       const double4 pj = cp[row[k]];
-      PAIR_FN(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, alpha,
-                      rc2, c, etab, acc, flag);
+      PAIR(pi, pj);
     }
     const int64_t i = order[a];
+    if (accumulate) {  // one thread owns particle i: += is race-free and deterministic
+      acc.fx += forces[3 * i + 0];
+      acc.fy += forces[3 * i + 1];
+      acc.fz += forces[3 * i + 2];
+    }
     forces[3 * i + 0] = acc.fx;
     forces[3 * i + 1] = acc.fy;
     forces[3 * i + 2] = acc.fz;
   }
+#undef PAIR
   if (flag) atomicOr(status, SLAB_STATUS_COINCIDENT_DEV);
   red[threadIdx.x] = acc.e;
   __syncthreads();
@@ -305,12 +352,13 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
 }
 
 // all pairs (ncx < 3 or ncy < 3): grid (i tiles, j splits)
+template <int KIND>
 __global__ void __launch_bounds__(128) brute_pair_kernel(
     const double* __restrict__ pos, const double* __restrict__ q, int64_t n, int64_t i_begin,
-    int64_t i_end, int jsplit, double lx, double ly, double alpha, double rc2,
-    double* __restrict__ fbuf, double* __restrict__ eblk, int* __restrict__ status) {
-  __shared__ double etab[kErfcxTabSize];
-  load_erfcx_table(etab);
+    int64_t i_end, int jsplit, double lx, double ly, double alpha, double rc2, double eps,
+    double sig2, double* __restrict__ fbuf, double* __restrict__ eblk, int* __restrict__ status) {
+  __shared__ double etab[KIND == 0 ? kErfcxTabSize : 1];
+  if constexpr (KIND == 0) load_erfcx_table(etab);
   __syncthreads();
   const int64_t i = i_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int js = blockIdx.y;
@@ -321,11 +369,16 @@ __global__ void __launch_bounds__(128) brute_pair_kernel(
   PairAcc acc{0.0, 0.0, 0.0, 0.0};
   int flag = 0;
   if (i < i_end) {
-    const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2], qi = q[i];
+    const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
+    const double qi = KIND == 0 ? q[i] : 0.0;
     for (int64_t j = j0; j < j1; ++j) {
       if (j == i) continue;
-      pair_accumulate(xi, yi, zi, qi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], q[j], lx, ly,
-                      ilx, ily, alpha, rc2, c, etab, acc, flag);
+      if constexpr (KIND == 0)
+        pair_accumulate(xi, yi, zi, qi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], q[j], lx, ly,
+                        ilx, ily, alpha, rc2, c, etab, acc, flag);
+      else
+        wca_accumulate<false>(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], lx, ly, ilx,
+                              ily, rc2, eps, sig2, acc, flag);
     }
     double* f = fbuf + ((size_t)js * n + i) * 3;
     f[0] = acc.fx;
@@ -344,12 +397,12 @@ __global__ void __launch_bounds__(128) brute_pair_kernel(
 }
 
 __global__ void brute_force_reduce_kernel(const double* __restrict__ fbuf, int jsplit, int64_t n3,
-                                          double* __restrict__ forces) {
+                                          double* __restrict__ forces, int accumulate) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n3) return;
   double v = 0.0;
   for (int s = 0; s < jsplit; ++s) v += fbuf[(size_t)s * n3 + e];
-  forces[e] = v;
+  forces[e] = accumulate ? forces[e] + v : v;
 }
 
 // u_s = 1/2 * sum of the per-block full-shell partials, fixed order
@@ -431,15 +484,18 @@ size_t short_work_bytes(const ShortPlan& p) {
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
                       double* energy_out, int* status, int64_t h0, int64_t h1,
-                      int* maxnn_out, cudaStream_t st) {
+                      int* maxnn_out, cudaStream_t st, int kind, double lj_eps,
+                      double lj_sigma, int accumulate) {
   const int64_t n = p.n;
+  const double sig2 = lj_sigma * lj_sigma;
   if (n < 2 || h1 <= h0) {
     cudaMemsetAsync(energy_out, 0, sizeof(double), st);
-    if (n > 0) cudaMemsetAsync(forces, 0, sizeof(double) * 3 * n, st);
+    if (n > 0 && !accumulate) cudaMemsetAsync(forces, 0, sizeof(double) * 3 * n, st);
     return cudaGetLastError();
   }
   // a shard (multi-GPU) writes only its home particles: clear the rest first
   const bool partial = h0 > 0 || h1 < n;
+  if (partial && accumulate) return cudaErrorInvalidValue;
   if (partial) cudaMemsetAsync(forces, 0, sizeof(double) * 3 * n, st);
   const int64_t nh = h1 - h0;
   char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(work) + 255) & ~(uintptr_t)255);
@@ -450,10 +506,14 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     double* fbuf = reinterpret_cast<double*>(w);
     const unsigned nbx = (unsigned)((nh + 127) / 128);
     if (partial) cudaMemsetAsync(fbuf, 0, sizeof(double) * 3 * n * p.jsplit, st);
-    brute_pair_kernel<<<dim3(nbx, p.jsplit), 128, 0, st>>>(pos, charge, n, h0, h1, p.jsplit, lx, ly,
-                                                           alpha, rc2, fbuf, eblk, status);
-    brute_force_reduce_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(fbuf, p.jsplit,
-                                                                               3 * n, forces);
+    if (kind == 0)
+      brute_pair_kernel<0><<<dim3(nbx, p.jsplit), 128, 0, st>>>(
+          pos, charge, n, h0, h1, p.jsplit, lx, ly, alpha, rc2, 0.0, 0.0, fbuf, eblk, status);
+    else
+      brute_pair_kernel<1><<<dim3(nbx, p.jsplit), 128, 0, st>>>(
+          pos, charge, n, h0, h1, p.jsplit, lx, ly, 0.0, rc2, lj_eps, sig2, fbuf, eblk, status);
+    brute_force_reduce_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(
+        fbuf, p.jsplit, 3 * n, forces, accumulate);
     half_sum_kernel<<<1, 1024, 0, st>>>(eblk, (int64_t)nbx * p.jsplit, energy_out);
     return cudaGetLastError();
   } else {
@@ -503,9 +563,14 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
           cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
     const int64_t pgrid = pair_grid(nblk);
-    pair_list_kernel<<<(unsigned)pgrid, kSRThreads, 0, st>>>(cp, order, nbr, nn, h0, h1, p.kcap,
-                                                             lx, ly, alpha, rc2, forces, eblk,
-                                                             status);
+    if (kind == 0)
+      pair_list_kernel<0><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
+          cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, alpha, rc2, 0.0, 0.0, forces, eblk, status,
+          accumulate);
+    else
+      pair_list_kernel<1><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
+          cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, 0.0, rc2, lj_eps, sig2, forces, eblk,
+          status, accumulate);
     half_sum_kernel<<<1, 1024, 0, st>>>(eblk, pgrid, energy_out);
   }
   return cudaGetLastError();

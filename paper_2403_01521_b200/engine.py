@@ -183,6 +183,43 @@ class Engine:
             _ptr(status), self._stream()), "slab_batch_energies")
         return out, status
 
+    # -- MD step (md.cu) ------------------------------------------------------
+    def wca(self, pos, box, eps, sigma, forces, energy, status):
+        """Enqueue: forces += WCA core forces; energy[0] = WCA energy; status |= bits."""
+        check(self.lib.slab_wca(
+            self.ctx, _ptr(pos), pos.shape[0],
+            SlabBox(box.lx, box.ly, box.lz, box.sigma_top, box.sigma_bot), float(eps),
+            float(sigma), _ptr(forces), _ptr(energy), _ptr(status), self._stream()), "slab_wca")
+
+    def walls(self, pos, lz, eps, sigma, forces, energy, status):
+        check(self.lib.slab_walls(self.ctx, _ptr(pos), pos.shape[0], float(lz), float(eps),
+                                  float(sigma), _ptr(forces), _ptr(energy), _ptr(status),
+                                  self._stream()), "slab_walls")
+
+    def md_langevin(self, pos, vel, forces, mass, dt, gamma, temperature, seed, counter, shift,
+                    box):
+        check(self.lib.slab_md_langevin(
+            _ptr(pos), _ptr(vel), _ptr(forces), _ptr(mass), pos.shape[0], float(dt), float(gamma),
+            float(temperature), ctypes.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), _ptr(counter),
+            _ptr(shift), float(box.lx), float(box.ly), self._stream()), "slab_md_langevin")
+
+    def md_kick(self, vel, forces, mass, h):
+        check(self.lib.slab_md_kick(_ptr(vel), _ptr(forces), _ptr(mass), vel.shape[0], float(h),
+                                    self._stream()), "slab_md_kick")
+
+    def md_drift(self, pos, vel, dt, shift, box):
+        check(self.lib.slab_md_drift(_ptr(pos), _ptr(vel), pos.shape[0], float(dt), _ptr(shift),
+                                     float(box.lx), float(box.ly), self._stream()),
+              "slab_md_drift")
+
+    def md_scale(self, vel, s):
+        check(self.lib.slab_md_scale(_ptr(vel), vel.shape[0], float(s), self._stream()),
+              "slab_md_scale")
+
+    def md_kinetic(self, vel, mass, out):
+        check(self.lib.slab_md_kinetic(self.ctx, _ptr(vel), _ptr(mass), vel.shape[0], _ptr(out),
+                                       self._stream()), "slab_md_kinetic")
+
     def recursive_pair_sum(self, q, theta, z, beta):
         torch = _torch()
         out = torch.empty((q.numel(), 2), dtype=torch.float64, device=self.device)

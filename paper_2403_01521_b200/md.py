@@ -1,0 +1,461 @@
+"""Device-resident MD engine around the evaluator.
+
+Mirrors reference ``pkg/src/slabewald/md.py``: the same options, result record,
+force field (Coulomb solver + WCA core + walls) and integrators, with the
+state (positions, velocities, forces, image shifts, thermostat counter) kept on
+the device between steps:
+
+* ``lj_forces`` (md.py:34-56) -> ``slab_wca`` (short-range pair machinery with
+  the WCA core, cutoff 2^(1/6) sigma);
+* ``wall_forces`` (md.py:59-77) -> ``slab_walls``;
+* ``langevin_step`` (md.py:180-193) -> ``slab_md_langevin`` (kick, drift, exact
+  OU, drift, xy wrap with image-shift accumulation in one kernel); the final
+  kick after the force evaluation -> ``slab_md_kick``;
+* velocity Verlet (md.py:300-305) -> ``slab_md_kick`` / ``slab_md_drift``;
+* Nose-Hoover (md.py:196-224) -> device kinetic-energy reductions and
+  ``slab_md_scale``, the chain variables on the host;
+* ``kinetic_energy`` (md.py:176-177) -> ``slab_md_kinetic``.
+
+Differences, by design: the Langevin noise is a counter-based Philox4x32-10
+stream keyed by the run seed (reproducible per seed, not numpy's Generator
+sequence -- the policy of the mode sampler); the ``ewald2d`` solver (the O(N^2)
+reference Ewald2D) is out of this hot path's scope and raises.
+Host numpy forms of ``langevin_step`` / ``nose_hoover_step`` /
+``maxwell_velocities`` / ``kinetic_energy`` are kept for API compatibility.
+"""
+
+from __future__ import annotations
+
+import csv
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .core import BoxGeometry, EwaldParams, ParticleSystem, choose_alpha, make_ewald_params
+from .ewald2d import check_short_range_cutoff, raise_on_status
+from .rbse2d import ModeSampler, _rb_commonv, charge_term_sum, normalization_H
+from .soe import SOEApprox, build_soe_contour
+from .soewald2d import full_sum_constants
+
+WCA_CUT = 2.0 ** (1.0 / 6.0)
+
+
+def _status_errors(status: int, where: str) -> None:
+    from ._native import SLAB_STATUS_COINCIDENT, SLAB_STATUS_WALL
+    if status & SLAB_STATUS_WALL:
+        raise ValueError("particle at or beyond a wall")
+    if where == "lj" and status & SLAB_STATUS_COINCIDENT:
+        raise ValueError("coincident particles in the repulsive core")
+    raise_on_status(status)
+
+
+def lj_forces(system: ParticleSystem, box: BoxGeometry, eps: float = 1.0, sigma: float = 1.0):
+    """Purely repulsive pair core 4 eps [(s/r)^12 - (s/r)^6] + eps below
+    r = 2^(1/6) s (md.py:34-56), on device.  Returns (energy, forces)."""
+    n = system.n
+    if n < 2 or eps == 0.0:
+        return 0.0, np.zeros((n, 3))
+    from .engine import get_engine, host_result, to_device
+    import torch
+    eng = get_engine()
+    pos = to_device(system.pos)
+    forces = torch.zeros((n, 3), dtype=torch.float64, device=eng.device)
+    energy = torch.zeros(8, dtype=torch.float64, device=eng.device)
+    while True:
+        status = torch.zeros(1, dtype=torch.int32, device=eng.device)
+        forces.zero_()
+        eng.wca(pos, box, eps, sigma, forces, energy, status)
+        st = int(status.cpu().item())
+        if not eng.handle_overflow(st):
+            break
+    _status_errors(st, "lj")
+    e, f = host_result(energy, forces)
+    return float(e[0]), f
+
+
+def wall_forces(system: ParticleSystem, box: BoxGeometry, eps: float = 1.0, sigma: float = 0.5):
+    """The same repulsive form on the distances to z = 0 and z = lz (md.py:59-77)."""
+    n = system.n
+    if n == 0:
+        return 0.0, np.zeros((0, 3))
+    from .engine import get_engine, host_result, to_device
+    import torch
+    eng = get_engine()
+    pos = to_device(system.pos)
+    forces = torch.zeros((n, 3), dtype=torch.float64, device=eng.device)
+    energy = torch.zeros(8, dtype=torch.float64, device=eng.device)
+    status = torch.zeros(1, dtype=torch.int32, device=eng.device)
+    eng.walls(pos, box.lz, eps, sigma, forces, energy, status)
+    _status_errors(int(status.cpu().item()), "walls")
+    e, f = host_result(energy, forces)
+    return float(e[0]), f
+
+
+@dataclass
+class MDOptions:
+    """Knobs for run_simulation; defaults give a stable dilute slab run (md.py:80-101)."""
+
+    dt: float = 0.005
+    n_steps: int = 1000
+    equilibration: int = 0
+    temperature: float = 1.0
+    thermostat: str = "langevin"      # langevin | nose-hoover | none
+    gamma: float = 1.0
+    tau: float = 0.5
+    solver: str = "soewald2d"         # soewald2d | rbse2d  (ewald2d: out of scope)
+    alpha: float | None = None
+    s: float = 4.0
+    soe_size: int = 8
+    batch_size: int = 16
+    lj_eps: float = 1.0
+    lj_sigma: float = 1.0
+    wall_eps: float = 1.0
+    wall_sigma: float = 0.5
+    coulomb: bool = True
+    seed: int = 0
+    sample_every: int = 10
+
+
+@dataclass
+class MDResult:
+    times: np.ndarray
+    positions: np.ndarray             # wrapped, (n_samples, N, 3)
+    unwrapped: np.ndarray             # (n_samples, N, 3), xy never wrapped
+    velocities: np.ndarray
+    potential: np.ndarray
+    kinetic: np.ndarray
+    conserved: np.ndarray             # NVE / NH invariant; nan for Langevin
+    charge: np.ndarray
+    mass: np.ndarray
+    box: BoxGeometry
+    options: MDOptions = field(repr=False)
+
+
+class _ForceField:
+    """Coulomb solver + WCA core + walls, evaluated on device (md.py:117-167).
+
+    ``evaluate_device`` enqueues one evaluation into caller buffers: forces (N,3)
+    and ``ebuf`` (10,) = [evaluate's 8 energy slots, u_lj, u_wall]; status bits
+    are OR-ed into ``status``.  Nothing synchronises."""
+
+    def __init__(self, box: BoxGeometry, charge: np.ndarray, opts: MDOptions, rb_seed: int):
+        self.box = box
+        self.opts = opts
+        self.params: EwaldParams | None = None
+        self.soe: SOEApprox | None = None
+        self.sampler = None
+        self.H = None
+        self.c_q = None
+        self._cv = None
+        self._uq = 0.0
+        if opts.coulomb:
+            if opts.solver not in ("soewald2d", "rbse2d"):
+                if opts.solver == "ewald2d":
+                    raise NotImplementedError(
+                        "the O(N^2) Ewald2D reference solver is outside this device path")
+                raise ValueError(f"unknown solver {opts.solver!r}")
+            alpha = opts.alpha
+            if alpha is None:
+                alpha = choose_alpha(len(charge), box,
+                                     "linear" if opts.solver == "rbse2d" else "balanced",
+                                     prefactor=0.8, s=opts.s)
+            self.params = make_ewald_params(alpha, opts.s, box)
+            check_short_range_cutoff(box, self.params.r_c)
+            self.soe = build_soe_contour(opts.soe_size)
+            Q = float(np.sum(np.asarray(charge) ** 2))
+            if opts.solver == "rbse2d":
+                self.sampler = ModeSampler(alpha, box, seed=rb_seed)
+                self.H = normalization_H(alpha, box)
+                self.c_q = charge_term_sum(alpha, box, Q)
+            else:
+                self._cv, self._uq = full_sum_constants(self.params, box, Q)
+        self._dev = None
+
+    def _device_consts(self, eng):
+        if self._dev is None:
+            from .engine import _SOEPack, to_device
+            d = {}
+            if self.opts.coulomb:
+                d["pack"] = _SOEPack(self.soe)
+                if self.opts.solver == "soewald2d":
+                    km = self.params.kmodes
+                    d["modes"] = to_device(km) if km.shape[0] else None
+                    d["cv"] = to_device(self._cv) if km.shape[0] else 0.0
+            self._dev = d
+        return self._dev
+
+    def evaluate_device(self, eng, pos, q, forces, ebuf, status):
+        import torch
+        opts = self.opts
+        dev = self._device_consts(eng)
+        if opts.coulomb:
+            if opts.solver == "soewald2d":
+                modes, cv, cconst = dev["modes"], dev["cv"], self._uq
+            else:
+                P = opts.batch_size
+                modes = self.sampler.batch_device(P)
+                cv, cconst = _rb_commonv(self.H, P, self.params.alpha), self.c_q
+            eng.evaluate(pos, q, self.box, self.params.alpha, self.params.r_c, self.soe, modes,
+                         cv, cconst, forces=forces, energy=ebuf[:8], soe_pack=dev["pack"])
+            status.bitwise_or_(ebuf[5:6].to(torch.int32))
+        else:
+            forces.zero_()
+            ebuf[:8].zero_()
+        if opts.lj_eps:
+            eng.wca(pos, self.box, opts.lj_eps, opts.lj_sigma, forces, ebuf[8:9], status)
+        else:
+            ebuf[8:9].zero_()
+        eng.walls(pos, self.box.lz, opts.wall_eps, opts.wall_sigma, forces, ebuf[9:10], status)
+
+    @staticmethod
+    def total(e: np.ndarray) -> float:
+        # EnergyBreakdown.total + u_lj + u_wall
+        return float(e[0] + e[1] + e[2] - e[3] + e[4] + e[8] + e[9])
+
+    def evaluate(self, system: ParticleSystem):
+        """Host form of md.py:144-167: (potential energy, forces (N,3))."""
+        from .engine import get_engine, host_result, to_device
+        import torch
+        eng = get_engine()
+        pos, q = to_device(system.pos), to_device(system.charge)
+        n = system.n
+        while True:
+            forces = torch.zeros((n, 3), dtype=torch.float64, device=eng.device)
+            ebuf = torch.zeros(10, dtype=torch.float64, device=eng.device)
+            status = torch.zeros(1, dtype=torch.int32, device=eng.device)
+            self.evaluate_device(eng, pos, q, forces, ebuf, status)
+            e, f = host_result(ebuf, forces)
+            st = int(status.cpu().item())
+            if not eng.handle_overflow(st):
+                break
+        _status_errors(st, "lj")
+        return self.total(e), f
+
+
+def maxwell_velocities(mass: np.ndarray, temperature: float,
+                       rng: np.random.Generator) -> np.ndarray:
+    """md.py:170-174 (host, once per run)."""
+    v = rng.normal(size=(len(mass), 3)) * np.sqrt(temperature / mass)[:, None]
+    v -= np.average(v, axis=0, weights=mass)[None, :]
+    return v
+
+
+def kinetic_energy(mass: np.ndarray, vel: np.ndarray) -> float:
+    return float(0.5 * np.sum(mass * np.sum(vel ** 2, axis=1)))
+
+
+def langevin_step(pos, vel, forces, mass, dt, gamma, temperature, noise):
+    """Host numpy form of md.py:180-193 (the device step is slab_md_langevin)."""
+    inv_m = 1.0 / mass[:, None]
+    vel = vel + 0.5 * dt * forces * inv_m
+    pos = pos + 0.5 * dt * vel
+    c = np.exp(-gamma * dt)
+    vel = c * vel + np.sqrt((1.0 - c * c) * temperature / mass)[:, None] * noise
+    pos = pos + 0.5 * dt * vel
+    return pos, vel
+
+
+def run_simulation(system: ParticleSystem, box: BoxGeometry, opts: MDOptions) -> MDResult:
+    """Integrate and sample (md.py:227-325) with device-resident state: per step
+    only kernel launches; the host reads energies / positions at sample points."""
+    from .engine import get_engine, to_device
+    import torch
+    n = system.n
+    if opts.thermostat not in ("langevin", "nose-hoover", "none"):
+        raise ValueError(f"unknown thermostat {opts.thermostat!r}")
+    eq = opts.equilibration
+    if not 0 <= eq <= opts.n_steps:
+        raise ValueError("equilibration must lie in [0, n_steps]")
+    ss = np.random.SeedSequence(opts.seed)
+    thermo_ss, rb_ss, vel_ss = ss.spawn(3)
+    ff = _ForceField(box, system.charge, opts, rb_seed=int(rb_ss.generate_state(1)[0]))
+    thermo_seed = int(thermo_ss.generate_state(1, dtype=np.uint64)[0])
+    mass_h = np.asarray(system.mass, dtype=np.float64)
+    if system.vel is not None and np.any(system.vel):
+        vel_h = np.array(system.vel, dtype=np.float64)
+    else:
+        vel_h = maxwell_velocities(mass_h, opts.temperature,
+                                   np.random.Generator(np.random.Philox(vel_ss)))
+    eng = get_engine()
+    dev = eng.device
+    pos = to_device(system.pos).clone()
+    vel = to_device(vel_h).clone()
+    q = to_device(system.charge)
+    mass = to_device(mass_h)
+    shift = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+    forces = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    ebuf = torch.zeros(10, dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    counter = torch.zeros(1, dtype=torch.int64, device=dev)
+    kin = torch.zeros(1, dtype=torch.float64, device=dev)
+    dt = opts.dt
+
+    eng.md_drift(pos, vel, 0.0, shift, box)  # initial wrap (md.py:255)
+
+    def evaluate():
+        ff.evaluate_device(eng, pos, q, forces, ebuf, status)
+
+    # first evaluation: settle the neighbour capacity (may rerun once)
+    while True:
+        status.zero_()
+        evaluate()
+        st = int(status.cpu().item())
+        if not eng.handle_overflow(st):
+            break
+    _status_errors(st, "lj")
+
+    n_samples = (opts.n_steps - eq) // opts.sample_every + 1
+    times = np.empty(n_samples)
+    traj = np.empty((n_samples, n, 3))
+    traj_un = np.empty((n_samples, n, 3))
+    vels = np.empty((n_samples, n, 3))
+    pot = np.empty(n_samples)
+    kin_h = np.empty(n_samples)
+    cons = np.full(n_samples, np.nan)
+    xi = 0.0
+    eta = 0.0
+    n_f = 3 * n
+    q_nh = n_f * opts.temperature * opts.tau ** 2
+
+    def kinetic():
+        eng.md_kinetic(vel, mass, kin)
+        return float(kin.cpu().item())
+
+    def record(idx, step):
+        st_ = int(status.cpu().item())
+        if st_:
+            _status_errors(st_, "lj")
+            from ._native import SLAB_STATUS_NBR_OVERFLOW
+            if st_ & SLAB_STATUS_NBR_OVERFLOW:
+                raise RuntimeError("short-range neighbour capacity exceeded during the run")
+        e = ebuf.cpu().numpy()
+        p = pos.cpu().numpy()
+        sh = shift.cpu().numpy()
+        times[idx] = step * dt
+        traj[idx] = p
+        traj_un[idx] = p
+        traj_un[idx, :, 0] += sh[:, 0]
+        traj_un[idx, :, 1] += sh[:, 1]
+        vels[idx] = vel.cpu().numpy()
+        u_now = _ForceField.total(e)
+        pot[idx] = u_now
+        kin_h[idx] = kinetic()
+        if opts.thermostat == "none":
+            cons[idx] = u_now + kin_h[idx]
+        elif opts.thermostat == "nose-hoover":
+            cons[idx] = u_now + kin_h[idx] + 0.5 * q_nh * xi ** 2 + n_f * opts.temperature * eta
+
+    def nh_half():
+        nonlocal xi, eta
+        k2 = 2.0 * kinetic()
+        xi += 0.25 * dt * (k2 - n_f * opts.temperature) / q_nh
+        s = np.exp(-0.5 * dt * xi)
+        eng.md_scale(vel, s)
+        eta += 0.5 * dt * xi
+        k2 = 2.0 * kinetic()
+        xi += 0.25 * dt * (k2 - n_f * opts.temperature) / q_nh
+
+    sample = 0
+    if eq == 0:
+        record(0, 0)
+        sample = 1
+    for step in range(1, opts.n_steps + 1):
+        if opts.thermostat == "langevin":
+            eng.md_langevin(pos, vel, forces, mass, dt, opts.gamma, opts.temperature,
+                            thermo_seed, counter, shift, box)
+            evaluate()
+            eng.md_kick(vel, forces, mass, 0.5 * dt)
+        elif opts.thermostat == "nose-hoover":
+            nh_half()
+            eng.md_kick(vel, forces, mass, 0.5 * dt)
+            eng.md_drift(pos, vel, dt, shift, box)
+            evaluate()
+            eng.md_kick(vel, forces, mass, 0.5 * dt)
+            nh_half()
+        else:
+            eng.md_kick(vel, forces, mass, 0.5 * dt)
+            eng.md_drift(pos, vel, dt, shift, box)
+            evaluate()
+            eng.md_kick(vel, forces, mass, 0.5 * dt)
+        if step >= eq and (step - eq) % opts.sample_every == 0:
+            record(sample, step)
+            sample += 1
+
+    return MDResult(times=times, positions=traj, unwrapped=traj_un, velocities=vels,
+                    potential=pot, kinetic=kin_h, conserved=cons,
+                    charge=np.array(system.charge, dtype=np.float64), mass=mass_h.copy(),
+                    box=box, options=opts)
+
+
+# ---------------------------------------------------------------------------
+# observables and I/O (host, md.py:332-406)
+# ---------------------------------------------------------------------------
+def compute_observables(result: MDResult, n_bins: int = 40, n_blocks: int = 5,
+                        max_lag_frac: float = 0.5, skip_frac: float = 0.2) -> dict:
+    """Mean-square displacements (multiple time origins, xy and z split) and
+    block-averaged z concentration profiles per charge species."""
+    nf = len(result.times)
+    skip = int(skip_frac * nf)
+    un = result.unwrapped[skip:]
+    zs = result.positions[skip:, :, 2]
+    nfu = un.shape[0]
+    if nfu < 4:
+        raise ValueError("trajectory too short for observables")
+    dt_f = result.times[1] - result.times[0] if nf > 1 else 1.0
+    max_lag = max(1, int(max_lag_frac * nfu))
+    lags = np.unique(np.linspace(1, max_lag, min(60, max_lag)).astype(int))
+    msd_xy = np.empty(len(lags))
+    msd_z = np.empty(len(lags))
+    for i, lag in enumerate(lags):
+        d = un[lag:] - un[:-lag]
+        msd_xy[i] = np.mean(np.sum(d[..., :2] ** 2, axis=-1))
+        msd_z[i] = np.mean(d[..., 2] ** 2)
+    box = result.box
+    edges = np.linspace(0.0, box.lz, n_bins + 1)
+    centers = 0.5 * (edges[:-1] + edges[1:])
+    bin_vol = box.area * (edges[1] - edges[0])
+    species = np.unique(result.charge)
+    blocks = np.array_split(np.arange(nfu), n_blocks)
+    conc, conc_std = {}, {}
+    for sp in species:
+        sel = result.charge == sp
+        means = []
+        for blk in blocks:
+            h = np.zeros(n_bins)
+            for f in blk:
+                h += np.histogram(zs[f, sel], bins=edges)[0]
+            means.append(h / (len(blk) * bin_vol))
+        means = np.array(means)
+        conc[float(sp)] = means.mean(axis=0)
+        conc_std[float(sp)] = means.std(axis=0, ddof=1)
+    return {"lag_times": lags * dt_f, "msd_xy": msd_xy, "msd_z": msd_z,
+            "z_bin_centers": centers, "concentration": conc, "concentration_std": conc_std}
+
+
+def write_trajectory_csv(path, result: MDResult) -> None:
+    """Frames in long form: step,id,x,y,z,vx,vy,vz."""
+    steps = np.rint(result.times / result.options.dt).astype(int)
+    with open(path, "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(["step", "id", "x", "y", "z", "vx", "vy", "vz"])
+        for f, step in enumerate(steps):
+            for i in range(result.positions.shape[1]):
+                x, y, z = result.positions[f, i]
+                vx, vy, vz = result.velocities[f, i]
+                wr.writerow([step, i, f"{x:.17g}", f"{y:.17g}", f"{z:.17g}",
+                             f"{vx:.17g}", f"{vy:.17g}", f"{vz:.17g}"])
+
+
+def write_observables_csv(msd_path, conc_path, obs: dict) -> None:
+    with open(msd_path, "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(["t", "msd_xy", "msd_z"])
+        for t, a, b in zip(obs["lag_times"], obs["msd_xy"], obs["msd_z"]):
+            wr.writerow([f"{t:.17g}", f"{a:.17g}", f"{b:.17g}"])
+    species = sorted(obs["concentration"])
+    with open(conc_path, "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(["z_bin_center"] + [f"concentration_q{sp:+g}" for sp in species])
+        for i, zc in enumerate(obs["z_bin_centers"]):
+            wr.writerow([f"{zc:.17g}"] + [f"{obs['concentration'][sp][i]:.17g}"
+                                          for sp in species])

@@ -188,12 +188,69 @@ def golden_units() -> dict:
     return out
 
 
+def md_system(seed=11):
+    """64 charges +-1 on a jittered 4x4x4 lattice in (8, 8, 6), seeded velocities."""
+    rng = np.random.default_rng(seed)
+    g = (np.arange(4) + 0.5)
+    lat = np.stack(np.meshgrid(g * 2.0, g * 2.0, g * 1.5 - 0.0, indexing="ij"), -1).reshape(-1, 3)
+    pos = lat + rng.uniform(-0.25, 0.25, size=lat.shape)
+    charge = np.array([1.0, -1.0] * 32)
+    vel = rng.normal(size=(64, 3)) * 0.7
+    return charge, np.ones(64), pos, vel
+
+
+def golden_md() -> dict:
+    """md.py: WCA core (brute and cell paths), walls, and short deterministic
+    trajectories (thermostat none / nose-hoover: no random numbers)."""
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    from slabewald import md
+    out = {}
+    rng = np.random.default_rng(5)
+    # WCA, brute path (reference: ncx == 1 when L < 2 cut)
+    box_b = core.BoxGeometry(2.0, 2.0, 3.0)
+    pos_b = rng.uniform([0, 0, 0.3], [2.0, 2.0, 2.7], size=(10, 3))
+    sb = core.make_system(np.ones(10), np.ones(10), pos_b, box=box_b)
+    out["wca_b_pos"] = sb.pos
+    out["wca_b_u"], out["wca_b_f"] = md.lj_forces(sb, box_b, 1.0, 1.0)
+    # WCA, cell path
+    box_c = core.BoxGeometry(12.0, 12.0, 6.0)
+    pos_c = rng.uniform([0, 0, 0.2], [12.0, 12.0, 5.8], size=(300, 3))
+    sc = core.make_system(np.ones(300), np.ones(300), pos_c, box=box_c)
+    out["wca_c_pos"] = sc.pos
+    out["wca_c_u"], out["wca_c_f"] = md.lj_forces(sc, box_c, 1.3, 0.9)
+    # walls
+    zw = np.concatenate([rng.uniform(0.05, 0.6, 20), rng.uniform(5.4, 5.95, 20),
+                         rng.uniform(1.0, 5.0, 20)])
+    pos_w = np.column_stack([rng.uniform(0, 12, 60), rng.uniform(0, 12, 60), zw])
+    sw = core.make_system(np.ones(60), np.ones(60), pos_w, box=box_c)
+    out["walls_pos"] = sw.pos
+    out["walls_u"], out["walls_f"] = md.wall_forces(sw, box_c, 1.0, 0.5)
+    # deterministic trajectories
+    charge, mass, pos, vel = md_system()
+    box = core.BoxGeometry(8.0, 8.0, 6.0)
+    out["traj_pos0"], out["traj_vel0"] = pos, vel
+    for thermo in ("none", "nose-hoover"):
+        sysm = core.ParticleSystem(charge=charge, mass=mass, pos=pos.copy(), vel=vel.copy())
+        opts = md.MDOptions(dt=0.002, n_steps=20, thermostat=thermo, solver="soewald2d",
+                            alpha=1.0, s=3.0, soe_size=8, sample_every=5, seed=3)
+        res = md.run_simulation(sysm, box, opts)
+        key = thermo.replace("-", "")
+        out[f"traj_{key}_pos"] = res.positions
+        out[f"traj_{key}_unwrapped"] = res.unwrapped
+        out[f"traj_{key}_vel"] = res.velocities
+        out[f"traj_{key}_pot"] = res.potential
+        out[f"traj_{key}_kin"] = res.kinetic
+        out[f"traj_{key}_cons"] = res.conserved
+    return out
+
+
 def main(argv):
     names = argv or ["units", "cfg1", "cfg2", "small_600", "small_2000", "cfg5_1e4",
                      "cfg3", "cfg5_1e5", "cfg4", "cfg5_1e6"]
     for name in names:
         t0 = time.perf_counter()
-        data = golden_units() if name == "units" else golden_workload(name)
+        data = (golden_units() if name == "units" else
+                golden_md() if name == "md" else golden_workload(name))
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in data.items()})
         print(f"{name}: wrote {path} ({os.path.getsize(path)/1e3:.0f} kB) "

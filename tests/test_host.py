@@ -142,3 +142,42 @@ def test_workload_generators_are_neutral_and_regenerate():
         assert wl.system.pos[:, 2].min() >= 0 and wl.system.pos[:, 2].max() <= wl.box.lz
         wl2 = make_workload(name)
         np.testing.assert_array_equal(wl.system.pos, wl2.system.pos)
+
+
+def test_particle_csv_round_trip_and_errors(tmp_path):
+    """core.py:305-329 particle CSV: exact round trip, rows read back by id,
+    header checked, box wrap applied on load."""
+    import paper_2403_01521_b200 as pk
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, 5, size=(7, 3))
+    s = pk.make_system(rng.choice([-1.0, 1.0], 7), rng.uniform(1, 2, 7), pos,
+                       rng.normal(size=(7, 3)))
+    p = tmp_path / "p.csv"
+    pk.save_particles(p, s)
+    t = pk.load_particles(p)
+    for a, b in ((t.pos, s.pos), (t.vel, s.vel), (t.charge, s.charge), (t.mass, s.mass)):
+        np.testing.assert_array_equal(a, b)
+    lines = p.read_text().splitlines()
+    shuffled = tmp_path / "q.csv"
+    shuffled.write_text("\n".join([lines[0]] + lines[1:][::-1]) + "\n")
+    np.testing.assert_array_equal(pk.load_particles(shuffled).pos, s.pos)
+    wrapped = pk.load_particles(p, box=pk.BoxGeometry(2.0, 2.0, 5.0))
+    assert np.all(wrapped.pos[:, :2] < 2.0)
+    bad = tmp_path / "bad.csv"
+    bad.write_text("id,q,m,x,y,z\n0,1,1,0,0,0\n")
+    with pytest.raises(ValueError, match="header"):
+        pk.load_particles(bad)
+
+
+def test_md_host_pieces_without_gpu():
+    """md.py host forms: options defaults, the numpy Langevin step, observables."""
+    from paper_2403_01521_b200 import md
+    o = md.MDOptions()
+    assert (o.dt, o.thermostat, o.solver, o.soe_size, o.batch_size) == \
+        (0.005, "langevin", "soewald2d", 8, 16)
+    pos = np.zeros((2, 3))
+    vel = np.ones((2, 3))
+    p2, v2 = md.langevin_step(pos, vel, np.zeros((2, 3)), np.ones(2), 0.1, 0.0, 1.0,
+                              np.zeros((2, 3)))
+    np.testing.assert_allclose(p2, 0.1 * vel)
+    np.testing.assert_allclose(v2, vel)
