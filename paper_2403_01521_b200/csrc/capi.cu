@@ -389,7 +389,7 @@ int slab_wca(SlabCtx* ctx, const double* d_pos, int64_t n, SlabBox box, double e
   if (n > INT32_MAX) return fail(SLAB_ERR_ARG, "n exceeds int32 indexing");
   cudaStream_t st = (cudaStream_t)stream;
   const double cut = 1.122462048309373 * sigma;  // WCA_CUT = 2^(1/6), md.py:31
-  auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, cut);
+  auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, cut, 1);
   if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;
   int rc = ensure_arena(ctx, slab::short_work_bytes(sp) + 1024);
   if (rc) return rc;

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(1024) half_sum_kernel(const double* __restrict
 // pair_list_kernel grid: one resident wave (5 CTAs per SM at 90 registers), grid-striding
 static int64_t pair_grid(int64_t blocks) { return blocks < 148 * 5 ? blocks : 148 * 5; }
 
-ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc) {
+ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int max_span) {
   ShortPlan p{};
   p.n = n;
   int ncx = (int)(lx / rc), ncy = (int)(ly / rc), ncz = (int)(lz / rc);
@@ -437,7 +437,7 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc) {
   } else {
     // half-edge cells (edge >= r_c/2, search span 2): ncx, ncy >= 6 >= 2*2+1 here
     const char* env = getenv("SLAB_SHORT_SPAN");  // tuning knob: 1 = cells of edge >= r_c
-    if (!(env && env[0] == '1')) {
+    if (max_span >= 2 && !(env && env[0] == '1')) {
       p.span = 2;
       ncx = (int)(2.0 * lx / rc);
       ncy = (int)(2.0 * ly / rc);
