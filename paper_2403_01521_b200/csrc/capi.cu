@@ -464,6 +464,17 @@ int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_the
   return SLAB_OK;
 }
 
+// short-range home-particle boundary of rank r of W (sharding.py home_range): the
+// lead rank (which also runs the k = 0 mode) takes 10 - round(1.15 W) tenths of a
+// regular share
+static int64_t home_bound(int64_t n, int r, int W) {
+  if (W <= 1 || r >= W) return r <= 0 ? 0 : n;
+  if (r <= 0) return 0;
+  int64_t lead = 10 - (23 * (int64_t)W + 10) / 20;
+  lead = lead < 0 ? 0 : lead;
+  return n * (lead + 10 * (int64_t)(r - 1)) / (lead + 10 * (int64_t)(W - 1));
+}
+
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (!ctx || !a) return fail(SLAB_ERR_ARG, "null context or arguments");
   const int64_t n = a->n;
@@ -512,7 +523,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (srank < 0 || srank >= scount) return fail(SLAB_ERR_ARG, "shard_rank out of range");
   const bool lead = srank == 0;  // the rank that owns the k = 0 mode and the constants
   if (!a->skip_short_range) {
-    const int64_t h0 = n * srank / scount, h1 = n * (srank + 1) / scount;
+    const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
     CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
                        a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, st));
   }

@@ -47,6 +47,8 @@ constexpr int kSB = SLAB_SWEEP_SB;
 constexpr int kSweepMaxThreads = SLAB_SWEEP_MAXT;  // force staging batch (particles)
 constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
 constexpr int kMaxR = 256;
+constexpr size_t kSmemPerSM = 227 * 1024;  // usable shared memory per SM (B200)
+constexpr int kAggRegs = 72;               // fourier_aggregate_mma_kernel (ptxas)
 
 __host__ __device__ inline int ncomp_of(int mh) { return 2 * mh + 1; }
 
@@ -179,6 +181,7 @@ static size_t agg_mma_smem(int R, int mh) {
 #ifndef SLAB_AGG_MMA_MAXW
 #define SLAB_AGG_MMA_MAXW 13  // m-tiles (warps) per CTA: P <= 104 in one CTA per chunk
 #endif
+constexpr int kAggMaxWarps = SLAB_AGG_MMA_MAXW;
 #ifndef SLAB_AGG_MMA_CB
 #define SLAB_AGG_MMA_CB 1  // constant-bank polynomial coefficients in the main loop
 #endif
@@ -309,17 +312,15 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, 2) fourier_aggregate_m
 // phase 2: carry scan over chunks (in place: aggregates -> carried-in states)
 // ---------------------------------------------------------------------------
 // Lanes are 32 consecutive items of one component (contiguous in the carry
-// array, so every load / store is a 512-byte coalesced row) and each warp of a
-// CTA owns one contiguous segment of chunks.  Pass 1 composes the segment's
-// affine maps T -> D T + X, the segments are composed across warps through
-// shared memory, pass 2 rewrites the segment with the exclusive carries.
-#ifndef SLAB_CARRY_SEGS
-#define SLAB_CARRY_SEGS 32
-#endif
-#ifndef SLAB_CARRY_BATCH
-#define SLAB_CARRY_BATCH 4
-#endif
-constexpr int kCarrySegs = SLAB_CARRY_SEGS;  // warps per CTA
+// array: every load / store is a 512-byte coalesced row); the chunk axis is cut
+// into T = G * kCarrySegs segments, one warp each (grid.z = G).  Three kernels:
+//   A  compose each segment's affine maps T -> D T + X          (segment maps)
+//   M  exclusive scan of the T segment maps per (item, comp)     (carried-in X)
+//   B  rewrite each segment's chunks with the exclusive carries
+// G is chosen per plan so that few-item plans (a multi-GPU rank's mode slice)
+// still expose thousands of warps.
+constexpr int kCarrySegs = 32;  // warps per CTA
+constexpr int kCarryBatch = 4;  // loads in flight per thread
 
 __device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, int l, int mh,
                                           double k, const double2* __restrict__ Df,
@@ -343,76 +344,141 @@ __device__ __forceinline__ AffC acompose(const AffC& a, const AffC& b) {
   return AffC{cmul(b.D, a.D), C2{x.re + b.X.re, x.im + b.X.im}};
 }
 
-__global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_kernel(
-    double2* __restrict__ carry, int nch, int P, int items, int mh,
-    const double* __restrict__ modetab, const double2* __restrict__ Df,
-    const double2* __restrict__ Db, const double* __restrict__ zbound) {
-  __shared__ AffC segm[kCarrySegs][32];
-  const int nitems = 2 * P, nc = ncomp_of(mh);
+struct CarryLane {
+  int item, comp, l, t, s0, s1;
+  bool valid, fwd, isg;
+  double k;
+};
+
+__device__ __forceinline__ CarryLane carry_lane(int nch, int P, int items, int mh, int nseg,
+                                                const double* __restrict__ modetab) {
+  CarryLane c;
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
-  const int comp = blockIdx.y;
+  c.comp = blockIdx.y;
   const int item_raw = blockIdx.x * 32 + lane;
-  const bool valid = item_raw < items;
-  const int item = valid ? item_raw : items - 1;
-  const bool fwd = item < P;
-  const int t = fwd ? item : item - P;
-  const bool isg = comp == 2 * mh;
-  const int l = comp < mh ? comp : comp - mh;
-  const double k = modetab[(size_t)t * mode_stride(mh) + 2];
+  c.valid = item_raw < items;
+  c.item = c.valid ? item_raw : items - 1;
+  c.fwd = c.item < P;
+  c.t = c.fwd ? c.item : c.item - P;
+  c.isg = c.comp == 2 * mh;
+  c.l = c.comp < mh ? c.comp : c.comp - mh;
+  c.k = modetab[(size_t)c.t * mode_stride(mh) + 2];
+  const int sg = blockIdx.z * kCarrySegs + seg;
+  const int per = (nch + nseg - 1) / nseg;
+  c.s0 = min(nch, sg * per);
+  c.s1 = min(nch, c.s0 + per);
+  return c;
+}
+
+__global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_compose_kernel(
+    const double2* __restrict__ carry, int nch, int P, int items, int mh, int nseg,
+    const double* __restrict__ modetab, const double2* __restrict__ Df,
+    const double2* __restrict__ Db, const double* __restrict__ zbound, AffC* __restrict__ segmap) {
+  const CarryLane c = carry_lane(nch, P, items, mh, nseg, modetab);
+  const int nitems = 2 * P, nc = ncomp_of(mh);
   const size_t cstride = (size_t)nc * nitems;
-  double2* base = carry + (size_t)comp * nitems + item;
-  const int per = (nch + kCarrySegs - 1) / kCarrySegs;
-  const int s0 = seg * per, s1 = min(nch, s0 + per);
-  constexpr int B = SLAB_CARRY_BATCH;
-  // pass 1: compose this segment (loads batched ahead of the dependent chain)
+  const double2* base = carry + (size_t)c.comp * nitems + c.item;
   AffC M{C2{1.0, 0.0}, C2{0.0, 0.0}};
-  for (int sb = s0; sb < s1; sb += B) {
-    double2 xs[B];
-    C2 ds[B];
+  for (int sb = c.s0; sb < c.s1; sb += kCarryBatch) {
+    double2 xs[kCarryBatch];
+    C2 ds[kCarryBatch];
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
+    for (int j = 0; j < kCarryBatch; ++j) {
       const int s = sb + j;
-      if (s < s1) {
-        const int c = fwd ? s : nch - 1 - s;
-        xs[j] = base[(size_t)c * cstride];
-        ds[j] = carry_decay(isg, fwd, c, nch, l, mh, k, Df, Db, zbound);
+      if (s < c.s1) {
+        const int ch = c.fwd ? s : nch - 1 - s;
+        xs[j] = base[(size_t)ch * cstride];
+        ds[j] = carry_decay(c.isg, c.fwd, ch, nch, c.l, mh, c.k, Df, Db, zbound);
       }
     }
 #pragma unroll
-    for (int j = 0; j < B; ++j)
-      if (sb + j < s1) M = acompose(M, AffC{ds[j], C2{xs[j].x, xs[j].y}});
+    for (int j = 0; j < kCarryBatch; ++j)
+      if (sb + j < c.s1) M = acompose(M, AffC{ds[j], C2{xs[j].x, xs[j].y}});
   }
-  segm[seg][lane] = M;
-  __syncthreads();
-  // carried state entering this segment: earlier segments applied in order (T0 = 0)
-  AffC pre{C2{1.0, 0.0}, C2{0.0, 0.0}};
-  for (int w = 0; w < seg; ++w) pre = acompose(pre, segm[w][lane]);
-  C2 T = pre.X;
-  if (!valid) return;
-  // pass 2: rewrite the segment with exclusive carries
-  for (int sb = s0; sb < s1; sb += B) {
-    double2 xs[B];
-    C2 ds[B];
+  if (c.valid) {
+    const int sg = blockIdx.z * kCarrySegs + (threadIdx.x >> 5);
+    segmap[((size_t)sg * nc + c.comp) * items + c.item] = M;
+  }
+}
+
+// one warp per (item, comp) chain: segmap[s].X <- exclusive prefix X (T0 = 0).
+// Lane j composes a contiguous run of segments, a shuffle scan composes the
+// lanes, then each lane rewrites its run.
+__global__ void __launch_bounds__(128) fourier_carry_segscan_kernel(AffC* __restrict__ segmap,
+                                                                   int items, int nc, int nseg) {
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // chain
+  const int lane = threadIdx.x & 31;
+  if (e >= items * nc) return;
+  const size_t stride = (size_t)nc * items;
+  AffC* m = segmap + e;
+  const int per = (nseg + 31) / 32;
+  const int s0 = min(nseg, lane * per), s1 = min(nseg, s0 + per);
+  AffC M{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  for (int s = s0; s < s1; ++s) M = acompose(M, m[(size_t)s * stride]);
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
+  for (int o = 1; o < 32; o <<= 1) {
+    AffC u;
+    u.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, o), __shfl_up_sync(0xffffffffu, M.D.im, o)};
+    u.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, o), __shfl_up_sync(0xffffffffu, M.X.im, o)};
+    if (lane >= o) M = acompose(u, M);
+  }
+  AffC pre;
+  pre.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, 1), __shfl_up_sync(0xffffffffu, M.D.im, 1)};
+  pre.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, 1), __shfl_up_sync(0xffffffffu, M.X.im, 1)};
+  if (lane == 0) pre = AffC{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  for (int s = s0; s < s1; ++s) {
+    AffC* ms = m + (size_t)s * stride;
+    const AffC cur = *ms;
+    ms->X = pre.X;
+    pre = acompose(pre, cur);
+  }
+}
+
+__global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_rewrite_kernel(
+    double2* __restrict__ carry, int nch, int P, int items, int mh, int nseg,
+    const double* __restrict__ modetab, const double2* __restrict__ Df,
+    const double2* __restrict__ Db, const double* __restrict__ zbound,
+    const AffC* __restrict__ segmap) {
+  const CarryLane c = carry_lane(nch, P, items, mh, nseg, modetab);
+  if (!c.valid) return;
+  const int nitems = 2 * P, nc = ncomp_of(mh);
+  const size_t cstride = (size_t)nc * nitems;
+  double2* base = carry + (size_t)c.comp * nitems + c.item;
+  const int sg = blockIdx.z * kCarrySegs + (threadIdx.x >> 5);
+  C2 T = segmap[((size_t)sg * nc + c.comp) * items + c.item].X;
+  for (int sb = c.s0; sb < c.s1; sb += kCarryBatch) {
+    double2 xs[kCarryBatch];
+    C2 ds[kCarryBatch];
+#pragma unroll
+    for (int j = 0; j < kCarryBatch; ++j) {
       const int s = sb + j;
-      if (s < s1) {
-        const int c = fwd ? s : nch - 1 - s;
-        xs[j] = base[(size_t)c * cstride];
-        ds[j] = carry_decay(isg, fwd, c, nch, l, mh, k, Df, Db, zbound);
+      if (s < c.s1) {
+        const int ch = c.fwd ? s : nch - 1 - s;
+        xs[j] = base[(size_t)ch * cstride];
+        ds[j] = carry_decay(c.isg, c.fwd, ch, nch, c.l, mh, c.k, Df, Db, zbound);
       }
     }
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
+    for (int j = 0; j < kCarryBatch; ++j) {
       const int s = sb + j;
-      if (s < s1) {
-        const int c = fwd ? s : nch - 1 - s;
-        base[(size_t)c * cstride] = make_double2(T.re, T.im);
+      if (s < c.s1) {
+        const int ch = c.fwd ? s : nch - 1 - s;
+        base[(size_t)ch * cstride] = make_double2(T.re, T.im);
         const C2 nt = cmul(ds[j], T);
         T = C2{nt.re + xs[j].x, nt.im + xs[j].y};
       }
     }
   }
+}
+
+// segment groups: enough CTAs to fill the GPU, at least ~16 chunks per segment
+static int carry_groups(int nch, int items, int mh) {
+  if (items <= 0) return 1;
+  const int ctas = ((items + 31) / 32) * ncomp_of(mh);
+  int g = (2 * 148 + ctas - 1) / ctas;
+  const int gmax = nch / (kCarrySegs * 16);
+  if (g > gmax) g = gmax;
+  return g < 1 ? 1 : g;
 }
 
 // ---------------------------------------------------------------------------
@@ -697,12 +763,32 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs) {
   p.ngroups = (nitems + kSweepMaxThreads - 1) / kSweepMaxThreads;
   if (p.ngroups < 1) p.ngroups = 1;
   p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
+  if (p.ipg < 1) p.ipg = 1;
   p.warps = (p.ipg + 31) / 32;
   if (p.warps < 1) p.warps = 1;
   const int64_t target_ctas = 4 * 148;
   int64_t rf = n * p.ngroups / target_ctas;
   int R = 16;
   while (R * 2 <= rf && R * 2 <= kMaxR) R *= 2;
+  // Few items per chunk (a multi-GPU rank's mode slice, small P) means small
+  // CTAs whose shared memory -- dominated by the R-particle decay and weight
+  // tables -- would cap the SM at a handful of warps: shrink R until both the
+  // sweep and the aggregate reach their register-limited occupancy.
+  {
+    const int tiles = P > 0 ? (P + 7) / 8 : 1;
+    const int ngy = (tiles + kAggMaxWarps - 1) / kAggMaxWarps;
+    const int tpc = (tiles + ngy - 1) / ngy;
+    auto ctas = [](size_t smem, int threads, int regs) {
+      const int by_smem = (int)(kSmemPerSM / (smem + 1024));
+      const int by_regs = 65536 / (regs * threads);
+      return by_smem < by_regs ? (by_smem < 32 ? by_smem : 32) : (by_regs < 32 ? by_regs : 32);
+    };
+    const int sw_full = 65536 / (128 * 32 * p.warps);
+    const int ag_full = 65536 / (kAggRegs * 32 * tpc);
+    while (R > 16 && (ctas(sweep_smem(R, mh, p.warps), 32 * p.warps, 128) < sw_full ||
+                      ctas(agg_mma_smem(R, mh), 32 * tpc, kAggRegs) < ag_full))
+      R /= 2;
+  }
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
   p.smem_sweep = sweep_smem(R, mh, p.warps);
@@ -722,6 +808,7 @@ size_t fourier_work_doubles(const FourierPlan& p) {
   d += 2 * (size_t)p.nch;                            // zbound
   d += (size_t)p.nch * p.P + p.P;                    // epart + per-mode sums
   d += (size_t)(p.nbuf + 1) * p.n * 3;               // fpart
+  d += 4 * (size_t)carry_groups(p.nch, p.items, p.mh) * 32 * ncomp_of(p.mh) * p.items;  // segmap
   return d + 64;
 }
 
@@ -740,6 +827,9 @@ void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w) {
   w.epart = q;
   q += (size_t)p.nch * p.P + p.P;
   w.fpart = q;
+  q += (size_t)(p.nbuf + 1) * p.n * 3;
+  q += (reinterpret_cast<uintptr_t>(q) / 8) & 1;
+  w.segmap = q;
 }
 
 cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, double2* dtab,
@@ -770,16 +860,25 @@ static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const doub
   dim3 grid(p.nch, p.ngroups);
   if (p.nch > 1) {
     const int tiles = (p.P + 7) / 8;
-    const int ngy = (tiles + SLAB_AGG_MMA_MAXW - 1) / SLAB_AGG_MMA_MAXW;
+    const int ngy = (tiles + kAggMaxWarps - 1) / kAggMaxWarps;
     const int tpc = (tiles + ngy - 1) / ngy;
     fourier_aggregate_mma_kernel<MH><<<dim3(p.nch, ngy), tpc * 32, agg_mma_smem(p.R, MH), st>>>(
         xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry);
   } else
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
   if (p.nch > 1) {
-    fourier_carry_kernel<<<dim3((p.items + 31) / 32, ncomp_of(MH)), 32 * kCarrySegs, 0, st>>>(
-        w.carry, p.nch, p.P, p.items, MH, w.modetab, w.dchunk, w.dchunk + (size_t)p.nch * MH,
-        w.zbound);
+    const int G = carry_groups(p.nch, p.items, MH), nseg = G * kCarrySegs;
+    const dim3 cg((p.items + 31) / 32, ncomp_of(MH), G);
+    const double2* Df = w.dchunk;
+    const double2* Db = w.dchunk + (size_t)p.nch * MH;
+    AffC* segmap = reinterpret_cast<AffC*>(w.segmap);
+    fourier_carry_compose_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
+        w.carry, p.nch, p.P, p.items, MH, nseg, w.modetab, Df, Db, w.zbound, segmap);
+    const int nchain = p.items * ncomp_of(MH);
+    fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(segmap, p.items,
+                                                                  ncomp_of(MH), nseg);
+    fourier_carry_rewrite_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
+        w.carry, p.nch, p.P, p.items, MH, nseg, w.modetab, Df, Db, w.zbound, segmap);
   }
   fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
       xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,

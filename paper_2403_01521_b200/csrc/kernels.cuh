@@ -64,6 +64,7 @@ struct FourierWork {
   double* zbound;    // 2 * nch        (z_end, z_start)
   double* epart;     // nch * P
   double* fpart;     // nbuf * n * 3
+  double* segmap;    // carry-scan segment maps (4 doubles each)
 };
 size_t fourier_work_doubles(const FourierPlan& p);
 void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w);

@@ -7,10 +7,10 @@
 // stable scatter, gives the same permutation bit for bit.  -0.0 is folded onto
 // +0.0 (the reference compares with '>' so they tie and keep input order).
 //
-// Per pass: histogram (per tile, smem atomics) -> one-block exclusive scan over
-// [digit][tile] -> stable scatter (warp match_any ranks + per-warp digit
-// prefix, 16 rounds of 256 keys per 4096-key tile).  8 passes for 64-bit keys,
-// ceil(bits/8) for the 32-bit cell-id keys of the short-range cell list.
+// All passes' digit counts in one read, then one Onesweep kernel per pass
+// (decoupled look-back for the tile offsets, stable scatter with warp
+// match_any ranks, 16 rounds of 256 keys per 4096-key tile).  8 passes for
+// 64-bit keys, ceil(bits/8) for the 32-bit cell-id keys of the cell list.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -33,106 +33,120 @@ __global__ void zkey_init_kernel(const double* __restrict__ z, int64_t stride, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Onesweep-style LSD radix sort: one kernel per digit pass.
+//   radix_digit_counts: all passes' global digit counts in one read of the keys
+//                       (digit totals do not depend on the key order);
+//   radix_digit_bases:  exclusive scans -> global base of every digit, per pass;
+//   radix_onesweep:     per 4096-key tile (tiles taken in launch order from an
+//                       atomic counter, so waiting only ever targets a running
+//                       tile): count the tile's digits, publish them, look back
+//                       over earlier tiles' published counts (decoupled
+//                       look-back) for the tile's exclusive offsets, then the
+//                       stable scatter (warp match_any ranks, 16 rounds).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kLbAgg = 1u << 30;   // look-back word: tile aggregate published
+constexpr uint32_t kLbInc = 2u << 30;   // inclusive prefix published
+constexpr uint32_t kLbVal = (1u << 30) - 1u;
+constexpr int kMaxPasses = 8;
+
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const K* __restrict__ keys,
-                                                                  int64_t n, int shift,
-                                                                  int32_t* __restrict__ hist,
-                                                                  int ntiles) {
-  __shared__ int32_t cnt[256];
-  cnt[threadIdx.x] = 0;
+__global__ void __launch_bounds__(kSortThreads) radix_digit_counts_kernel(
+    const K* __restrict__ keys, int64_t n, int passes, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t cnt[kMaxPasses][256];
+  for (int e = threadIdx.x; e < kMaxPasses * 256; e += blockDim.x) (&cnt[0][0])[e] = 0;
   __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * kSortTile;
-#pragma unroll 4
-  for (int r = 0; r < kSortItems; ++r) {
-    int64_t p = base + r * kSortThreads + threadIdx.x;
-    if (p < n) atomicAdd(&cnt[(unsigned)(keys[p] >> shift) & 255u], 1);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const K k = keys[p];
+    for (int ps = 0; ps < passes; ++ps) atomicAdd(&cnt[ps][(unsigned)(k >> (8 * ps)) & 255u], 1u);
   }
   __syncthreads();
-  hist[threadIdx.x * (int64_t)ntiles + blockIdx.x] = cnt[threadIdx.x];
+  for (int e = threadIdx.x; e < passes * 256; e += blockDim.x) {
+    const uint32_t v = (&cnt[0][0])[e];
+    if (v) atomicAdd(&counts[e], v);
+  }
 }
 
-// Row-wise exclusive scan of hist[256][ntiles] (one block per digit row); the
-// row total lands in rowtot[digit].
-__global__ void __launch_bounds__(1024) scan_rows_kernel(int32_t* __restrict__ hist, int ntiles,
-                                                         int32_t* __restrict__ rowtot) {
-  __shared__ int32_t wsum[32];
-  __shared__ int32_t carry;
-  int32_t* row = hist + (int64_t)blockIdx.x * ntiles;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
+// one block per pass: bases[ps][d] = sum_{d' < d} counts[ps][d']
+__global__ void __launch_bounds__(256) radix_digit_bases_kernel(const uint32_t* __restrict__ counts,
+                                                                uint32_t* __restrict__ bases) {
+  __shared__ uint32_t s[256];
+  const int ps = blockIdx.x, d = threadIdx.x;
+  s[d] = counts[ps * 256 + d];
   __syncthreads();
-  for (int base = 0; base < ntiles; base += 1024) {
-    int i = base + threadIdx.x;
-    int32_t v = i < ntiles ? row[i] : 0;
-    int32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
+  for (int o = 1; o < 256; o <<= 1) {
+    const uint32_t y = d >= o ? s[d - o] : 0u;
     __syncthreads();
-    if (warp == 0) {
-      int32_t s = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int32_t y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
-      }
-      wsum[lane] = s;
-    }
-    __syncthreads();
-    if (i < ntiles) row[i] = carry + (warp ? wsum[warp - 1] : 0) + x - v;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += wsum[31];
+    s[d] += y;
     __syncthreads();
   }
-  if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
-}
-
-// offsets[d][t] += sum_{d' < d} rowtot[d']
-__global__ void __launch_bounds__(256) add_digit_base_kernel(int32_t* __restrict__ hist, int ntiles,
-                                                             const int32_t* __restrict__ rowtot) {
-  __shared__ int32_t pre[256];
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int d = 0; d < 256; ++d) { pre[d] = run; run += rowtot[d]; }
-  }
-  __syncthreads();
-  int64_t total = (int64_t)256 * ntiles;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x)
-    hist[i] += pre[i / ntiles];
+  bases[ps * 256 + d] = s[d] - counts[ps * 256 + d];
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+__global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(
     const K* __restrict__ kin, const int32_t* __restrict__ vin, K* __restrict__ kout,
-    int32_t* __restrict__ vout, int64_t n, int shift, const int32_t* __restrict__ offsets,
-    int ntiles) {
+    int32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ bases,
+    uint32_t* __restrict__ look, int* __restrict__ tile_ctr) {
   __shared__ int32_t base[256];
   __shared__ int32_t wcnt[kSortThreads / 32][256];
+  __shared__ uint32_t tcnt[256];
+  __shared__ int tile_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  base[tid] = offsets[tid * (int64_t)ntiles + blockIdx.x];
+  if (tid == 0) tile_s = atomicAdd(tile_ctr, 1);
+  tcnt[tid] = 0u;
+  __syncthreads();
+  const int tile = tile_s;
+  const int64_t tile0 = (int64_t)tile * kSortTile;
+  K keys[kSortItems];
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    const int64_t p = tile0 + r * kSortThreads + tid;
+    keys[r] = p < n ? kin[p] : K(0);
+    if (p < n) atomicAdd(&tcnt[(unsigned)(keys[r] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  // decoupled look-back for digit `tid`
+  {
+    const uint32_t own = tcnt[tid];
+    volatile uint32_t* lk = look;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      lk[tid] = kLbInc | own;
+    } else {
+      lk[(size_t)tile * 256 + tid] = kLbAgg | own;
+      for (int t = tile - 1; t >= 0; --t) {
+        uint32_t v;
+        do {
+          v = lk[(size_t)t * 256 + tid];
+        } while ((v & ~kLbVal) == 0u);
+        excl += v & kLbVal;
+        if (v & kLbInc) break;
+      }
+      lk[(size_t)tile * 256 + tid] = kLbInc | (excl + own);
+    }
+    base[tid] = (int32_t)(bases[tid] + excl);
+  }
   const unsigned lt_mask = (1u << lane) - 1u;
-  int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
 #pragma unroll
     for (int w = 0; w < kSortThreads / 32; ++w) wcnt[w][tid] = 0;
     __syncthreads();
-    int64_t p = tile0 + r * kSortThreads + tid;
-    bool valid = p < n;
-    K key = valid ? kin[p] : K(0);
-    unsigned digit = valid ? (unsigned)(key >> shift) & 255u : 256u;
-    unsigned peers = __match_any_sync(0xffffffffu, digit);
-    int rank = __popc(peers & lt_mask);
+    const int64_t p = tile0 + r * kSortThreads + tid;
+    const bool valid = p < n;
+    const K key = keys[r];
+    const unsigned digit = valid ? (unsigned)(key >> shift) & 255u : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, digit);
+    const int rank = __popc(peers & lt_mask);
     if (valid && rank == 0) wcnt[warp][digit] = __popc(peers);
     __syncthreads();
     {  // digit tid: exclusive prefix over warps, advance the tile-running base
       int32_t run = base[tid];
 #pragma unroll
       for (int w = 0; w < kSortThreads / 32; ++w) {
-        int32_t c = wcnt[w][tid];
+        const int32_t c = wcnt[w][tid];
         wcnt[w][tid] = run;
         run += c;
       }
@@ -140,11 +154,11 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     }
     __syncthreads();
     if (valid) {
-      int32_t dst = wcnt[warp][digit] + rank;
+      const int32_t dst = wcnt[warp][digit] + rank;
       kout[dst] = key;
       vout[dst] = vin[p];
     }
-    __syncthreads();
+    __syncthreads();  // wcnt is reset by the next round
   }
 }
 
@@ -176,16 +190,27 @@ cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_
                              int32_t* hist, int64_t n, int key_bits, cudaStream_t st,
                              K** keys_out, int32_t** vals_out) {
   const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+  const int passes = (key_bits + 7) / 8;
   K *ki = keys, *ko = keys_alt;
   int32_t *vi = vals, *vo = vals_alt;
   if (n > 0) {
-    for (int shift = 0; shift < key_bits; shift += 8) {
-      radix_hist_kernel<K><<<ntiles, kSortThreads, 0, st>>>(ki, n, shift, hist, ntiles);
-      scan_rows_kernel<<<256, 1024, 0, st>>>(hist, ntiles, hist + (int64_t)256 * ntiles);
-      add_digit_base_kernel<<<(unsigned)((256 * (int64_t)ntiles + 255) / 256 < 1184 ? (256 * (int64_t)ntiles + 255) / 256 : 1184), 256, 0, st>>>(
-          hist, ntiles, hist + (int64_t)256 * ntiles);
-      radix_scatter_kernel<K><<<ntiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist,
-                                                               ntiles);
+    // workspace: counts [passes][256] | bases [passes][256] | tile counters [passes]
+    //            | look-back words [passes][ntiles][256]
+    uint32_t* counts = reinterpret_cast<uint32_t*>(hist);
+    uint32_t* bases = counts + kMaxPasses * 256;
+    int* tctr = reinterpret_cast<int*>(bases + kMaxPasses * 256);
+    uint32_t* look = reinterpret_cast<uint32_t*>(tctr + 64);
+    const size_t clear = sizeof(uint32_t) * ((size_t)kMaxPasses * 256 * 2 + 64 +
+                                            (size_t)passes * ntiles * 256);
+    cudaMemsetAsync(hist, 0, clear, st);
+    int grid = (int)((n + kSortThreads - 1) / kSortThreads);
+    grid = grid < 4 * 148 ? grid : 4 * 148;
+    radix_digit_counts_kernel<K><<<grid, kSortThreads, 0, st>>>(ki, n, passes, counts);
+    radix_digit_bases_kernel<<<passes, 256, 0, st>>>(counts, bases);
+    for (int ps = 0; ps < passes; ++ps) {
+      radix_onesweep_kernel<K><<<ntiles, kSortThreads, 0, st>>>(
+          ki, vi, ko, vo, n, 8 * ps, bases + ps * 256, look + (size_t)ps * ntiles * 256,
+          tctr + ps);
       K* tk = ki; ki = ko; ko = tk;
       int32_t* tv = vi; vi = vo; vo = tv;
     }
@@ -196,8 +221,8 @@ cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_
 }
 
 int64_t radix_hist_entries(int64_t n) {
-  int64_t ntiles = (n + kSortTile - 1) / kSortTile;
-  return 256 * (ntiles > 0 ? ntiles : 1) + 256;  // + row totals
+  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  return (int64_t)kMaxPasses * 256 * 2 + 64 + (int64_t)kMaxPasses * (ntiles > 0 ? ntiles : 1) * 256;
 }
 
 cudaError_t sort_by_z_device(const double* z, int64_t stride, int64_t n, SortWork& w,

@@ -14,12 +14,50 @@ gives the single-GPU result up to summation order.
 from __future__ import annotations
 
 
+# Modes are split evenly: a rank's sweep cost is quantised by whole warps of
+# items, so trimming the lead rank's modes buys little (LEAD_MODE_DISCOUNT = 0);
+# the lead's extra k = 0 mode work is balanced on the short range instead.
+LEAD_MODE_DISCOUNT = 0
+
+
 def mode_slice(P: int, rank: int, world: int) -> tuple[int, int]:
-    return P * rank // world, P * (rank + 1) // world
+    """Contiguous mode range of rank r: equal shares of P + d "mode units", the
+    lead rank's share reduced by d (its k = 0 mode work)."""
+    if world <= 1:
+        return 0, P
+    d = min(LEAD_MODE_DISCOUNT, P // world)
+
+    def bound(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return P
+        return min(P, max(0, (P + d) * r // world - d))
+    return bound(rank), bound(rank + 1)
+
+
+# The lead rank takes a reduced share of the short-range home particles: it also
+# runs the k = 0 mode and the assembly constants (~0.4 ms at cfg4, against a
+# short-range share of ~3.5 ms / W).  Lead share in tenths of a regular share:
+# 10 - round(1.15 W) (8, 5, 1 tenths at W = 2, 4, 8); slab_evaluate uses the same
+# integer formula (capi.cu home_bound).
+def lead_home_tenths(world: int) -> int:
+    return max(0, 10 - (23 * world + 10) // 20)
 
 
 def home_range(n: int, rank: int, world: int) -> tuple[int, int]:
-    return n * rank // world, n * (rank + 1) // world
+    if world <= 1:
+        return 0, n
+    lead = lead_home_tenths(world)
+    units = lead + 10 * (world - 1)
+
+    def bound(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return n
+        return n * (lead + 10 * (r - 1)) // units
+    return bound(rank), bound(rank + 1)
 
 
 def is_lead(rank: int) -> bool:
