@@ -189,7 +189,7 @@ template <int MH>
 __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, 2) fourier_aggregate_mma_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
-    int tiles_per_cta, BVec b, double2* __restrict__ carry) {
+    int tiles_per_cta, BVec b, double2* __restrict__ carry, int c0) {
   constexpr int MHP = mma_mhp(MH);  // pairs padded to whole n-tiles of 4 pairs
   constexpr int NT = MHP / 2;       // n-tiles: 2 directions x MHP/4
   constexpr int NCOL = 8 * NT;      // (dir, l, re/im) columns
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, 2) fourier_aggregate_m
   double* sy = sx + R;
   double* sz = sy + R;
   double* sq = sz + R;
-  const int c = blockIdx.x;
+  const int c = c0 + blockIdx.x;
   const int64_t a0 = (int64_t)c * R;
   const int len = (int)(a0 + R < n ? R : n - a0);
   const double z_end = zs[a0 + len - 1], z_start = zs[a0];
@@ -344,14 +344,18 @@ __device__ __forceinline__ AffC acompose(const AffC& a, const AffC& b) {
   return AffC{cmul(b.D, a.D), C2{x.re + b.X.re, x.im + b.X.im}};
 }
 
+// chunk ranges: this plan scans chunks [c0, c1) of the nch global chunks (a
+// z-split multi-GPU rank owns a contiguous range); segment position s maps to
+// chunk c0 + s (forward items) or c1 - 1 - s (backward items)
 struct CarryLane {
-  int item, comp, l, t, s0, s1;
+  int item, comp, l, t, s0, s1, c0, c1;
   bool valid, fwd, isg;
   double k;
+  __device__ __forceinline__ int chunk(int s) const { return fwd ? c0 + s : c1 - 1 - s; }
 };
 
-__device__ __forceinline__ CarryLane carry_lane(int nch, int P, int items, int mh, int nseg,
-                                                const double* __restrict__ modetab) {
+__device__ __forceinline__ CarryLane carry_lane(int c0, int c1, int P, int items, int mh,
+                                                int nseg, const double* __restrict__ modetab) {
   CarryLane c;
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
   c.comp = blockIdx.y;
@@ -364,17 +368,20 @@ __device__ __forceinline__ CarryLane carry_lane(int nch, int P, int items, int m
   c.l = c.comp < mh ? c.comp : c.comp - mh;
   c.k = modetab[(size_t)c.t * mode_stride(mh) + 2];
   const int sg = blockIdx.z * kCarrySegs + seg;
-  const int per = (nch + nseg - 1) / nseg;
-  c.s0 = min(nch, sg * per);
-  c.s1 = min(nch, c.s0 + per);
+  const int len = c1 - c0;
+  const int per = (len + nseg - 1) / nseg;
+  c.s0 = min(len, sg * per);
+  c.s1 = min(len, c.s0 + per);
+  c.c0 = c0;
+  c.c1 = c1;
   return c;
 }
 
 __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_compose_kernel(
-    const double2* __restrict__ carry, int nch, int P, int items, int mh, int nseg,
-    const double* __restrict__ modetab, const double2* __restrict__ Df,
+    const double2* __restrict__ carry, int nch, int c0, int c1, int P, int items, int mh,
+    int nseg, const double* __restrict__ modetab, const double2* __restrict__ Df,
     const double2* __restrict__ Db, const double* __restrict__ zbound, AffC* __restrict__ segmap) {
-  const CarryLane c = carry_lane(nch, P, items, mh, nseg, modetab);
+  const CarryLane c = carry_lane(c0, c1, P, items, mh, nseg, modetab);
   const int nitems = 2 * P, nc = ncomp_of(mh);
   const size_t cstride = (size_t)nc * nitems;
   const double2* base = carry + (size_t)c.comp * nitems + c.item;
@@ -386,7 +393,7 @@ __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_compose_kernel(
     for (int j = 0; j < kCarryBatch; ++j) {
       const int s = sb + j;
       if (s < c.s1) {
-        const int ch = c.fwd ? s : nch - 1 - s;
+        const int ch = c.chunk(s);
         xs[j] = base[(size_t)ch * cstride];
         ds[j] = carry_decay(c.isg, c.fwd, ch, nch, c.l, mh, c.k, Df, Db, zbound);
       }
@@ -404,8 +411,11 @@ __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_compose_kernel(
 // one warp per (item, comp) chain: segmap[s].X <- exclusive prefix X (T0 = 0).
 // Lane j composes a contiguous run of segments, a shuffle scan composes the
 // lanes, then each lane rewrites its run.
-__global__ void __launch_bounds__(128) fourier_carry_segscan_kernel(AffC* __restrict__ segmap,
-                                                                   int items, int nc, int nseg) {
+// mode 0: exclusive prefixes with carried-in state tin[chain] (NULL = 0);
+// mode 1: only the range's total map -> total[chain] (z-split phase 1).
+__global__ void __launch_bounds__(128) fourier_carry_segscan_kernel(
+    AffC* __restrict__ segmap, int items, int nc, int nseg, const double2* __restrict__ tin,
+    AffC* __restrict__ total, int mode) {
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // chain
   const int lane = threadIdx.x & 31;
   if (e >= items * nc) return;
@@ -422,10 +432,19 @@ __global__ void __launch_bounds__(128) fourier_carry_segscan_kernel(AffC* __rest
     u.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, o), __shfl_up_sync(0xffffffffu, M.X.im, o)};
     if (lane >= o) M = acompose(u, M);
   }
+  if (mode == 1) {  // lane 31 holds the inclusive composition of every segment
+    if (lane == 31) total[e] = M;
+    return;
+  }
   AffC pre;
   pre.D = C2{__shfl_up_sync(0xffffffffu, M.D.re, 1), __shfl_up_sync(0xffffffffu, M.D.im, 1)};
   pre.X = C2{__shfl_up_sync(0xffffffffu, M.X.re, 1), __shfl_up_sync(0xffffffffu, M.X.im, 1)};
   if (lane == 0) pre = AffC{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  if (tin) {  // state entering the range: X <- D T_in + X
+    const double2 t2 = tin[e];
+    const C2 dx = cmul(pre.D, C2{t2.x, t2.y});
+    pre.X = C2{dx.re + pre.X.re, dx.im + pre.X.im};
+  }
   for (int s = s0; s < s1; ++s) {
     AffC* ms = m + (size_t)s * stride;
     const AffC cur = *ms;
@@ -435,11 +454,11 @@ __global__ void __launch_bounds__(128) fourier_carry_segscan_kernel(AffC* __rest
 }
 
 __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_rewrite_kernel(
-    double2* __restrict__ carry, int nch, int P, int items, int mh, int nseg,
+    double2* __restrict__ carry, int nch, int c0, int c1, int P, int items, int mh, int nseg,
     const double* __restrict__ modetab, const double2* __restrict__ Df,
     const double2* __restrict__ Db, const double* __restrict__ zbound,
     const AffC* __restrict__ segmap) {
-  const CarryLane c = carry_lane(nch, P, items, mh, nseg, modetab);
+  const CarryLane c = carry_lane(c0, c1, P, items, mh, nseg, modetab);
   if (!c.valid) return;
   const int nitems = 2 * P, nc = ncomp_of(mh);
   const size_t cstride = (size_t)nc * nitems;
@@ -453,7 +472,7 @@ __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_rewrite_kernel(
     for (int j = 0; j < kCarryBatch; ++j) {
       const int s = sb + j;
       if (s < c.s1) {
-        const int ch = c.fwd ? s : nch - 1 - s;
+        const int ch = c.chunk(s);
         xs[j] = base[(size_t)ch * cstride];
         ds[j] = carry_decay(c.isg, c.fwd, ch, nch, c.l, mh, c.k, Df, Db, zbound);
       }
@@ -462,13 +481,31 @@ __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_rewrite_kernel(
     for (int j = 0; j < kCarryBatch; ++j) {
       const int s = sb + j;
       if (s < c.s1) {
-        const int ch = c.fwd ? s : nch - 1 - s;
+        const int ch = c.chunk(s);
         base[(size_t)ch * cstride] = make_double2(T.re, T.im);
         const C2 nt = cmul(ds[j], T);
         T = C2{nt.re + xs[j].x, nt.im + xs[j].y};
       }
     }
   }
+}
+
+// z-split phase 2: state entering rank r's chunk range, per (comp, item) chain,
+// from every rank's total map (gathered [W][nc][items]): forward items compose
+// ranks 0 .. r-1, backward items ranks W-1 .. r+1 (their chunk order runs down).
+__global__ void fourier_zsplit_tin_kernel(const AffC* __restrict__ totals, int W, int r,
+                                          int items, int nc, int P, double2* __restrict__ tin) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= items * nc) return;
+  const int item = e % items;
+  const bool fwd = item < P;
+  AffC pre{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  if (fwd) {
+    for (int q = 0; q < r; ++q) pre = acompose(pre, totals[(size_t)q * nc * items + e]);
+  } else {
+    for (int q = W - 1; q > r; --q) pre = acompose(pre, totals[(size_t)q * nc * items + e]);
+  }
+  tin[e] = make_double2(pre.X.re, pre.X.im);
 }
 
 // segment groups: enough CTAs to fill the GPU, at least ~16 chunks per segment
@@ -501,7 +538,7 @@ __global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
     const double* __restrict__ modetab, int P, int items, int ipg, BVec b,
     const double2* __restrict__ carry, double* __restrict__ epart, double* __restrict__ fpart,
-    int want_forces) {
+    int want_forces, int c0) {
   extern __shared__ double4 smem4[];
   const int nwarps = blockDim.x >> 5;
   double2* sC = reinterpret_cast<double2*>(smem4);         // [MH][blockDim]
@@ -512,7 +549,7 @@ __global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
   double* sz = sq + R;                                     // R + 2 (halo below / above)
   double* stage = sz + R + 2;                              // nwarps * kSB*3 * 33
 
-  const int c = blockIdx.x, g = blockIdx.y;
+  const int c = c0 + blockIdx.x, g = blockIdx.y;
   const int64_t a0 = (int64_t)c * R;
   const int len = (int)(a0 + R < n ? R : n - a0);
   const int64_t a1 = a0 + len;
@@ -689,12 +726,12 @@ __global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
 // per-mode sums over chunks (one block per mode, fixed-order tree), then Kahan
 // over modes in mode order exactly like soewald2d.py:204-207
 __global__ void __launch_bounds__(256) fourier_mode_energy_kernel(
-    const double* __restrict__ epart, int nch, int P, int mh, const double* __restrict__ modetab,
-    double* __restrict__ se) {
+    const double* __restrict__ epart, int c0, int c1, int P, int mh,
+    const double* __restrict__ modetab, double* __restrict__ se) {
   __shared__ double red[256];
   const int t = blockIdx.x;
   double s = 0.0;
-  for (int c = threadIdx.x; c < nch; c += 256) s += epart[(size_t)c * P + t];
+  for (int c = c0 + threadIdx.x; c < c1; c += 256) s += epart[(size_t)c * P + t];
   red[threadIdx.x] = s;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
@@ -726,9 +763,10 @@ __global__ void kahan_modes_kernel(const double* __restrict__ se, int nseg, int 
 // ngroups * nwarps (when nbuf exceeds the grid) is the mixed warp's backward one.
 __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int nbuf,
                                             int ngroups, int nwarps, int ipg, int nitems,
-                                            int64_t n3, double* __restrict__ out) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= n3) return;
+                                            int64_t n3, double* __restrict__ out, int64_t e0,
+                                            int64_t e1) {
+  int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= e1) return;
   double v = 0.0;
   for (int b = 0; b < nbuf; ++b) {
     if (b < ngroups * nwarps) {
@@ -791,6 +829,8 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs) {
   }
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
+  p.c0 = 0;
+  p.c1 = p.nch;
   p.smem_sweep = sweep_smem(R, mh, p.warps);
   // one partial force buffer per (group, warp) + one for the backward lanes of
   // the (at most one) warp that holds both directions
@@ -809,6 +849,7 @@ size_t fourier_work_doubles(const FourierPlan& p) {
   d += (size_t)p.nch * p.P + p.P;                    // epart + per-mode sums
   d += (size_t)(p.nbuf + 1) * p.n * 3;               // fpart
   d += 4 * (size_t)carry_groups(p.nch, p.items, p.mh) * 32 * ncomp_of(p.mh) * p.items;  // segmap
+  d += 8 * (size_t)ncomp_of(p.mh) * p.items;  // z-split carried-in states (double2) + spare
   return d + 64;
 }
 
@@ -830,6 +871,8 @@ void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w) {
   q += (size_t)(p.nbuf + 1) * p.n * 3;
   q += (reinterpret_cast<uintptr_t>(q) / 8) & 1;
   w.segmap = q;
+  q += 4 * (size_t)carry_groups(p.nch, p.items, p.mh) * 32 * ncomp_of(p.mh) * p.items;
+  w.tin = q;
 }
 
 cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, double2* dtab,
@@ -840,49 +883,147 @@ cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, doub
 }
 
 template <int MH>
-static cudaError_t run_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
-                          const double* ys, const double* zs, const double* qs,
-                          const double2* dtab, const BVec& b, int want_forces,
-                          cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    // largest shared-memory carveout so two CTAs of each fit per SM
-    cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sweep_smem(kMaxR, MH, 8));
-    cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         100);
-    cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)agg_mma_smem(kMaxR, MH));
-    cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr_done = true;
-  }
-  dim3 grid(p.nch, p.ngroups);
+static void set_attrs() {
+  static bool done = false;
+  if (done) return;
+  // largest shared-memory carveout so two CTAs of each fit per SM
+  cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sweep_smem(kMaxR, MH, 8));
+  cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       100);
+  cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)agg_mma_smem(kMaxR, MH));
+  cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  done = true;
+}
+
+static dim3 carry_grid(const FourierPlan& p) {
+  return dim3((p.items + 31) / 32, ncomp_of(p.mh), carry_groups(p.c1 - p.c0, p.items, p.mh));
+}
+
+// phase 1: aggregates of chunks [c0, c1) and their segment maps; with `totals`,
+// also the range's total map per (comp, item) chain (z-split exchange payload)
+template <int MH>
+static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
+                             const double* ys, const double* zs, const double* qs,
+                             const BVec& b, double* totals, cudaStream_t st) {
+  set_attrs<MH>();
+  const int nch_r = p.c1 - p.c0;
+  if (nch_r <= 0) return cudaGetLastError();
   if (p.nch > 1) {
     const int tiles = (p.P + 7) / 8;
     const int ngy = (tiles + kAggMaxWarps - 1) / kAggMaxWarps;
     const int tpc = (tiles + ngy - 1) / ngy;
-    fourier_aggregate_mma_kernel<MH><<<dim3(p.nch, ngy), tpc * 32, agg_mma_smem(p.R, MH), st>>>(
-        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry);
-  } else
-    cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
-  if (p.nch > 1) {
-    const int G = carry_groups(p.nch, p.items, MH), nseg = G * kCarrySegs;
-    const dim3 cg((p.items + 31) / 32, ncomp_of(MH), G);
-    const double2* Df = w.dchunk;
-    const double2* Db = w.dchunk + (size_t)p.nch * MH;
-    AffC* segmap = reinterpret_cast<AffC*>(w.segmap);
+    fourier_aggregate_mma_kernel<MH><<<dim3(nch_r, ngy), tpc * 32, agg_mma_smem(p.R, MH), st>>>(
+        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry, p.c0);
+    const dim3 cg = carry_grid(p);
+    const int nseg = cg.z * kCarrySegs;
     fourier_carry_compose_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
-        w.carry, p.nch, p.P, p.items, MH, nseg, w.modetab, Df, Db, w.zbound, segmap);
-    const int nchain = p.items * ncomp_of(MH);
-    fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(segmap, p.items,
-                                                                  ncomp_of(MH), nseg);
-    fourier_carry_rewrite_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
-        w.carry, p.nch, p.P, p.items, MH, nseg, w.modetab, Df, Db, w.zbound, segmap);
+        w.carry, p.nch, p.c0, p.c1, p.P, p.items, MH, nseg, w.modetab, w.dchunk,
+        w.dchunk + (size_t)p.nch * MH, w.zbound, reinterpret_cast<AffC*>(w.segmap));
+    if (totals) {
+      const int nchain = p.items * ncomp_of(MH);
+      fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(
+          reinterpret_cast<AffC*>(w.segmap), p.items, ncomp_of(MH), nseg, nullptr,
+          reinterpret_cast<AffC*>(totals), 1);
+    }
+  } else {
+    cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
+    if (totals) {  // one chunk: its total map is (1, 0) -- never combined (W = 1)
+      cudaMemsetAsync(totals, 0, sizeof(AffC) * ncomp_of(MH) * (size_t)p.items, st);
+    }
   }
-  fourier_sweep_kernel<MH><<<grid, p.warps * 32, p.smem_sweep, st>>>(
+  return cudaGetLastError();
+}
+
+// phase 2: carried-in states (optionally entering the range with tin), the sweep
+template <int MH>
+static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
+                             const double* ys, const double* zs, const double* qs,
+                             const double2* dtab, const BVec& b, int want_forces,
+                             const double2* tin, cudaStream_t st) {
+  const int nch_r = p.c1 - p.c0;
+  if (nch_r <= 0) return cudaGetLastError();
+  if (p.nch > 1) {
+    const dim3 cg = carry_grid(p);
+    const int nseg = cg.z * kCarrySegs;
+    const int nchain = p.items * ncomp_of(MH);
+    AffC* segmap = reinterpret_cast<AffC*>(w.segmap);
+    fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(segmap, p.items, ncomp_of(MH),
+                                                                  nseg, tin, nullptr, 0);
+    fourier_carry_rewrite_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
+        w.carry, p.nch, p.c0, p.c1, p.P, p.items, MH, nseg, w.modetab, w.dchunk,
+        w.dchunk + (size_t)p.nch * MH, w.zbound, segmap);
+  }
+  fourier_sweep_kernel<MH><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
       xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
-      w.fpart, want_forces);
+      w.fpart, want_forces, p.c0);
+  return cudaGetLastError();
+}
+
+cudaError_t fourier_phase1(const FourierPlan& p, const FourierWork& w, const double* xs,
+                           const double* ys, const double* zs, const double* qs,
+                           const double* modes, const double* commonv, double commonv_scalar,
+                           double area, const BVec& b, const WVec& wv, int* status,
+                           double* totals, cudaStream_t st) {
+  if (p.P <= 0 || p.n < 2) return cudaSuccess;
+  mode_table_kernel<<<(p.P + 127) / 128, 128, 0, st>>>(modes, commonv, commonv_scalar, p.P, p.mh,
+                                                       area, b, wv, w.modetab, status);
+  const int nb = p.nch * p.mh;
+  chunk_bounds_kernel<<<(nb + 127) / 128, 128, 0, st>>>(zs, p.n, p.R, p.nch, p.mh, b, w.zbound,
+                                                        w.dchunk, w.dchunk + (size_t)p.nch * p.mh);
+  switch (p.mh) {
+#define FCASE(K) \
+  case K: return phase1_mh<K>(p, w, xs, ys, zs, qs, b, totals, st);
+    FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
+    FCASE(12)
+#undef FCASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t fourier_zsplit_tin(const FourierPlan& p, const double* totals, int W, int r,
+                               double* tin, cudaStream_t st) {
+  if (p.P <= 0 || p.n < 2) return cudaSuccess;
+  const int nchain = p.items * ncomp_of(p.mh);
+  fourier_zsplit_tin_kernel<<<(nchain + 127) / 128, 128, 0, st>>>(
+      reinterpret_cast<const AffC*>(totals), W, r, p.items, ncomp_of(p.mh), p.P,
+      reinterpret_cast<double2*>(tin));
+  return cudaGetLastError();
+}
+
+cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const double* xs,
+                           const double* ys, const double* zs, const double* qs,
+                           const double2* dtab, const BVec& b, int want_forces,
+                           double* energy_out, double* forces_sorted, const double* tin,
+                           cudaStream_t st, int seg_len) {
+  if (p.P <= 0 || p.n < 2) return cudaSuccess;
+  if (seg_len <= 0 || p.P % seg_len != 0) seg_len = p.P;
+  const double2* tin2 = reinterpret_cast<const double2*>(tin);
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (p.mh) {
+#define FCASE(K) \
+  case K: e = phase2_mh<K>(p, w, xs, ys, zs, qs, dtab, b, want_forces, tin2, st); break;
+    FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
+    FCASE(12)
+#undef FCASE
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  double* se = w.epart + (size_t)p.nch * p.P;  // P scratch doubles after the partials
+  fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.c0, p.c1, p.P, p.mh, w.modetab, se);
+  const int nseg = p.P / seg_len;
+  kahan_modes_kernel<<<(nseg + 127) / 128, 128, 0, st>>>(se, nseg, seg_len, energy_out);
+  if (want_forces) {
+    const int64_t n3 = p.n * 3;
+    const int64_t e0 = (int64_t)p.c0 * p.R * 3;
+    int64_t e1 = (int64_t)p.c1 * p.R * 3;
+    e1 = e1 < n3 ? e1 : n3;
+    if (e1 > e0)
+      fourier_force_reduce_kernel<<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
+          w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
+  }
   return cudaGetLastError();
 }
 
@@ -892,33 +1033,11 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
                         double commonv_scalar, double area, const BVec& b, const WVec& wv,
                         int want_forces, double* energy_out, int* status, double* forces_sorted,
                         cudaStream_t st, int seg_len) {
-  if (p.P <= 0 || p.n < 2) return cudaSuccess;
-  if (seg_len <= 0 || p.P % seg_len != 0) seg_len = p.P;
-  mode_table_kernel<<<(p.P + 127) / 128, 128, 0, st>>>(modes, commonv, commonv_scalar, p.P, p.mh,
-                                                       area, b, wv, w.modetab, status);
-  const int nb = p.nch * p.mh;
-  chunk_bounds_kernel<<<(nb + 127) / 128, 128, 0, st>>>(zs, p.n, p.R, p.nch, p.mh, b, w.zbound,
-                                                        w.dchunk, w.dchunk + (size_t)p.nch * p.mh);
-  cudaError_t e = cudaErrorInvalidValue;
-  switch (p.mh) {
-#define FCASE(K) \
-  case K: e = run_mh<K>(p, w, xs, ys, zs, qs, dtab, b, want_forces, st); break;
-    FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
-    FCASE(12)
-#undef FCASE
-    default: return cudaErrorInvalidValue;
-  }
+  cudaError_t e = fourier_phase1(p, w, xs, ys, zs, qs, modes, commonv, commonv_scalar, area, b,
+                                 wv, status, nullptr, st);
   if (e != cudaSuccess) return e;
-  double* se = w.epart + (size_t)p.nch * p.P;  // P scratch doubles after the partials
-  fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.nch, p.P, p.mh, w.modetab, se);
-  const int nseg = p.P / seg_len;
-  kahan_modes_kernel<<<(nseg + 127) / 128, 128, 0, st>>>(se, nseg, seg_len, energy_out);
-  if (want_forces) {
-    const int64_t n3 = p.n * 3;
-    fourier_force_reduce_kernel<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(
-        w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted);
-  }
-  return cudaGetLastError();
+  return fourier_phase2(p, w, xs, ys, zs, qs, dtab, b, want_forces, energy_out, forces_sorted,
+                        nullptr, st, seg_len);
 }
 
 }  // namespace slab

@@ -53,6 +53,7 @@ struct FourierPlan {
   int warps;      // warps per CTA
   int nbuf;       // partial force buffers (per group x warp, + 1 if a warp mixes directions)
   int items;      // active (mode, direction) items: 2P, or P for energy-only (forward)
+  int c0, c1;     // chunk range this plan scans (z-split multi-GPU rank), default [0, nch)
   size_t smem_sweep;
 };
 FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2);
@@ -65,6 +66,7 @@ struct FourierWork {
   double* epart;     // nch * P
   double* fpart;     // nbuf * n * 3
   double* segmap;    // carry-scan segment maps (4 doubles each)
+  double* tin;       // z-split: state entering the chunk range, per (comp, item) (double2)
 };
 size_t fourier_work_doubles(const FourierPlan& p);
 void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w);
@@ -76,6 +78,22 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
                         double commonv_scalar, double area, const BVec& b, const WVec& wv,
                         int want_forces, double* energy_out, int* status, double* forces_sorted,
                         cudaStream_t st, int seg_len = 0);  // seg_len > 0: energy per segment
+// the same as two phases around a z-split exchange: phase 1 builds the chunk
+// range's aggregates (and, with `totals`, its total map per (comp, item):
+// 4 doubles each, the all-gather payload); fourier_zsplit_tin composes the
+// gathered totals of the other ranks into `tin`; phase 2 finishes from `tin`
+cudaError_t fourier_phase1(const FourierPlan& p, const FourierWork& w, const double* xs,
+                           const double* ys, const double* zs, const double* qs,
+                           const double* modes, const double* commonv, double commonv_scalar,
+                           double area, const BVec& b, const WVec& wv, int* status,
+                           double* totals, cudaStream_t st);
+cudaError_t fourier_zsplit_tin(const FourierPlan& p, const double* totals, int W, int r,
+                               double* tin, cudaStream_t st);
+cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const double* xs,
+                           const double* ys, const double* zs, const double* qs,
+                           const double2* dtab, const BVec& b, int want_forces,
+                           double* energy_out, double* forces_sorted, const double* tin,
+                           cudaStream_t st, int seg_len = 0);
 
 // ---------------------------------------------------------------- zero.cu
 struct ZeroPlan {
