@@ -106,7 +106,22 @@ typedef struct SlabEvalArgs {
    * kernels (Fourier 3-phase scan + k = 0 mode) for roofline timing */
   void* ev_scan_begin;
   void* ev_scan_end;
+  /* multi-GPU decomposition (shard_count > 1):
+   *   SLAB_SHARD_MODES  (0): rank r evaluates its slice of d_modes (one call);
+   *   SLAB_SHARD_ZSPLIT (1): rank r scans ALL modes over its contiguous range of
+   *     the z-sorted particles (chunks nch*r/W .. nch*(r+1)/W), in two calls
+   *     around an all-gather (SURVEY 8(e) alternative):
+   *       phase 1 writes this rank's chunk-range total maps to d_xchg
+   *         (slab_zsplit_exchange_doubles() doubles);
+   *       the caller all-gathers them into d_xchg[W][...] (rank order);
+   *       phase 2 (same arguments, d_xchg = gathered) finishes the evaluation.
+   *   phase 0 = the whole evaluation in one call (shard_mode MODES, or W = 1). */
+  int shard_mode;
+  int phase;
+  double* d_xchg;
 } SlabEvalArgs;
+
+enum { SLAB_SHARD_MODES = 0, SLAB_SHARD_ZSPLIT = 1 };
 
 typedef struct SlabCtx SlabCtx;
 
@@ -158,6 +173,10 @@ int slab_sample_modes(SlabCtx* ctx, int64_t* d_state, uint64_t seed, double alph
 /* Full evaluation (sort, gather, short range, Fourier sweep, zero mode, self,
  * slab, assembly, scatter to input order). */
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* args, void* stream);
+
+/* Size of one rank's z-split exchange payload (doubles): 4 (M + 1) 2P with
+ * forces, 4 (M + 1) P energy-only; M = SOE terms, P = modes. */
+int64_t slab_zsplit_exchange_doubles(int64_t nmode, int soe_terms, int want_forces);
 
 /* rbse2d.py:320-330 _rb_batch_energy_kernel (the body of run_many_batches):
  * for b < nbatch, d_out[b] = Kahan-combined forward-sweep energy of modes

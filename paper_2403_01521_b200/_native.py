@@ -25,6 +25,8 @@ SLAB_STATUS_SINGULAR = 2
 SLAB_STATUS_NBR_OVERFLOW = 4
 SLAB_STATUS_NONFINITE = 8
 SLAB_STATUS_WALL = 16
+SLAB_SHARD_MODES = 0
+SLAB_SHARD_ZSPLIT = 1
 
 EXPORTED = (
     "slab_ctx_create", "slab_ctx_destroy", "slab_last_error", "slab_version",
@@ -32,7 +34,7 @@ EXPORTED = (
     "slab_sample_modes", "slab_evaluate", "slab_recursive_pair_sum", "slab_fp64_peak",
     "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors", "slab_batch_energies",
     "slab_wca", "slab_walls", "slab_md_langevin", "slab_md_kick", "slab_md_drift",
-    "slab_md_scale", "slab_md_kinetic",
+    "slab_md_scale", "slab_md_kinetic", "slab_zsplit_exchange_doubles",
 )
 
 
@@ -76,6 +78,9 @@ class SlabEvalArgs(ctypes.Structure):
         ("shard_count", ctypes.c_int),
         ("ev_scan_begin", ctypes.c_void_p),
         ("ev_scan_end", ctypes.c_void_p),
+        ("shard_mode", ctypes.c_int),
+        ("phase", ctypes.c_int),
+        ("d_xchg", ctypes.c_void_p),
     ]
 
 
@@ -116,13 +121,15 @@ def load():
     lib.slab_md_drift.argtypes = [vp, vp, i64, dbl, vp, dbl, dbl, vp]
     lib.slab_md_scale.argtypes = [vp, i64, dbl, vp]
     lib.slab_md_kinetic.argtypes = [vp, vp, vp, i64, vp, vp]
+    lib.slab_zsplit_exchange_doubles.argtypes = [i64, cint, cint]
     lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
     lib.slab_ctx_neighbor_capacity.argtypes = [vp, cint]
     lib.slab_ctx_last_max_neighbors.argtypes = [vp, ctypes.POINTER(cint)]
 
     for name in EXPORTED:
-        if name not in ("slab_last_error", "slab_version"):
+        if name not in ("slab_last_error", "slab_version", "slab_zsplit_exchange_doubles"):
             getattr(lib, name).restype = cint
+    lib.slab_zsplit_exchange_doubles.restype = i64
     _lib = lib
     return lib
 

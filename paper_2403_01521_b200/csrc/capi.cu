@@ -40,6 +40,7 @@ struct SlabCtx {
   int* d_maxnn = nullptr;  // longest neighbour row of the last short-range run
   double* md_part = nullptr;  // block partials of the O(N) MD reductions
   int64_t md_part_cap = 0;
+  int32_t* zs_perm = nullptr;  // z-split: the sort permutation between phase 1 and phase 2
 };
 
 namespace {
@@ -490,13 +491,29 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const SlabBox& box = a->box;
   const double area = box.lx * box.ly;
-  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, (a->want_forces && n > 0) ? 2 : 1);
+  const int scount = a->shard_count > 1 ? a->shard_count : 1;
+  const int srank = scount > 1 ? a->shard_rank : 0;
+  if (srank < 0 || srank >= scount) return fail(SLAB_ERR_ARG, "shard_rank out of range");
+  const bool zsplit = a->shard_mode == SLAB_SHARD_ZSPLIT;
+  if (a->shard_mode != SLAB_SHARD_MODES && !zsplit) return fail(SLAB_ERR_ARG, "bad shard_mode");
+  if (a->phase < 0 || a->phase > 2) return fail(SLAB_ERR_ARG, "phase must be 0, 1 or 2");
+  if (a->phase != 0 && !zsplit) return fail(SLAB_ERR_ARG, "phases belong to the z-split mode");
+  if (zsplit && a->phase == 0) return fail(SLAB_ERR_ARG, "z-split runs as phase 1 + phase 2");
+  if (zsplit && a->nmode > 0 && !a->d_xchg) return fail(SLAB_ERR_ARG, "z-split needs d_xchg");
+  const bool forces = a->want_forces && n > 0;
+  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, forces ? 2 : 1);
+  if (zsplit) {  // this rank's contiguous chunk range of the z-sorted particles
+    fp.c0 = (int)((int64_t)fp.nch * srank / scount);
+    fp.c1 = (int)((int64_t)fp.nch * (srank + 1) / scount);
+  }
   auto zp = slab::zero_plan(n, sh.mh);
   auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, a->r_c);
   if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;
   const size_t N = (size_t)(n > 0 ? n : 1);
   size_t bytes = sorted_bytes(n, sh.mh, fp, zp, true) + pad(24 * N) +
                  (a->skip_short_range ? 0 : pad(slab::short_work_bytes(sp))) + 8192;
+  if (a->phase == 2 && bytes > ctx->arena_bytes)
+    return fail(SLAB_ERR_ARG, "phase 2 without a matching phase 1 on this context");
   rc = ensure_arena(ctx, bytes);
   if (rc) return rc;
   Carver cv{(char*)ctx->arena};
@@ -509,38 +526,54 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   double* u_s = ctx->small;
   double* u_sweep = ctx->small + 1;
   double* u_pair = ctx->small + 2;
-
-  CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
-  CK(cudaMemsetAsync(ctx->small, 0, 8 * sizeof(double), st));
-  CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
-  int32_t* perm = nullptr;
-  if (n > 0) {
-    CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm, ctx->status));
-    CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm, st));
-  }
-  const int scount = a->shard_count > 1 ? a->shard_count : 1;
-  const int srank = scount > 1 ? a->shard_rank : 0;
-  if (srank < 0 || srank >= scount) return fail(SLAB_ERR_ARG, "shard_rank out of range");
   const bool lead = srank == 0;  // the rank that owns the k = 0 mode and the constants
-  if (!a->skip_short_range) {
-    const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
-    CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
-                       a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, st));
+  int32_t* perm = nullptr;
+
+  if (a->phase != 2) {  // ---- sort, short range, aggregates
+    CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(ctx->small, 0, 8 * sizeof(double), st));
+    CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
+    if (n > 0) {
+      CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm, ctx->status));
+      CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm,
+                             st));
+    }
+    ctx->zs_perm = perm;
+    if (!a->skip_short_range) {
+      const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
+      CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
+                         a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, st));
+    }
+    if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, st));
+    if (n >= 2) {
+      CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
+      if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, st));
+      if (a->nmode > 0)
+        CK(slab::fourier_phase1(fp, fw, w.xs, w.ys, w.zs, w.qs, a->d_modes, a->d_commonv,
+                                a->commonv_scalar, area, sh.b, sh.w, ctx->status,
+                                a->phase == 1 ? a->d_xchg : nullptr, st));
+    } else if (forces) {
+      CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * N, st));
+    }
+    if (a->phase == 1) return SLAB_OK;
+  } else {
+    perm = ctx->zs_perm;
   }
-  const bool forces = a->want_forces && n > 0;
-  if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, st));
+
+  // ---- carried-in states, sweep, k = 0 mode, assembly
   if (n >= 2) {
-    CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
-    if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, st));
-    if (a->nmode > 0)
-      CK(slab::fourier_run(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, a->d_modes, a->d_commonv,
-                           a->commonv_scalar, area, sh.b, sh.w, forces ? 1 : 0, u_sweep,
-                           ctx->status, w.fsorted, st));
+    if (a->nmode > 0) {
+      const double* tin = nullptr;
+      if (a->phase == 2) {
+        CK(slab::fourier_zsplit_tin(fp, a->d_xchg, scount, srank, fw.tin, st));
+        tin = fw.tin;
+      }
+      CK(slab::fourier_phase2(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, sh.b, forces ? 1 : 0,
+                              u_sweep, w.fsorted, tin, st));
+    }
     if (lead)
       CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
                           w.fzf, w.fzb, u_pair, st));
-  } else if (forces) {
-    CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * N, st));
   }
   if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, st));
   if (forces) {
@@ -554,6 +587,11 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
                            lead ? u_pair : nullptr, ctx->status, a->d_energy, ctx->small + 64,
                            lead ? 1 : 0, st));
   return SLAB_OK;
+}
+
+int64_t slab_zsplit_exchange_doubles(int64_t nmode, int soe_terms, int want_forces) {
+  if (nmode <= 0 || soe_terms <= 0) return 0;
+  return 4 * (int64_t)(soe_terms + 1) * (want_forces ? 2 : 1) * nmode;
 }
 
 }  // extern "C"

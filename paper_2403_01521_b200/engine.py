@@ -86,13 +86,17 @@ class Engine:
     # -- full evaluation ----------------------------------------------------
     def evaluate(self, pos, charge, box, alpha, r_c, soe, modes, commonv, charge_const,
                  forces=None, energy=None, want_forces=True, skip_short_range=False,
-                 perm=None, soe_pack=None, shard=(0, 1), scan_events=None):
+                 perm=None, soe_pack=None, shard=(0, 1), scan_events=None, shard_mode=0,
+                 phase=0, xchg=None):
         """Enqueue one energy/force evaluation.  ``commonv`` is a float (RB) or a
         (P,) device tensor (full mode sum).  Writes energy (8,) and forces (n,3).
 
         ``shard=(rank, count)``: multi-GPU share (caller passes this rank's mode
         slice and sums forces / energy[0:5] over ranks).  ``scan_events``: a pair
-        of torch.cuda.Event recorded around the SOE scan kernels."""
+        of torch.cuda.Event recorded around the SOE scan kernels.
+        ``shard_mode=1`` (z-split): ``phase`` 1 writes this rank's exchange payload
+        into ``xchg``, phase 2 (``xchg`` = all ranks' payloads, rank order)
+        finishes; see ``SlabEvalArgs`` in the header."""
         torch = _torch()
         n = charge.numel()
         if energy is None:
@@ -113,7 +117,8 @@ class Engine:
             d_forces=_ptr(forces) if want_forces else None, d_energy=_ptr(energy),
             d_perm=_ptr(perm), shard_rank=int(shard[0]), shard_count=int(shard[1]),
             ev_scan_begin=ctypes.c_void_p(scan_events[0].cuda_event) if scan_events else None,
-            ev_scan_end=ctypes.c_void_p(scan_events[1].cuda_event) if scan_events else None)
+            ev_scan_end=ctypes.c_void_p(scan_events[1].cuda_event) if scan_events else None,
+            shard_mode=int(shard_mode), phase=int(phase), d_xchg=_ptr(xchg))
         check(self.lib.slab_evaluate(self.ctx, ctypes.byref(args), self._stream()),
               "slab_evaluate")
         return energy, forces
@@ -308,7 +313,7 @@ class DeviceEvaluator:
 
     def __init__(self, system, box, params, soe, P=None, H=None, c_q=None, seed=0, thin=10,
                  burn_in=100, modes=None, device=None, sample=True, rank=0, world=1,
-                 group=None):
+                 group=None, shard_mode="zsplit"):
         from .rbse2d import charge_term_sum, normalization_H
         from .soewald2d import full_sum_constants
         torch = require_cuda()
@@ -349,9 +354,20 @@ class DeviceEvaluator:
             if self.sample:
                 self.eng.sample_modes(self.state, self.seed, self.alpha, box.lx, box.ly,
                                       self.thin, burn_in, 0)
-        # this rank's contiguous slice of the mode list (items are independent)
+        # multi-GPU split: "zsplit" (default) -- every rank scans all modes over its
+        # contiguous range of the z-sorted particles, one all-gather of the chunk-range
+        # maps between the two phases; "modes" -- each rank scans its slice of the
+        # modes over all particles (no mid-evaluation exchange)
+        if shard_mode not in ("zsplit", "modes"):
+            raise ValueError("shard_mode must be 'zsplit' or 'modes'")
+        self.zsplit = shard_mode == "zsplit" and self.world > 1
         from .sharding import mode_slice
-        self.t0, self.t1 = mode_slice(self.P, self.rank, self.world)
+        self.t0, self.t1 = (0, self.P) if self.zsplit else mode_slice(self.P, self.rank,
+                                                                      self.world)
+        if self.zsplit:
+            cnt = int(_native.load().slab_zsplit_exchange_doubles(self.P, len(soe.w), 1))
+            self.xloc = torch.zeros(max(cnt, 1), dtype=torch.float64, device=dev)
+            self.xall = torch.zeros(self.world * max(cnt, 1), dtype=torch.float64, device=dev)
 
     def set_positions(self, pos):
         """Replace the device positions (e.g. after an MD update), in place."""
@@ -365,13 +381,24 @@ class DeviceEvaluator:
                                   self.thin, 0, self.P, self.modes)
         modes = self.modes[self.t0:self.t1] if self.t1 > self.t0 else None
         cv = self.commonv[self.t0:self.t1] if torch.is_tensor(self.commonv) else self.commonv
-        self.eng.evaluate(self.pos, self.charge, self.box, self.alpha, self.params.r_c, self.soe,
-                          modes, cv, self.charge_const, forces=self.forces, energy=self.energy,
-                          soe_pack=self.pack, shard=(self.rank, self.world),
-                          scan_events=scan_events)
+        args = (self.pos, self.charge, self.box, self.alpha, self.params.r_c, self.soe, modes,
+                cv, self.charge_const)
+        kw = dict(forces=self.forces, energy=self.energy, soe_pack=self.pack,
+                  shard=(self.rank, self.world), scan_events=scan_events)
+        if self.zsplit:
+            self.eng.evaluate(*args, shard_mode=1, phase=1, xchg=self.xloc, **kw)
+            self.exchange(self.xloc, self.xall)
+            self.eng.evaluate(*args, shard_mode=1, phase=2, xchg=self.xall, **kw)
+        else:
+            self.eng.evaluate(*args, **kw)
         if self.reduce:
             import torch.distributed as dist
             dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
+
+    def exchange(self, local, gathered):
+        """z-split: every rank's chunk-range maps, in rank order (NCCL all-gather)."""
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(gathered, local, group=self.group)
 
     def warmup(self):
         """Run one step synchronously (workspace allocation, kernel attributes,

@@ -15,7 +15,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(REPO, "include", "slabewald_b200.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(?:int|const char\*)\s+(slab_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(?:int|int64_t|const char\*)\s+(slab_\w+)\s*\(", src)))
 
 
 def test_header_declares_the_boundary():

@@ -395,3 +395,49 @@ def test_run_many_batches_matches_per_batch_estimates(pk):
         if b % 97 == 0 or b == nb - 1:
             want = pk.rb_energy_estimate(s, box, 0.8, soe8, modes, H, c_q) + det
             assert est[b] == pytest.approx(want, rel=1e-12, abs=1e-12), b
+
+
+@pytest.mark.parametrize("W,forces", [(3, True), (4, False), (2, True)])
+def test_zsplit_ranks_sum_to_the_single_gpu_evaluation(pk, W, forces):
+    """z-split multi-GPU decomposition (SURVEY 8(e) alternative), emulated on one
+    GPU with one context per rank: phase 1 on every rank, the all-gather as a
+    concatenation, phase 2 on every rank; summed forces / energies equal the
+    single-GPU evaluation."""
+    import torch
+    from paper_2403_01521_b200 import _native
+    from paper_2403_01521_b200.configs import make_workload
+    from paper_2403_01521_b200.engine import Engine, get_engine
+    wl = make_workload("small_2000")
+    soe = pk.build_soe_contour(wl.m)
+    params = wl.params()
+    eng = get_engine()
+    dev = eng.device
+    pos = torch.as_tensor(wl.system.pos).to(dev)
+    q = torch.as_tensor(wl.system.charge).to(dev)
+    smp = pk.ModeSampler(wl.alpha, wl.box, seed=3)
+    modes = torch.as_tensor(smp.batch(wl.P)).to(dev)
+    args = (pos, q, wl.box, wl.alpha, params.r_c, soe, modes, 0.37, 1.5)
+    e1, f1 = eng.evaluate(*args, want_forces=forces)
+    e1 = e1.cpu().numpy()
+    cnt = int(_native.load().slab_zsplit_exchange_doubles(wl.P, wl.m, 1 if forces else 0))
+    engines = [Engine(dev) for _ in range(W)]
+    xloc = [torch.zeros(cnt, dtype=torch.float64, device=dev) for _ in range(W)]
+    for r in range(W):
+        engines[r].evaluate(*args, want_forces=forces, shard=(r, W), shard_mode=1, phase=1,
+                            xchg=xloc[r])
+    xall = torch.cat(xloc)
+    etot = np.zeros(8)
+    ftot = np.zeros((wl.n, 3))
+    for r in range(W):
+        e, f = engines[r].evaluate(*args, want_forces=forces, shard=(r, W), shard_mode=1,
+                                   phase=2, xchg=xall)
+        e = e.cpu().numpy()
+        assert int(e[5]) == 0
+        etot[:5] += e[:5]
+        if forces:
+            ftot += f.cpu().numpy()
+    for k in range(5):
+        assert etot[k] == pytest.approx(e1[k], rel=1e-12, abs=1e-12), k
+    if forces:
+        f1 = f1.cpu().numpy()
+        np.testing.assert_allclose(ftot, f1, rtol=0, atol=1e-12 * np.max(np.abs(f1)))

@@ -7,12 +7,16 @@ in turn -- the per-GPU work of the multi-GPU run without the NCCL all-reduce
 (the driver's scaling run measures the real thing)."""
 import sys
 
+import os
+
 import torch
 
 sys.path.insert(0, ".")
 import paper_2403_01521_b200 as pk  # noqa: E402
 from paper_2403_01521_b200.configs import make_workload  # noqa: E402
 from paper_2403_01521_b200.engine import DeviceEvaluator  # noqa: E402
+
+MODE = os.environ.get("SHARD_MODE", "zsplit")
 
 
 def main():
@@ -23,8 +27,9 @@ def main():
     params = wl.params()
     for r in range(W):
         ev = DeviceEvaluator(wl.system, wl.box, params, soe, P=wl.P, seed=wl.seed, rank=r,
-                             world=W)
+                             world=W, shard_mode=MODE)
         ev.reduce = False  # one GPU: time the rank's own work only
+        ev.exchange = lambda local, gathered: None  # (results meaningless; timing only)
         ev.warmup()
         for _ in range(2):
             ev.step()
@@ -46,8 +51,9 @@ def profile_rank(name="cfg4", W=8, r=1):
     wl = make_workload(name)
     soe = pk.build_soe_contour(wl.m)
     ev = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, P=wl.P, seed=wl.seed, rank=r,
-                         world=W)
+                         world=W, shard_mode=MODE)
     ev.reduce = False
+    ev.exchange = lambda local, gathered: None
     ev.warmup()
     ev.step()
     torch.cuda.synchronize()
