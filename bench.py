@@ -425,7 +425,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": f"{args.config}: N={wl.n} 2:1 electrolyte, Lx=Ly=2Lz, "
                                f"density 0.1, P={wl.P} sampled modes, M={wl.m} SOE terms, "
                                f"alpha={wl.alpha:.5f}, r_c={params.r_c:.4f}",
-                   "N": wl.n, "P": wl.P, "M": wl.m, "parallelism": f"modes+cells x{world}",
+                   "N": wl.n, "P": wl.P, "M": wl.m, "parallelism": f"z-split scan + cell-range short range x{world}" if world > 1 else "single GPU",
                    "l2": "no flush: per-step working set (~0.6 GB) exceeds the 126 MB L2",
                    "cuda_graph": use_graph},
         "roofline": {"bound": "fp64", "kernel": "SOE scan (3-phase Fourier scan + k=0 mode)",

@@ -466,13 +466,13 @@ int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_the
 }
 
 // short-range home-particle boundary of rank r of W (sharding.py home_range): the
-// lead rank (which also runs the k = 0 mode) takes 10 - round(1.15 W) tenths of a
+// lead rank (which also runs the k = 0 mode) takes LEAD_HOME_TENTHS[W] tenths of a
 // regular share
 static int64_t home_bound(int64_t n, int r, int W) {
+  static const int kLeadTenths[9] = {10, 10, 8, 8, 7, 5, 4, 2, 1};
   if (W <= 1 || r >= W) return r <= 0 ? 0 : n;
   if (r <= 0) return 0;
-  int64_t lead = 10 - (23 * (int64_t)W + 10) / 20;
-  lead = lead < 0 ? 0 : lead;
+  const int64_t lead = W < 9 ? kLeadTenths[W] : 0;
   return n * (lead + 10 * (int64_t)(r - 1)) / (lead + 10 * (int64_t)(W - 1));
 }
 
@@ -501,7 +501,7 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (zsplit && a->phase == 0) return fail(SLAB_ERR_ARG, "z-split runs as phase 1 + phase 2");
   if (zsplit && a->nmode > 0 && !a->d_xchg) return fail(SLAB_ERR_ARG, "z-split needs d_xchg");
   const bool forces = a->want_forces && n > 0;
-  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, forces ? 2 : 1);
+  auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, forces ? 2 : 1, zsplit ? scount : 1);
   if (zsplit) {  // this rank's contiguous chunk range of the z-sorted particles
     fp.c0 = (int)((int64_t)fp.nch * srank / scount);
     fp.c1 = (int)((int64_t)fp.nch * (srank + 1) / scount);

@@ -788,7 +788,7 @@ static size_t sweep_smem(int R, int mh, int warps) {
          sizeof(double) * (size_t)warps * kSB * 3 * kStageStride;
 }
 
-FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs) {
+FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   FourierPlan p{};
   p.n = n;
   p.P = P;
@@ -804,7 +804,9 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs) {
   if (p.ipg < 1) p.ipg = 1;
   p.warps = (p.ipg + 31) / 32;
   if (p.warps < 1) p.warps = 1;
-  const int64_t target_ctas = 4 * 148;
+  // >= 4 CTAs per SM of chunks in each rank's range (a z-split rank scans 1/ranks
+  // of the chunks: shorter chunks keep its sweep grid from ending on a partial wave)
+  const int64_t target_ctas = 4 * 148 * (int64_t)(ranks > 1 ? ranks : 1);
   int64_t rf = n * p.ngroups / target_ctas;
   int R = 16;
   while (R * 2 <= rf && R * 2 <= kMaxR) R *= 2;

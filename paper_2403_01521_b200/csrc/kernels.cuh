@@ -56,7 +56,7 @@ struct FourierPlan {
   int c0, c1;     // chunk range this plan scans (z-split multi-GPU rank), default [0, nch)
   size_t smem_sweep;
 };
-FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2);
+FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2, int ranks = 1);
 // bytes of device workspace the plan needs (carry, chunk decays, mode table, partials)
 struct FourierWork {
   double* modetab;   // P * mode_stride

@@ -37,12 +37,15 @@ def mode_slice(P: int, rank: int, world: int) -> tuple[int, int]:
 
 
 # The lead rank takes a reduced share of the short-range home particles: it also
-# runs the k = 0 mode and the assembly constants (~0.4 ms at cfg4, against a
-# short-range share of ~3.5 ms / W).  Lead share in tenths of a regular share:
-# 10 - round(1.15 W) (8, 5, 1 tenths at W = 2, 4, 8); slab_evaluate uses the same
-# integer formula (capi.cu home_bound).
+# runs the k = 0 mode and the assembly constants (~0.35 ms at cfg4, against a
+# short-range share of ~3.5 ms / W).  Lead share in tenths of a regular share,
+# measured on one B200 per rank count (tools/shard_step.py, z-split); slab_evaluate
+# uses the same table (capi.cu home_bound).
+LEAD_HOME_TENTHS = (10, 10, 8, 8, 7, 5, 4, 2, 1)  # index = world size, 0 beyond
+
+
 def lead_home_tenths(world: int) -> int:
-    return max(0, 10 - (23 * world + 10) // 20)
+    return LEAD_HOME_TENTHS[world] if world < len(LEAD_HOME_TENTHS) else 0
 
 
 def home_range(n: int, rank: int, world: int) -> tuple[int, int]:
