@@ -1,0 +1,121 @@
+"""GPU: edge cases and size-independent properties of the evaluation.
+
+Small / ragged cases are checked against the CPU oracle (oracle/, itself pinned
+to the reference's goldens in test_oracle.py); at N = 1e7 -- beyond what the
+oracle or the reference finish in test time -- size-independent identities
+(charge scaling, translation invariance, Newton's third law, shard sums)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-10
+F_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_2403_01521_b200 as pk
+    return pk
+
+
+def _oracle_eval(pk, s, box, params, soe, modes, cv, cq):
+    from oracle import oracle as O
+    O.build()
+    e, f, flag = O.energy_forces(s.pos, s.charge, box, params.alpha, params.r_c, modes,
+                                 np.broadcast_to(cv, (len(modes),)).copy(), cq, soe.w, soe.s)
+    assert flag == 0
+    return e, f
+
+
+def _check(bd, f, e_ref, f_ref):
+    got = [bd.u_s, bd.u_l_k, bd.u_l_0, bd.u_self, bd.u_ps]
+    for g, r in zip(got, e_ref):
+        assert abs(g - r) <= E_TOL * max(abs(r), 1e-300) or g == r == 0
+    if f_ref.size:
+        fmax = max(np.max(np.abs(f_ref)), 1e-300)
+        assert np.max(np.abs(f - f_ref)) <= F_TOL * fmax
+
+
+class _Stub:
+    def __init__(self, modes):
+        self.modes = modes
+
+    def batch(self, P):
+        return self.modes
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 17, 257, 4097])
+def test_ragged_sizes_match_oracle(pk, n):
+    """Empty, single, tiny and chunk-ragged systems (chunk lengths are powers of
+    two; 257 and 4097 leave one-particle tail chunks), charged slab walls."""
+    rng = np.random.default_rng(100 + n)
+    box = pk.BoxGeometry(12.0, 9.0, 7.0, sigma_top=0.004, sigma_bot=-0.0015)
+    pos = rng.uniform([0, 0, 0.1], [12.0, 9.0, 6.9], size=(n, 3))
+    q = rng.choice([-1.0, 1.0, 2.0], size=n)
+    s = pk.make_system(q, np.ones(n), pos, box)
+    params = pk.make_ewald_params(0.9, 3.5, box)
+    soe = pk.build_soe_contour(16)
+    modes = pk.ModeSampler(0.9, box, seed=n).batch(13)
+    H = pk.normalization_H(0.9, box)
+    cq = pk.charge_term_sum(0.9, box, float(np.sum(q ** 2)))
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 13, H=H, c_q=cq)
+    assert f.shape == (n, 3)
+    cv = (H / 13) * (2 / np.sqrt(np.pi)) * 0.9
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes, cv, cq)
+    _check(bd, f, e_ref, f_ref)
+
+
+def test_single_mode_and_full_sum_small(pk):
+    """P = 1 (one item pair per chunk) and a full deterministic mode sum."""
+    rng = np.random.default_rng(7)
+    box = pk.BoxGeometry(15.0, 15.0, 6.0)
+    n = 600
+    s = pk.make_system(np.where(np.arange(n) % 2 == 0, 1.0, -1.0), np.ones(n),
+                       rng.uniform([0, 0, 0.2], [15, 15, 5.8], size=(n, 3)), box)
+    params = pk.make_ewald_params(0.7, 3.0, box)
+    soe = pk.build_soe_contour(8)
+    modes = pk.ModeSampler(0.7, box, seed=1).batch(1)
+    H = pk.normalization_H(0.7, box)
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 1, H=H, c_q=0.0)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
+                                H * (2 / np.sqrt(np.pi)) * 0.7, 0.0)
+    _check(bd, f, e_ref, f_ref)
+
+
+@pytest.fixture(scope="module")
+def big(pk):
+    from paper_2403_01521_b200.configs import make_workload
+    return make_workload("cfg5_1e7")
+
+
+def _eval(pk, wl, s, modes):
+    params = wl.params()
+    soe = pk.build_soe_contour(wl.m)
+    H = pk.normalization_H(wl.alpha, wl.box)
+    return pk.rb_energy_forces(s, wl.box, params, soe, _Stub(modes), wl.P, H=H, c_q=0.0)
+
+
+def test_size_independent_identities_at_1e7(pk, big):
+    """N = 1e7 (cfg5): charge scaling by lambda scales every energy term and the
+    forces by lambda^2 exactly up to rounding; a uniform in-plane translation
+    (periodic) leaves energies and forces unchanged; the total force of a
+    neutral slab without wall charges vanishes (Newton's third law, all terms)."""
+    wl = big
+    modes = pk.ModeSampler(wl.alpha, wl.box, seed=wl.seed).batch(wl.P)
+    bd, f = _eval(pk, wl, wl.system, modes)
+    fmax = np.max(np.abs(f))
+    lam = 1.5
+    s2 = pk.make_system(wl.system.charge * lam, wl.system.mass, wl.system.pos, wl.box)
+    bd2, f2 = _eval(pk, wl, s2, modes)
+    for k in ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps"):
+        a, b = getattr(bd, k) * lam ** 2, getattr(bd2, k)
+        assert abs(a - b) <= 1e-11 * max(abs(a), 1.0), k
+    assert np.max(np.abs(f * lam ** 2 - f2)) <= 1e-11 * lam ** 2 * fmax
+    shift = np.array([0.37 * wl.box.lx, 0.61 * wl.box.ly, 0.0])
+    s3 = pk.make_system(wl.system.charge, wl.system.mass, wl.system.pos + shift, wl.box)
+    bd3, f3 = _eval(pk, wl, s3, modes)
+    assert abs(bd3.total - bd.total) <= 1e-10 * abs(bd.total)
+    assert np.max(np.abs(f3 - f)) <= 1e-9 * fmax
+    assert np.all(np.abs(f.sum(axis=0)) <= 1e-9 * fmax * np.sqrt(wl.n))
