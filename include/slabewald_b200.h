@@ -218,6 +218,22 @@ int slab_md_scale(double* d_vel, int64_t n, double s, void* stream);
 int slab_md_kinetic(SlabCtx* ctx, const double* d_vel, const double* d_mass, int64_t n,
                     double* d_out, void* stream);
 
+/* ---- O(N^2 K) Ewald2D reference solver -------------------
+ * ewald2d.py:331-442 _fourier_ref_kernel: pairwise Fourier sum over the modes
+ * (integer indices d_mxy (nmode,2), ring of equal |k| d_ring, ring norms
+ * d_kappa), "stable" (naive = 0) or "naive" xi kernels.  d_energy[0] = the pair
+ * sum (without the charge term u_q), d_forces (n,3) written.  At most 256 rings
+ * and |mx|, |my| <= 64 (SLAB_ERR_UNSUPPORTED otherwise). */
+int slab_ewald_ref_fourier(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                           double lx, double ly, double alpha, const int* d_mxy,
+                           const int* d_ring, int nmode, const double* d_kappa, int nring,
+                           int mxmax, int mymax, int naive, double* d_forces, double* d_energy,
+                           void* stream);
+/* ewald2d.py:477-501 _zero_mode_kernel: d_energy[0] = sum_{i<j} q_i q_j G(|z_ij|),
+ * d_fz[i] = sum_j q_i q_j erf(a |z_ij|) sign(z_ij) (before the 2 pi / A factor). */
+int slab_ewald_ref_zero(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                        double alpha, double* d_fz, double* d_energy, void* stream);
+
 /* Recursion of soewald2d.py:42-64 recursive_pair_sum on sorted z:
  * out[a] = sum_{j<a} q_j exp(-i theta_j - beta (z_a - z_j)), complex interleaved. */
 int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,

@@ -35,6 +35,7 @@ EXPORTED = (
     "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors", "slab_batch_energies",
     "slab_wca", "slab_walls", "slab_md_langevin", "slab_md_kick", "slab_md_drift",
     "slab_md_scale", "slab_md_kinetic", "slab_zsplit_exchange_doubles",
+    "slab_ewald_ref_fourier", "slab_ewald_ref_zero",
 )
 
 
@@ -122,6 +123,9 @@ def load():
     lib.slab_md_scale.argtypes = [vp, i64, dbl, vp]
     lib.slab_md_kinetic.argtypes = [vp, vp, vp, i64, vp, vp]
     lib.slab_zsplit_exchange_doubles.argtypes = [i64, cint, cint]
+    lib.slab_ewald_ref_fourier.argtypes = [vp, vp, vp, i64, dbl, dbl, dbl, vp, vp, cint, vp, cint,
+                                           cint, cint, cint, vp, vp, vp]
+    lib.slab_ewald_ref_zero.argtypes = [vp, vp, vp, i64, dbl, vp, vp, vp]
     lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
     lib.slab_ctx_neighbor_capacity.argtypes = [vp, cint]
     lib.slab_ctx_last_max_neighbors.argtypes = [vp, ctypes.POINTER(cint)]

@@ -453,6 +453,38 @@ int slab_md_kinetic(SlabCtx* ctx, const double* d_vel, const double* d_mass, int
   return SLAB_OK;
 }
 
+// ---------------------------------------------------------------- Ewald2D reference (ewald_ref.cu)
+int slab_ewald_ref_fourier(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                           double lx, double ly, double alpha, const int* d_mxy,
+                           const int* d_ring, int nmode, const double* d_kappa, int nring,
+                           int mxmax, int mymax, int naive, double* d_forces, double* d_energy,
+                           void* stream) {
+  if (!ctx || n < 0 || nmode < 0 || nring < 0 || !d_energy ||
+      (n > 0 && (!d_pos || !d_charge || !d_forces)) ||
+      (nmode > 0 && (!d_mxy || !d_ring || !d_kappa)))
+    return fail(SLAB_ERR_ARG, "bad Ewald2D reference arguments");
+  if (nring > slab::ewald_ref_max_ring() || mxmax > slab::ewald_ref_max_m() ||
+      mymax > slab::ewald_ref_max_m() || mxmax < 0 || mymax < 0)
+    return fail(SLAB_ERR_UNSUPPORTED, "mode set too large for the device Ewald2D reference");
+  int rc = ensure_md_part(ctx, 2 * n);  // 128-thread block partials (MD uses 256)
+  if (rc) return rc;
+  CK(slab::ewald_ref_fourier(d_pos, d_charge, n, lx, ly, alpha, d_mxy, d_ring, nmode, d_kappa,
+                             nring, mxmax, mymax, naive, d_forces, d_energy, ctx->md_part,
+                             (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
+int slab_ewald_ref_zero(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                        double alpha, double* d_fz, double* d_energy, void* stream) {
+  if (!ctx || n < 0 || !d_energy || (n > 0 && (!d_pos || !d_charge || !d_fz)))
+    return fail(SLAB_ERR_ARG, "bad k = 0 reference arguments");
+  int rc = ensure_md_part(ctx, 2 * n);
+  if (rc) return rc;
+  CK(slab::ewald_ref_zero(d_pos, d_charge, n, alpha, d_fz, d_energy, ctx->md_part,
+                          (cudaStream_t)stream));
+  return SLAB_OK;
+}
+
 int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_theta,
                             const double* d_z, int64_t n, double beta_re, double beta_im,
                             double* d_out, void* stream) {

@@ -175,4 +175,16 @@ cudaError_t fz_accumulate(int64_t n, const double* fzf, const double* fzb, doubl
 
 namespace slab {
 cudaError_t fp64_peak(double* tflops);
+// ---------------------------------------------------------------- ewald_ref.cu
+int64_t ewald_ref_partials(int64_t n);
+int ewald_ref_max_ring();
+int ewald_ref_max_m();
+cudaError_t ewald_ref_fourier(const double* pos, const double* charge, int64_t n, double lx,
+                              double ly, double alpha, const int* mxy, const int* ring_id,
+                              int nmode, const double* kappa, int nring, int mxmax, int mymax,
+                              int naive, double* forces, double* energy, double* part,
+                              cudaStream_t st);
+cudaError_t ewald_ref_zero(const double* pos, const double* charge, int64_t n, double alpha,
+                           double* fz, double* energy, double* part, cudaStream_t st);
+
 }  // namespace slab

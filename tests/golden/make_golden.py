@@ -244,13 +244,40 @@ def golden_md() -> dict:
     return out
 
 
+def golden_ewald_ref() -> dict:
+    """ewald2d.py: the O(N^2 K) Ewald2D reference on two small neutral systems
+    (stable and naive xi kernels, k = 0 mode, full breakdown)."""
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    out = {}
+    for tag, n, box_l, alpha, s_par, seed in (("a", 60, (10.0, 10.0, 5.0), 0.6, 3.0, 21),
+                                              ("b", 200, (14.0, 11.0, 7.0), 0.8, 3.5, 22)):
+        rng = np.random.default_rng(seed)
+        box = core.BoxGeometry(*box_l)
+        pos = rng.uniform([0, 0, 0.2], [box_l[0], box_l[1], box_l[2] - 0.2], size=(n, 3))
+        q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+        sysm = core.make_system(q, np.ones(n), pos, box=box)
+        params = core.make_ewald_params(alpha, s_par, box)
+        bd, f = ewald2d.ref_energy_forces(sysm, box, params)
+        out[f"{tag}_pos"] = sysm.pos
+        out[f"{tag}_nmode"] = params.kmodes.shape[0]
+        for k in ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps"):
+            out[f"{tag}_{k}"] = getattr(bd, k)
+        out[f"{tag}_forces"] = f
+        uk, fk = ewald2d.fourier_energy_forces_ref(sysm, box, params, "naive")
+        out[f"{tag}_naive_u"], out[f"{tag}_naive_f"] = uk, fk
+        u0, f0 = ewald2d.zero_mode_energy_forces_ref(sysm, box, alpha)
+        out[f"{tag}_zero_u"], out[f"{tag}_zero_f"] = u0, f0
+    return out
+
+
 def main(argv):
     names = argv or ["units", "cfg1", "cfg2", "small_600", "small_2000", "cfg5_1e4",
                      "cfg3", "cfg5_1e5", "cfg4", "cfg5_1e6"]
     for name in names:
         t0 = time.perf_counter()
         data = (golden_units() if name == "units" else
-                golden_md() if name == "md" else golden_workload(name))
+                golden_md() if name == "md" else
+                golden_ewald_ref() if name == "ewald_ref" else golden_workload(name))
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in data.items()})
         print(f"{name}: wrote {path} ({os.path.getsize(path)/1e3:.0f} kB) "

@@ -441,3 +441,37 @@ def test_zsplit_ranks_sum_to_the_single_gpu_evaluation(pk, W, forces):
     if forces:
         f1 = f1.cpu().numpy()
         np.testing.assert_allclose(ftot, f1, rtol=0, atol=1e-12 * np.max(np.abs(f1)))
+
+
+@pytest.mark.parametrize("tag,box_l,alpha,s_par", [("a", (10.0, 10.0, 5.0), 0.6, 3.0),
+                                                   ("b", (14.0, 11.0, 7.0), 0.8, 3.5)])
+def test_ewald2d_reference_solver_matches_reference(pk, tag, box_l, alpha, s_par):
+    """the O(N^2 K) Ewald2D reference on device against the
+    reference's own ref_energy_forces (stable), the naive xi variant and the
+    k = 0 mode (tests/golden/ewald_ref.npz); and SOEwald2D agrees with it to the
+    SOE accuracy (M = 16, eps ~ 1e-9)."""
+    g = load_golden("ewald_ref")
+    box = pk.BoxGeometry(*box_l)
+    pos = g[f"{tag}_pos"]
+    n = len(pos)
+    s = pk.make_system(np.where(np.arange(n) % 2 == 0, 1.0, -1.0), np.ones(n), pos, box)
+    params = pk.make_ewald_params(alpha, s_par, box)
+    bd, f = pk.ref_energy_forces(s, box, params)
+    for k in ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps"):
+        ref = float(g[f"{tag}_{k}"])
+        assert getattr(bd, k) == pytest.approx(ref, rel=1e-10, abs=1e-12), k
+    fref = g[f"{tag}_forces"]
+    np.testing.assert_allclose(f, fref, rtol=0, atol=1e-9 * np.max(np.abs(fref)))
+    un, fn = pk.fourier_energy_forces_ref(s, box, params, "naive")
+    assert un == pytest.approx(float(g[f"{tag}_naive_u"]), rel=1e-10)
+    np.testing.assert_allclose(fn, g[f"{tag}_naive_f"], rtol=0,
+                               atol=1e-9 * np.max(np.abs(g[f"{tag}_naive_f"])))
+    u0, f0 = pk.zero_mode_energy_forces_ref(s, box, alpha)
+    assert u0 == pytest.approx(float(g[f"{tag}_zero_u"]), rel=1e-10)
+    np.testing.assert_allclose(f0, g[f"{tag}_zero_f"], rtol=0,
+                               atol=1e-9 * np.max(np.abs(g[f"{tag}_zero_f"])))
+    soe = pk.build_soe_contour(16)
+    bs, fs = pk.soe_energy_forces(s, box, params, soe)
+    assert bs.total == pytest.approx(bd.total, rel=1e-7)
+    with pytest.raises(ValueError, match="neutral"):
+        pk.ref_energy_forces(pk.make_system(np.ones(n), np.ones(n), pos, box), box, params)
