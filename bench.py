@@ -389,7 +389,7 @@ def run_ours(args, rank, world, local):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms, scan_ms = float(tt[0]), float(tt[1])
     e = ev.energy.cpu().numpy()
-    status = int(e[5])
+    status = ev.status()
 
     # ---- e2e: the public API from pinned host memory, result read back ----
     e2e = None

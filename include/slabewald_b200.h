@@ -91,7 +91,9 @@ typedef struct SlabEvalArgs {
   int want_forces;          /* 0: energies only (forces untouched) */
   int skip_short_range;     /* 1: u_s = 0, no short-range forces (sub-path calls) */
   double* d_forces;         /* (n,3) out, input order */
-  double* d_energy;         /* (8,) out: u_s,u_l_k,u_l_0,u_self,u_ps,status,0,0 */
+  double* d_energy;         /* (8,) out: u_s, u_l_k, u_l_0, u_self, u_ps, status bits,
+                               Q = sum q^2 (lead rank), status as sum_k bit_k 256^k (a
+                               SUM all-reduce over ranks keeps every bit recoverable) */
   int64_t* d_perm;          /* optional (n,) out: the z-sort permutation, or NULL */
   /* Multi-GPU (one process per GPU, particles replicated): this
    * rank evaluates only its share and the caller sums d_forces and d_energy[0..4]

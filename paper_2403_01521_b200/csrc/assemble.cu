@@ -90,9 +90,16 @@ __global__ void __launch_bounds__(512) assemble_energy_kernel(
     energy[2] = u0;
     energy[3] = include_constants ? alpha / kSqrtPi * Q : 0.0;
     energy[4] = include_constants ? r1[0] : 0.0;
-    energy[5] = status ? (double)status[0] : 0.0;
-    energy[6] = Q;
-    energy[7] = 0.0;
+    const int st = status ? status[0] : 0;
+    energy[5] = (double)st;
+    energy[6] = include_constants ? Q : 0.0;
+    // status again, one 8-bit counter per bit (bit k -> 256^k): the multi-GPU
+    // all-reduce SUMS the packed energies, which keeps "any rank set bit k"
+    // recoverable for up to 255 ranks (slot 5 is the single-rank form)
+    double spread = 0.0, w = 1.0;
+    for (int k = 0; k < 6; ++k, w *= 256.0)
+      if (st & (1 << k)) spread += w;
+    energy[7] = spread;
   }
 }
 

@@ -395,6 +395,11 @@ class DeviceEvaluator:
             import torch.distributed as dist
             dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
 
+    def status(self) -> int:
+        """Status bits of the last step (any rank, after the all-reduce); synchronous."""
+        from .ewald2d import status_of
+        return status_of(self.energy.cpu().numpy(), summed=self.reduce)
+
     def exchange(self, local, gathered):
         """z-split: every rank's chunk-range maps, in rank order (NCCL all-gather)."""
         import torch.distributed as dist
@@ -407,7 +412,7 @@ class DeviceEvaluator:
         while True:
             self._enqueue()
             torch.cuda.synchronize(self.eng.device)
-            if not self.eng.handle_overflow(int(self.energy[5].item())):
+            if not self.eng.handle_overflow(self.status()):
                 return
 
     def capture(self):

@@ -48,6 +48,19 @@ def check_short_range_cutoff(box: BoxGeometry, r_c: float) -> None:
         raise ValueError("r_c must not exceed half the in-plane box size")
 
 
+def status_of(energy, summed: bool = False) -> int:
+    """Status bits from an evaluation's energy vector; ``summed``: the vector went
+    through the multi-GPU SUM all-reduce (decode slot 7's 8-bit-per-bit counters)."""
+    if not summed:
+        return int(energy[5])
+    v = int(round(float(energy[7])))
+    st = 0
+    for k in range(6):
+        if (v >> (8 * k)) & 255:
+            st |= 1 << k
+    return st
+
+
 def raise_on_status(status: int) -> None:
     from ._native import SLAB_STATUS_COINCIDENT, SLAB_STATUS_NONFINITE, SLAB_STATUS_SINGULAR
     if status & SLAB_STATUS_NONFINITE:  # checked first, like sort_by_z (core.py:206-207)

@@ -181,3 +181,18 @@ def test_md_host_pieces_without_gpu():
                               np.zeros((2, 3)))
     np.testing.assert_allclose(p2, 0.1 * vel)
     np.testing.assert_allclose(v2, vel)
+
+
+def test_status_survives_the_sum_allreduce():
+    """Slot 7 carries the status bits as 8-bit counters: summing the energy
+    vectors of several ranks (the multi-GPU all-reduce) keeps every bit."""
+    from paper_2403_01521_b200.ewald2d import status_of
+    def vec(bits):
+        v = np.zeros(8)
+        v[5] = bits
+        v[7] = sum(256.0 ** k for k in range(6) if bits & (1 << k))
+        return v
+    ranks = [vec(4), vec(4 | 1), vec(0), vec(4)]
+    assert status_of(sum(ranks), summed=True) == 5
+    assert status_of(vec(8)) == 8
+    assert status_of(sum(vec(0) for _ in range(8)), summed=True) == 0
