@@ -347,7 +347,8 @@ def run_ours(args, rank, world, local):
         ev.capture()
         for _ in range(2):
             ev.step()
-    launches_per_step, ktimes = profile_step(ev, torch) if rank == 0 else (0, {})
+    # every rank steps (the step has collectives); rank 0 reports its own counts
+    launches_per_step, ktimes = profile_step(ev, torch)
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident, CUDA events, max over ranks ----
@@ -413,6 +414,8 @@ def run_ours(args, rank, world, local):
                "api": "paper_2403_01521_b200.rb_energy_forces (numpy in / numpy out)"}
 
     if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
         return 0
     peak = ctypes_peak(_native)
     flops = scan_flops(wl.n, wl.P, wl.m, world)
