@@ -21,6 +21,10 @@
 
 namespace slab {
 
+#ifndef SLAB_ZERO_LANES
+#define SLAB_ZERO_LANES 1
+#endif
+
 template <int MH>
 __global__ void zero_aggregate_kernel(const double* __restrict__ zs, const double* __restrict__ qs,
                                       const double2* __restrict__ dtab, int64_t n, int R, int nch,
@@ -247,6 +251,55 @@ __global__ void zero_sweep_kernel(const double* __restrict__ zs, const double* _
   }
 }
 
+// ---- lane-per-pair aggregate (default): the (chunk, direction) work is spread
+// over G = pow2 >= MH lanes, lane l < MH carrying pair l (4 doubles of state
+// instead of 4 MH per thread; the thread-per-chunk kernel runs at 10%
+// occupancy): 0.106 -> 0.066 ms at cfg4.  Lane reads of the decay rows are
+// contiguous; the (S0, S1) prefix sums are carried redundantly by every lane.
+// (The same split of the sweep needs a per-particle shuffle reduction over the
+// pairs and measured slower, 0.154 against 0.124 ms.)
+template <int MH>
+__host__ __device__ constexpr int zlanes() {
+  return MH <= 2 ? 2 : MH <= 4 ? 4 : MH <= 8 ? 8 : 16;
+}
+
+template <int MH>
+__global__ void __launch_bounds__(128) zero_aggregate_lane_kernel(
+    const double* __restrict__ zs, const double* __restrict__ qs,
+    const double2* __restrict__ dtab, int64_t n, int R, int nch, double2* __restrict__ zagg) {
+  constexpr int G = zlanes<MH>();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t grp = e / G;
+  const int l = (int)(e - grp * G);
+  if (grp >= 2 * (int64_t)nch) return;
+  const int c = (int)(grp >> 1), dir = (int)(grp & 1);
+  const int64_t a0 = (int64_t)c * R, a1 = a0 + R < n ? a0 + R : n;
+  const bool act = l < MH;
+  C2 TA{0.0, 0.0}, TB{0.0, 0.0};
+  double S0 = 0.0, S1 = 0.0;
+  for (int64_t s = 0; s < a1 - a0; ++s) {
+    const int64_t a = dir == 0 ? a0 + s : a1 - 1 - s;
+    const double q = qs[a];
+    if (s > 0 && act) {
+      const int64_t ad = dir == 0 ? a : a + 1;
+      const double dz = zs[ad] - zs[ad - 1];
+      const double2 d = dtab[ad * MH + l];
+      const C2 bt{fma(dz, TA.re, TB.re), fma(dz, TA.im, TB.im)};
+      TB = cmul(bt, C2{d.x, d.y});
+      TA = cmul(TA, C2{d.x, d.y});
+    }
+    TA.re += q;
+    S0 += q;
+    S1 = fma(q, zs[a], S1);
+  }
+  double2* out = zagg + ((size_t)c * 2 + dir) * (2 * MH + 1);
+  if (act) {
+    out[l] = make_double2(TA.re, TA.im);
+    out[MH + l] = make_double2(TB.re, TB.im);
+  }
+  if (l == 0) out[2 * MH] = make_double2(S0, S1);
+}
+
 // three fixed-order block sums over chunks (one block per term), then combine
 __global__ void __launch_bounds__(256) zero_energy_kernel(const double* __restrict__ zep, int nch,
                                                           double* __restrict__ tsum) {
@@ -299,7 +352,13 @@ static void zero_launch(const ZeroPlan& p, double* work, const double* zs, const
   double* zep = zdz + 2 * nch;
   double* tsum = zep + 3 * nch;
   const int nthr = 2 * p.nch;
+#if SLAB_ZERO_LANES
+  const int64_t nlane = (int64_t)nthr * zlanes<MH>();
+  zero_aggregate_lane_kernel<MH><<<(unsigned)((nlane + 127) / 128), 128, 0, st>>>(
+      zs, qs, dtab, p.n, p.R, p.nch, zagg);
+#else
   zero_aggregate_kernel<MH><<<(nthr + 63) / 64, 64, 0, st>>>(zs, qs, dtab, p.n, p.R, p.nch, zagg);
+#endif
   const int nd = 2 * p.nch * MH;
   zero_chunk_decay_kernel<<<(nd + 255) / 256, 256, 0, st>>>(zs, p.n, p.R, p.nch, MH, b, zdz, zD);
   zero_carry_kernel<<<2 * (MH + 1), kZCarryThreads, 0, st>>>(p.nch, MH, zdz, zD, zagg);
