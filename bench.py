@@ -400,7 +400,11 @@ def run_ours(args, rank, world, local):
         pinned_sys.pos = pinned_like(sysm.pos)
         pinned_sys.charge = pinned_like(sysm.charge)
         sampler = ModeSampler(wl.alpha, wl.box, seed=wl.seed)
-        pk.rb_energy_forces(pinned_sys, wl.box, params, soe, sampler, wl.P, H=H, c_q=c_q)
+        # W untimed calls, at least 2: the second still takes fresh page-locked
+        # result buffers from the host allocator (the first call's are still held)
+        for _ in range(max(2, args.warmup)):
+            bd, f = pk.rb_energy_forces(pinned_sys, wl.box, params, soe, sampler, wl.P, H=H,
+                                        c_q=c_q)
         torch.cuda.synchronize()
         te = time.perf_counter()
         for _ in range(K):

@@ -176,6 +176,20 @@ int slab_sample_modes(SlabCtx* ctx, int64_t* d_state, uint64_t seed, double alph
  * slab, assembly, scatter to input order). */
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* args, void* stream);
 
+/* slab_evaluate on HOST buffers -- the call behind rb_energy_forces /
+ * soe_energy_forces (rbse2d.py:274-317, soewald2d.py:398-438), whose inputs and
+ * outputs are numpy arrays.  h_pos (n x 3, AoS) and h_charge (n) are read,
+ * h_forces (n x 3, input order; may be NULL when want_forces = 0) and
+ * h_energy (8, the d_energy layout) are written; args->d_pos / d_charge /
+ * d_forces / d_energy are ignored (the context keeps device copies) while
+ * d_modes / d_commonv stay DEVICE pointers (the device sampler's output).
+ * Uploads run on a context-owned stream, the charges overlapping the z sort;
+ * page-locked host memory copies at DMA speed.  Synchronises `stream` before
+ * returning.  Unsharded (shard_mode 0, phase 0) evaluations only. */
+int slab_evaluate_host(SlabCtx* ctx, const SlabEvalArgs* args, const double* h_pos,
+                       const double* h_charge, double* h_forces, double* h_energy,
+                       void* stream);
+
 /* Size of one rank's z-split exchange payload (doubles): 4 (M + 1) 2P with
  * forces, 4 (M + 1) P energy-only; M = SOE terms, P = modes. */
 int64_t slab_zsplit_exchange_doubles(int64_t nmode, int soe_terms, int want_forces);

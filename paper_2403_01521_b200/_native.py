@@ -35,7 +35,7 @@ EXPORTED = (
     "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors", "slab_batch_energies",
     "slab_wca", "slab_walls", "slab_md_langevin", "slab_md_kick", "slab_md_drift",
     "slab_md_scale", "slab_md_kinetic", "slab_zsplit_exchange_doubles",
-    "slab_ewald_ref_fourier", "slab_ewald_ref_zero",
+    "slab_ewald_ref_fourier", "slab_ewald_ref_zero", "slab_evaluate_host",
 )
 
 
@@ -111,6 +111,7 @@ def load():
     lib.slab_sample_modes.argtypes = [vp, vp, ctypes.c_uint64, dbl, dbl, dbl, cint, cint, i64, vp,
                                       vp, vp]
     lib.slab_evaluate.argtypes = [vp, ctypes.POINTER(SlabEvalArgs), vp]
+    lib.slab_evaluate_host.argtypes = [vp, ctypes.POINTER(SlabEvalArgs), vp, vp, vp, vp, vp]
     lib.slab_recursive_pair_sum.argtypes = [vp, vp, vp, vp, i64, dbl, dbl, vp, vp]
     lib.slab_batch_energies.argtypes = [vp, vp, vp, i64, SlabSOE, dbl, dbl, vp, i64, i64, dbl, vp,
                                         vp, vp]

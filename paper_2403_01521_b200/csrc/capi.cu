@@ -41,6 +41,15 @@ struct SlabCtx {
   double* md_part = nullptr;  // block partials of the O(N) MD reductions
   int64_t md_part_cap = 0;
   int32_t* zs_perm = nullptr;  // z-split: the sort permutation between phase 1 and phase 2
+  // slab_evaluate_host: device copies of the host buffers, an upload stream and
+  // its events (created on first use)
+  double* h_dpos = nullptr;
+  double* h_dq = nullptr;
+  double* h_dforces = nullptr;
+  double* h_denergy = nullptr;
+  int64_t h_cap = -1;
+  cudaStream_t up_stream = nullptr;
+  cudaEvent_t ev_pos = nullptr, ev_q = nullptr;
 };
 
 namespace {
@@ -194,6 +203,13 @@ int slab_ctx_destroy(SlabCtx* ctx) {
   if (ctx->sampler_scratch) cudaFree(ctx->sampler_scratch);
   if (ctx->d_maxnn) cudaFree(ctx->d_maxnn);
   if (ctx->md_part) cudaFree(ctx->md_part);
+  if (ctx->h_dpos) cudaFree(ctx->h_dpos);
+  if (ctx->h_dq) cudaFree(ctx->h_dq);
+  if (ctx->h_dforces) cudaFree(ctx->h_dforces);
+  if (ctx->h_denergy) cudaFree(ctx->h_denergy);
+  if (ctx->up_stream) cudaStreamDestroy(ctx->up_stream);
+  if (ctx->ev_pos) cudaEventDestroy(ctx->ev_pos);
+  if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
   delete ctx;
   return SLAB_OK;
 }
@@ -508,8 +524,78 @@ static int64_t home_bound(int64_t n, int r, int W) {
   return n * (lead + 10 * (int64_t)(r - 1)) / (lead + 10 * (int64_t)(W - 1));
 }
 
+static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
+                         cudaEvent_t pos_ready, cudaEvent_t charge_ready);
+
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (!ctx || !a) return fail(SLAB_ERR_ARG, "null context or arguments");
+  return evaluate_impl(ctx, a, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+int slab_evaluate_host(SlabCtx* ctx, const SlabEvalArgs* args, const double* h_pos,
+                       const double* h_charge, double* h_forces, double* h_energy,
+                       void* stream) {
+  if (!ctx || !args || !h_energy) return fail(SLAB_ERR_ARG, "null context or arguments");
+  const int64_t n = args->n;
+  if (n < 0) return fail(SLAB_ERR_ARG, "bad evaluation arguments");
+  if (n > 0 && (!h_pos || !h_charge)) return fail(SLAB_ERR_ARG, "host inputs missing");
+  if (args->want_forces && n > 0 && !h_forces) return fail(SLAB_ERR_ARG, "forces output missing");
+  if (args->shard_mode != SLAB_SHARD_MODES || args->phase != 0)
+    return fail(SLAB_ERR_ARG, "the host-buffer form runs unsharded-mode evaluations only");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!ctx->up_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_pos, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_q, cudaEventDisableTiming));
+    CK(cudaMalloc(&ctx->h_denergy, 8 * sizeof(double)));
+  }
+  if (n > ctx->h_cap) {
+    CK(cudaStreamSynchronize(st));
+    if (ctx->h_dpos) CK(cudaFree(ctx->h_dpos));
+    if (ctx->h_dq) CK(cudaFree(ctx->h_dq));
+    if (ctx->h_dforces) CK(cudaFree(ctx->h_dforces));
+    const size_t cap = (size_t)(n > 0 ? n : 1);
+    CK(cudaMalloc(&ctx->h_dpos, 3 * sizeof(double) * cap));
+    CK(cudaMalloc(&ctx->h_dq, sizeof(double) * cap));
+    CK(cudaMalloc(&ctx->h_dforces, 3 * sizeof(double) * cap));
+    ctx->h_cap = n;
+  }
+  // uploads on the side stream, concurrent with work already queued on `stream`
+  // (e.g. the device sampler's chain for this batch): positions first (the z
+  // sort needs only them), then charges, which land while the sort runs.  The
+  // buffers are private to this entry point, which leaves both streams idle
+  // on return (success or failure), so no earlier work can still read them.
+  if (n > 0) {
+    CK(cudaMemcpyAsync(ctx->h_dpos, h_pos, 3 * sizeof(double) * n, cudaMemcpyHostToDevice,
+                       ctx->up_stream));
+    CK(cudaEventRecord(ctx->ev_pos, ctx->up_stream));
+    CK(cudaMemcpyAsync(ctx->h_dq, h_charge, sizeof(double) * n, cudaMemcpyHostToDevice,
+                       ctx->up_stream));
+  } else {
+    CK(cudaEventRecord(ctx->ev_pos, ctx->up_stream));
+  }
+  CK(cudaEventRecord(ctx->ev_q, ctx->up_stream));
+  SlabEvalArgs a = *args;
+  a.d_pos = ctx->h_dpos;
+  a.d_charge = ctx->h_dq;
+  a.d_forces = args->want_forces ? ctx->h_dforces : nullptr;
+  a.d_energy = ctx->h_denergy;
+  const int rc = evaluate_impl(ctx, &a, st, ctx->ev_pos, ctx->ev_q);
+  if (rc) {
+    cudaStreamSynchronize(ctx->up_stream);
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  if (args->want_forces && n > 0)
+    CK(cudaMemcpyAsync(h_forces, ctx->h_dforces, 3 * sizeof(double) * n,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_energy, ctx->h_denergy, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return SLAB_OK;
+}
+
+static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
+                         cudaEvent_t pos_ready, cudaEvent_t charge_ready) {
   const int64_t n = a->n;
   if (n < 0 || a->nmode < 0 || !a->d_energy || (n > 0 && (!a->d_pos || !a->d_charge)))
     return fail(SLAB_ERR_ARG, "bad evaluation arguments");
@@ -520,7 +606,6 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   SOEHost sh;
   int rc = prepare_soe(a->soe, a->alpha, sh);
   if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
   const SlabBox& box = a->box;
   const double area = box.lx * box.ly;
   const int scount = a->shard_count > 1 ? a->shard_count : 1;
@@ -565,8 +650,10 @@ int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
     CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
     CK(cudaMemsetAsync(ctx->small, 0, 8 * sizeof(double), st));
     CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
+    if (pos_ready) CK(cudaStreamWaitEvent(st, pos_ready, 0));
     if (n > 0) {
       CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm, ctx->status));
+      if (charge_ready) CK(cudaStreamWaitEvent(st, charge_ready, 0));
       CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm,
                              st));
     }

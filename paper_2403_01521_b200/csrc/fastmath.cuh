@@ -157,14 +157,25 @@ __device__ __forceinline__ void sincos_fast_cb(double th, double* s, double* c) 
 // distances put x = alpha r in ~20 adjacent rows).  Interval-major rows read as
 // 16-byte pairs measured 5% slower on the pair kernel (8 lanes per LDS.128
 // phase over 8 bank groups collide).
+#ifndef SLAB_ERFC_CB
+#define SLAB_ERFC_CB 1  // constant-bank exp in the pair kernel: 2.34 -> 2.27 ms at cfg4
+#endif
+// kTabOnly: the caller guarantees x < 6 (alpha r_c < 6): no branch around the
+// table (the libdevice arm costs ~8 branch-control instructions per pair even
+// when never taken)
+template <bool kTabOnly = false>
 __device__ __forceinline__ void erfc_gauss(double x, const double* __restrict__ tab,
                                            double* erfc_out, double* g_out) {
   const double hi = x * x;
   const double lo = fma(x, x, -hi);
+#if SLAB_ERFC_CB
+  double g = exp_neg_cb(hi);
+#else
   double g = exp_neg(hi);
+#endif
   g = fma(-lo, g, g);  // e^{-(hi+lo)} = e^{-hi} (1 - lo)
   double ex;
-  if (x < SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W) {
+  if (kTabOnly || x < SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W) {
     const int i = (int)(x * SLAB_ERFCX_INV_W);
     const double u = fma(2.0 * SLAB_ERFCX_INV_W, x, -(double)(2 * i + 1));
     const double* cf = tab + i;

@@ -118,11 +118,11 @@ struct ShortPlan {
   int jsplit;     // brute path: j-range splits
   int64_t nblk;   // energy partial count
   int kcap;       // neighbour-row capacity (multiple of 8)
-  int span;       // cell search span: 1 (edge >= r_c) or 2 (edge >= r_c/2)
+  int span;       // cell search span S: cells of edge >= r_c / S, (2S+1)^2 columns
 };
 // max_span 1: cells of edge >= rc (fewer cells: the short WCA cutoff of a big box
 // would otherwise need ~6e7 half-edge cells at N = 1e6)
-ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int max_span = 2);
+ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int max_span = 3);
 size_t short_work_bytes(const ShortPlan& p);
 cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const double* charge,
                       double lx, double ly, double lz, double alpha, double rc, double* forces,

@@ -69,6 +69,13 @@ __device__ __forceinline__ void pair_accumulate(double xi, double yi, double zi,
 // scheduler can interleave.  Masked pairs add exact zeros.  (Measured slower:
 // carrying the image shift in the row entries instead of rint(dx / lx), +5%;
 // a warp-vote guard instead of the branch around the table, +4%; every extra table row costs: the per-block smem fill is ~7% of the kernel.)
+// d - l rint(d / l), with the reciprocal product (a compare/select form for the
+// shifts -1, 0, 1 measured 3% slower on the pair kernel: FRND is full rate)
+__device__ __forceinline__ double min_image(double d, double l, double il) {
+  return __dsub_rn(d, __dmul_rn(l, rint(__dmul_rn(d, il))));
+}
+
+template <bool kTabOnly>
 __device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, double zi, double qi,
                                                        double xj, double yj, double zj, double qj,
                                                        double lx, double ly, double ilx, double ily,
@@ -77,8 +84,8 @@ __device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, dou
                                                        PairAcc& acc, int& flag) {
   double dx = __dsub_rn(xi, xj), dy = __dsub_rn(yi, yj);
   const double dz = __dsub_rn(zi, zj);
-  dx = __dsub_rn(dx, __dmul_rn(lx, rint(__dmul_rn(dx, ilx))));
-  dy = __dsub_rn(dy, __dmul_rn(ly, rint(__dmul_rn(dy, ily))));
+  dx = min_image(dx, lx, ilx);
+  dy = min_image(dy, ly, ily);
   const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
   const bool in = d2 <= rc2;
   const bool coincident = d2 < 1e-24;
@@ -89,7 +96,7 @@ __device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, dou
   const double d = d2u * inv_d;
   const double qq = use ? qi * qj : 0.0;
   double e, g;
-  erfc_gauss(alpha * d, etab, &e, &g);
+  erfc_gauss<kTabOnly>(alpha * d, etab, &e, &g);
   acc.e = fma(qq * e, inv_d, acc.e);
   const double fmag = qq * (e * inv_d + c * g) * (inv_d * inv_d);
   acc.fx = fma(fmag, dx, acc.fx);
@@ -184,9 +191,10 @@ constexpr int kRing = 16;  // staged neighbour indices per thread (two 32-byte s
 // Pass 1: neighbour rows.  One thread per home particle in cell order.  Cells
 // are ordered z-fastest, so the z cells of one (x, y) column are one contiguous
 // range: at most (2S+1)^2 ranges per particle, each trimmed to the z extent the
-// r_c sphere has over that column (corner columns often drop out).  S = 2 on
-// cells of edge >= r_c/2: mean search volume ~10.5 r_c^3, against 15.6 r_c^3
-// for untrimmed 5-cell columns and 27 r_c^3 for S = 1 on cells >= r_c.  Conservative fp32 distance screen; hits go to a
+// r_c sphere has over that column (corner columns often drop out).  Mean
+// candidates per home at uniform density (sphere = 1): 2.3x for S = 2 (cells of
+// edge >= r_c/2), 1.8x for S = 3 (the default), 6.4x for the reference's
+// 27 cells of edge >= r_c.  Conservative fp32 distance screen; hits go to a
 // per-thread ring in shared memory (slot-major: conflict-free) and are written
 // as whole 32-byte sectors into the row nbr[(a - a_begin) * kcap + k].
 template <int S>
@@ -285,7 +293,8 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
 // flight per iteration (measured: 2 or 8 in flight, a generic unrolled loop, or
 // a min-blocks launch bound are all 5-20% slower).  Each force is owned by one
 // thread: deterministic.
-// KIND 0: erfc Coulomb (alpha); KIND 1: WCA core (eps, sig2 = sigma^2).
+// KIND 0: erfc Coulomb (alpha); KIND 2: the same with alpha r_c inside the erfcx table
+// (branch-free); KIND 1: WCA core (eps, sig2 = sigma^2).
 template <int KIND>
 __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     const double4* __restrict__ cp, const int32_t* __restrict__ order,
@@ -293,9 +302,9 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2, double eps,
     double sig2, double* __restrict__ forces, double* __restrict__ eblk,
     int* __restrict__ status, int accumulate) {
-  __shared__ double etab[KIND == 0 ? kErfcxTabSize : 1];
+  __shared__ double etab[KIND != 1 ? kErfcxTabSize : 1];
   __shared__ double red[kSRThreads];
-  if constexpr (KIND == 0) load_erfcx_table(etab);
+  if constexpr (KIND != 1) load_erfcx_table(etab);
   __syncthreads();
   const double c = kTwoOverSqrtPi * alpha;
   const double ilx = 1.0 / lx, ily = 1.0 / ly;
@@ -303,8 +312,8 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
   int flag = 0;
 #define PAIR(pi, pj)                                                                          \
   do {                                                                                        \
-    if constexpr (KIND == 0)                                                                  \
-      pair_accumulate_masked(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, \
+    if constexpr (KIND != 1)                                                                  \
+      pair_accumulate_masked<KIND == 2>(pi.x, pi.y, pi.z, pi.w, pj.x, pj.y, pj.z, pj.w, lx, ly, ilx, ily, \
                              alpha, rc2, c, etab, acc, flag);                                 \
     else                                                                                      \
       wca_accumulate<true>(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, lx, ly, ilx, ily, rc2, eps,    \
@@ -423,6 +432,11 @@ __global__ void __launch_bounds__(1024) half_sum_kernel(const double* __restrict
 // pair_list_kernel grid: one resident wave (5 CTAs per SM at 90 registers), grid-striding
 static int64_t pair_grid(int64_t blocks) { return blocks < 148 * 5 ? blocks : 148 * 5; }
 
+#ifndef SLAB_SHORT_SPAN_DEFAULT
+#define SLAB_SHORT_SPAN_DEFAULT 3  // cfg4: nbr_build 1.12 -> 1.02 ms (pair_list +0.04)
+#endif
+constexpr int kShortSpan = SLAB_SHORT_SPAN_DEFAULT;
+
 ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int max_span) {
   ShortPlan p{};
   p.n = n;
@@ -435,13 +449,17 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int 
   if (p.brute) {
     ncx = ncy = ncz = 1;
   } else {
-    // half-edge cells (edge >= r_c/2, search span 2): ncx, ncy >= 6 >= 2*2+1 here
-    const char* env = getenv("SLAB_SHORT_SPAN");  // tuning knob: 1 = cells of edge >= r_c
-    if (max_span >= 2 && !(env && env[0] == '1')) {
-      p.span = 2;
-      ncx = (int)(2.0 * lx / rc);
-      ncy = (int)(2.0 * ly / rc);
-      ncz = (int)(2.0 * lz / rc);
+    // cells of edge >= r_c / S searched over (2S+1)^2 columns: ncx, ncy >= 3S >=
+    // 2S+1 here.  SLAB_SHORT_SPAN (1..3) overrides the default for tuning.
+    const char* env = getenv("SLAB_SHORT_SPAN");
+    int S = kShortSpan;
+    if (env && env[0] >= '1' && env[0] <= '3') S = env[0] - '0';
+    S = S < max_span ? S : max_span;
+    if (S >= 2) {
+      p.span = S;
+      ncx = (int)(S * lx / rc);
+      ncy = (int)(S * ly / rc);
+      ncz = (int)(S * lz / rc);
       ncz = ncz < 1 ? 1 : ncz;
     }
   }
@@ -554,7 +572,11 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     // |r| <= 1e3; the exact fp64 test is applied to every survivor
     const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);
     const int64_t nblk = (nh + kSRThreads - 1) / kSRThreads;
-    if (p.span == 2)
+    if (p.span == 3)
+      nbr_build_kernel<3><<<(unsigned)nblk, kSRThreads, 0, st>>>(
+          cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
+          nn, maxnn, status);
+    else if (p.span == 2)
       nbr_build_kernel<2><<<(unsigned)nblk, kSRThreads, 0, st>>>(
           cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
@@ -563,7 +585,13 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
           cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
     const int64_t pgrid = pair_grid(nblk);
-    if (kind == 0)
+    // every pair has alpha d <= alpha r_c: below the table end -> branch-free form
+    const bool tab_only = alpha * sqrt(rc2) < 0.999 * SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W;
+    if (kind == 0 && tab_only)
+      pair_list_kernel<2><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
+          cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, alpha, rc2, 0.0, 0.0, forces, eblk, status,
+          accumulate);
+    else if (kind == 0)
       pair_list_kernel<0><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
           cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, alpha, rc2, 0.0, 0.0, forces, eblk, status,
           accumulate);

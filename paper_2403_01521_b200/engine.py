@@ -123,6 +123,38 @@ class Engine:
               "slab_evaluate")
         return energy, forces
 
+    def evaluate_host(self, pos, charge, box, alpha, r_c, soe, modes, commonv, charge_const,
+                      want_forces=True, skip_short_range=False):
+        """One evaluation on HOST arrays through ``slab_evaluate_host`` (uploads on
+        a side stream, charges overlapping the z sort; one synchronisation).
+        ``pos`` (n,3) / ``charge`` (n,) float64 numpy (page-locked memory copies at
+        DMA speed); ``modes`` a device (P,3) tensor or None; returns numpy
+        (energy (8,), forces (n,3) or None) backed by page-locked buffers."""
+        torch = _torch()
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        charge = np.ascontiguousarray(charge, dtype=np.float64)
+        n = charge.shape[0]
+        if pos.shape != (n, 3):
+            raise ValueError("pos must be (n, 3)")
+        e_h = torch.empty(8, dtype=torch.float64, pin_memory=True)
+        f_h = torch.empty((n, 3), dtype=torch.float64, pin_memory=True) if want_forces else None
+        pack = _SOEPack(soe)
+        P = 0 if modes is None else modes.shape[0]
+        cv_t = commonv if torch.is_tensor(commonv) else None
+        args = SlabEvalArgs(
+            n=n, box=SlabBox(box.lx, box.ly, box.lz, box.sigma_top, box.sigma_bot),
+            alpha=float(alpha), r_c=float(r_c), soe=pack.struct,
+            d_modes=_ptr(modes) if P else None, nmode=P, d_commonv=_ptr(cv_t),
+            commonv_scalar=0.0 if cv_t is not None else float(commonv),
+            charge_const=float(charge_const), want_forces=1 if want_forces else 0,
+            skip_short_range=1 if skip_short_range else 0, shard_rank=0, shard_count=1,
+            shard_mode=0, phase=0)
+        hp = ctypes.c_void_p
+        check(self.lib.slab_evaluate_host(
+            self.ctx, ctypes.byref(args), hp(pos.ctypes.data), hp(charge.ctypes.data),
+            _ptr(f_h), _ptr(e_h), self._stream()), "slab_evaluate_host")
+        return e_h.numpy(), (f_h.numpy() if f_h is not None else None)
+
     # -- sub-paths ----------------------------------------------------------
     def short_range(self, pos, charge, box, alpha, r_c):
         """Synchronous: (energy, forces, status), rerun once after a capacity overflow."""

@@ -183,7 +183,9 @@ def rb_energy_forces(system: ParticleSystem, box: BoxGeometry, params: EwaldPara
         H = normalization_H(alpha, box)
     if c_q is None:
         c_q = charge_term_sum(alpha, box, float(np.sum(system.charge ** 2)))
-    modes = sampler.batch(P)
+    # our ModeSampler hands its batch over on device (no host round trip); any
+    # other sampler object (a stub with a fixed k-set) through batch(P)
+    modes = sampler.batch_device(int(P)) if isinstance(sampler, ModeSampler) else sampler.batch(P)
     e, f = device_evaluate(system, box, alpha, params.r_c, soe, modes, _rb_commonv(H, P, alpha),
                            c_q)
     return _breakdown(e), f

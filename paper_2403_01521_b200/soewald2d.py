@@ -50,20 +50,26 @@ def _check_sorted(z):
 def device_evaluate(system: ParticleSystem, box: BoxGeometry, alpha: float, r_c: float,
                     soe: SOEApprox, modes, commonv, charge_const: float, want_forces=True,
                     skip_short_range=False):
-    """One ``slab_evaluate`` call on host arrays; returns (energy[8], forces or None)."""
-    from .engine import get_engine, host_result, to_device
+    """One ``slab_evaluate_host`` call on the host arrays (uploads, evaluation and
+    result download in one C call, one synchronisation); ``modes`` is a host
+    (P,3) array or a device tensor (the device sampler's batch).  Returns
+    (energy[8], forces or None)."""
+    import torch
+
+    from .engine import get_engine, to_device
     if not skip_short_range:
         check_short_range_cutoff(box, r_c)
     eng = get_engine()
-    pos = to_device(system.pos)
-    q = to_device(system.charge)
-    modes = np.asarray(modes, dtype=np.float64).reshape(-1, 3)
-    mt = to_device(modes) if modes.shape[0] else None
+    if torch.is_tensor(modes):
+        mt = modes if modes.shape[0] else None
+    else:
+        modes = np.asarray(modes, dtype=np.float64).reshape(-1, 3)
+        mt = to_device(modes) if modes.shape[0] else None
     cv = to_device(commonv) if isinstance(commonv, np.ndarray) else float(commonv)
     while True:
-        energy, forces = eng.evaluate(pos, q, box, alpha, r_c, soe, mt, cv, charge_const,
-                                      want_forces=want_forces, skip_short_range=skip_short_range)
-        e, f = host_result(energy, forces if want_forces else None)  # one sync, pinned D2H
+        e, f = eng.evaluate_host(system.pos, system.charge, box, alpha, r_c, soe, mt, cv,
+                                 charge_const, want_forces=want_forces,
+                                 skip_short_range=skip_short_range)
         if not eng.handle_overflow(int(e[5])):
             break
     raise_on_status(int(e[5]))  # includes the non-finite-z check done on device

@@ -84,6 +84,29 @@ def test_single_mode_and_full_sum_small(pk):
     _check(bd, f, e_ref, f_ref)
 
 
+@pytest.mark.parametrize("box_xy", [15.0, 11.0])
+def test_alpha_rc_beyond_erfcx_table(pk, box_xy):
+    """s = alpha r_c = 6.5: pair distances reach past the erfcx table's end
+    (x < 6), so the pair kernel keeps the libdevice arm (the branch-free form is
+    only taken when alpha r_c < 6); 15 x 15 runs the cell list, 11 x 11 the
+    all-pairs kernel."""
+    rng = np.random.default_rng(11)
+    box = pk.BoxGeometry(box_xy, box_xy, 6.0)
+    n = 700
+    s = pk.make_system(np.where(np.arange(n) % 2 == 0, 1.0, -1.0), np.ones(n),
+                       rng.uniform([0, 0, 0.2], [box_xy, box_xy, 5.8], size=(n, 3)), box)
+    alpha = 1.6
+    params = pk.make_ewald_params(alpha, 6.5, box)
+    assert params.alpha * params.r_c >= 6.0
+    soe = pk.build_soe_contour(8)
+    modes = pk.ModeSampler(alpha, box, seed=3).batch(5)
+    H = pk.normalization_H(alpha, box)
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 5, H=H, c_q=0.0)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
+                                (H / 5) * (2 / np.sqrt(np.pi)) * alpha, 0.0)
+    _check(bd, f, e_ref, f_ref)
+
+
 @pytest.fixture(scope="module")
 def big(pk):
     from paper_2403_01521_b200.configs import make_workload
