@@ -186,7 +186,10 @@ constexpr int kAggMaxWarps = SLAB_AGG_MMA_MAXW;
 #define SLAB_AGG_MMA_CB 1  // constant-bank polynomial coefficients in the main loop
 #endif
 template <int MH>
-__global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, 2) fourier_aggregate_mma_kernel(
+#ifndef SLAB_AGG_MINB
+#define SLAB_AGG_MINB 2
+#endif
+__global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier_aggregate_mma_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
     int tiles_per_cta, BVec b, double2* __restrict__ carry, int c0) {
