@@ -439,7 +439,11 @@ __global__ void __launch_bounds__(kSRThreads) nbr_cells_kernel(
 // thread: deterministic.
 // KIND 0: erfc Coulomb (alpha); KIND 2: the same with alpha r_c inside the erfcx table
 // (branch-free); KIND 1: WCA core (eps, sig2 = sigma^2).
-template <int KIND>
+// SPLIT > 1 (small systems, fewer homes than one resident wave of threads):
+// SPLIT consecutive lanes share a home, taking its row's 4-entry blocks round
+// robin, and combine their partial forces with a fixed xor-shuffle tree
+// (deterministic).
+template <int KIND, int SPLIT>
 __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     const double4* __restrict__ cp, const int32_t* __restrict__ order,
     const int32_t* __restrict__ nbr, const int32_t* __restrict__ nn, int64_t a_begin,
@@ -463,15 +467,21 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
       wca_accumulate<true>(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, lx, ly, ilx, ily, rc2, eps,    \
                            sig2, acc, flag);                                                  \
   } while (0)
-  // grid-stride over home particles: the smem erfcx fill is paid once per CTA
-  for (int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x; a < a_end;
-       a += (int64_t)gridDim.x * kSRThreads) {
-    const double4 pi = cp[a];
-    const int cnt = nn[a - a_begin];
-    const int32_t* row = nbr + (a - a_begin) * (int64_t)kcap;
+  // grid-stride over home particles (warp-uniform bound: the SPLIT lanes of a
+  // home shuffle together): the smem erfcx fill is paid once per CTA
+  const int sub = threadIdx.x % SPLIT;
+  constexpr int kHomesPerCta = kSRThreads / SPLIT;
+  const int64_t warp_first = (int64_t)(threadIdx.x & ~31) / SPLIT;
+  for (int64_t base = a_begin + blockIdx.x * (int64_t)kHomesPerCta; base + warp_first < a_end;
+       base += (int64_t)gridDim.x * kHomesPerCta) {
+    const int64_t a = base + threadIdx.x / SPLIT;
+    const bool active = a < a_end;
+    const double4 pi = active ? cp[a] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const int cnt = active ? nn[a - a_begin] : 0;
+    const int32_t* row = nbr + (active ? a - a_begin : 0) * (int64_t)kcap;
     acc.fx = acc.fy = acc.fz = 0.0;
-    int k = 0;
-    for (; k + 4 <= cnt; k += 4) {
+    int k = 4 * sub;
+    for (; k + 4 <= cnt; k += 4 * SPLIT) {
       const int4 j4 = *reinterpret_cast<const int4*>(row + k);
       const double4 p0 = cp[j4.x], p1 = cp[j4.y], p2 = cp[j4.z], p3 = cp[j4.w];
       PAIR(pi, p0);
@@ -479,19 +489,28 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
       PAIR(pi, p2);
       PAIR(pi, p3);
     }
-    for (; k < cnt; ++k) {
-      const double4 pj = cp[row[k]];
-      PAIR(pi, pj);
+    if (sub == 0)
+      for (k = cnt & ~3; k < cnt; ++k) {
+        const double4 pj = cp[row[k]];
+        PAIR(pi, pj);
+      }
+#pragma unroll
+    for (int o = 1; o < SPLIT; o <<= 1) {
+      acc.fx += __shfl_xor_sync(0xffffffffu, acc.fx, o);
+      acc.fy += __shfl_xor_sync(0xffffffffu, acc.fy, o);
+      acc.fz += __shfl_xor_sync(0xffffffffu, acc.fz, o);
     }
-    const int64_t i = order[a];
-    if (accumulate) {  // one thread owns particle i: += is race-free and deterministic
-      acc.fx += forces[3 * i + 0];
-      acc.fy += forces[3 * i + 1];
-      acc.fz += forces[3 * i + 2];
+    if (active && sub == 0) {
+      const int64_t i = order[a];
+      if (accumulate) {  // one thread owns particle i: += is race-free and deterministic
+        acc.fx += forces[3 * i + 0];
+        acc.fy += forces[3 * i + 1];
+        acc.fz += forces[3 * i + 2];
+      }
+      forces[3 * i + 0] = acc.fx;
+      forces[3 * i + 1] = acc.fy;
+      forces[3 * i + 2] = acc.fz;
     }
-    forces[3 * i + 0] = acc.fx;
-    forces[3 * i + 1] = acc.fy;
-    forces[3 * i + 2] = acc.fz;
   }
 #undef PAIR
   if (flag) atomicOr(status, SLAB_STATUS_COINCIDENT_DEV);
@@ -575,6 +594,46 @@ __global__ void __launch_bounds__(1024) half_sum_kernel(const double* __restrict
 
 // pair_list_kernel grid: one resident wave (5 CTAs per SM at 90 registers), grid-striding
 static int64_t pair_grid(int64_t blocks) { return blocks < 148 * 5 ? blocks : 148 * 5; }
+// lanes per home: fill one resident wave (148 SMs x 5 CTAs x 128 threads) when
+// there are fewer homes than that (cfg2, N = 1e4: 8 lanes per home)
+static int pair_split(int64_t nh) {
+  int s = 1;
+  while (s < 8 && nh * s < (int64_t)148 * 5 * kSRThreads) s *= 2;
+  return s;
+}
+
+template <int KIND>
+static void launch_pair_split(int split, unsigned grid, cudaStream_t st, const double4* cp,
+                              const int32_t* order, const int32_t* nbr, const int32_t* nn,
+                              int64_t h0, int64_t h1, int kcap, double lx, double ly,
+                              double alpha, double rc2, double eps, double sig2, double* forces,
+                              double* eblk, int* status, int accumulate) {
+#define SLAB_PAIR_LAUNCH(S)                                                                 \
+  pair_list_kernel<KIND, S><<<grid, kSRThreads, 0, st>>>(cp, order, nbr, nn, h0, h1, kcap, lx, \
+                                                         ly, alpha, rc2, eps, sig2, forces,   \
+                                                         eblk, status, accumulate)
+  if (split >= 8) SLAB_PAIR_LAUNCH(8);
+  else if (split == 4) SLAB_PAIR_LAUNCH(4);
+  else if (split == 2) SLAB_PAIR_LAUNCH(2);
+  else SLAB_PAIR_LAUNCH(1);
+#undef SLAB_PAIR_LAUNCH
+}
+
+static void launch_pair_list(int kind, int split, unsigned grid, cudaStream_t st,
+                             const double4* cp, const int32_t* order, const int32_t* nbr,
+                             const int32_t* nn, int64_t h0, int64_t h1, int kcap, double lx,
+                             double ly, double alpha, double rc2, double eps, double sig2,
+                             double* forces, double* eblk, int* status, int accumulate) {
+  if (kind == 2)
+    launch_pair_split<2>(split, grid, st, cp, order, nbr, nn, h0, h1, kcap, lx, ly, alpha, rc2,
+                         eps, sig2, forces, eblk, status, accumulate);
+  else if (kind == 0)
+    launch_pair_split<0>(split, grid, st, cp, order, nbr, nn, h0, h1, kcap, lx, ly, alpha, rc2,
+                         eps, sig2, forces, eblk, status, accumulate);
+  else
+    launch_pair_split<1>(split, grid, st, cp, order, nbr, nn, h0, h1, kcap, lx, ly, alpha, rc2,
+                         eps, sig2, forces, eblk, status, accumulate);
+}
 
 #ifndef SLAB_SHORT_SPAN_DEFAULT
 #define SLAB_SHORT_SPAN_DEFAULT 3  // cfg4: nbr_build 1.12 -> 1.02 ms (pair_list +0.04)
@@ -615,7 +674,7 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int 
   int js = (int)(592 / (nbx > 0 ? nbx : 1));
   p.jsplit = p.brute ? (js < 1 ? 1 : (js > 64 ? 64 : js)) : 1;
   p.nblk = p.brute ? (int64_t)p.jsplit * (nbx > 0 ? nbx : 1)
-                   : pair_grid((n + kSRThreads - 1) / kSRThreads);
+                   : (int64_t)148 * 5;  // pair_grid cap: any home count / split
   // neighbour-row capacity: 1.6x the mean-density sphere count + slack, rounded to
   // whole 32-byte sectors; grown by the caller after an overflow report
   const double dens = n / (lx * ly * lz);
@@ -738,21 +797,14 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
       nbr_build_kernel<1><<<(unsigned)nblk, kSRThreads, 0, st>>>(
           cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
-    const int64_t pgrid = pair_grid(nblk);
+    const int split = pair_split(nh);
+    const int64_t pgrid = pair_grid((nh * split + kSRThreads - 1) / kSRThreads);
     // every pair has alpha d <= alpha r_c: below the table end -> branch-free form
     const bool tab_only = alpha * sqrt(rc2) < 0.999 * SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W;
-    if (kind == 0 && tab_only)
-      pair_list_kernel<2><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
-          cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, alpha, rc2, 0.0, 0.0, forces, eblk, status,
-          accumulate);
-    else if (kind == 0)
-      pair_list_kernel<0><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
-          cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, alpha, rc2, 0.0, 0.0, forces, eblk, status,
-          accumulate);
-    else
-      pair_list_kernel<1><<<(unsigned)pgrid, kSRThreads, 0, st>>>(
-          cp, order, nbr, nn, h0, h1, p.kcap, lx, ly, 0.0, rc2, lj_eps, sig2, forces, eblk,
-          status, accumulate);
+    const int kk = kind == 0 ? (tab_only ? 2 : 0) : 1;
+    launch_pair_list(kk, split, (unsigned)pgrid, st, cp, order, nbr, nn, h0, h1, p.kcap, lx, ly,
+                     kind == 0 ? alpha : 0.0, rc2, kind == 0 ? 0.0 : lj_eps,
+                     kind == 0 ? 0.0 : sig2, forces, eblk, status, accumulate);
     half_sum_kernel<<<1, 1024, 0, st>>>(eblk, pgrid, energy_out);
   }
   return cudaGetLastError();

@@ -84,6 +84,27 @@ def test_single_mode_and_full_sum_small(pk):
     _check(bd, f, e_ref, f_ref)
 
 
+@pytest.mark.parametrize("n", [30000, 60000])
+def test_pair_row_split_sizes_match_oracle(pk, n):
+    """Home counts below one resident wave of threads split each neighbour row
+    over 4 (n = 3e4) or 2 (n = 6e4) lanes combined by a shuffle tree."""
+    rng = np.random.default_rng(n)
+    L = (2 * n / 0.1) ** (1 / 3)
+    box = pk.BoxGeometry(L, L, L / 2)
+    pos = rng.uniform([0, 0, 0.05], [L, L, L / 2 - 0.05], size=(n, 3))
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    s = pk.make_system(q, np.ones(n), pos, box)
+    alpha = 0.4
+    params = pk.make_ewald_params(alpha, 3.0, box)
+    soe = pk.build_soe_contour(8)
+    modes = pk.ModeSampler(alpha, box, seed=n).batch(5)
+    H = pk.normalization_H(alpha, box)
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 5, H=H, c_q=0.0)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
+                                (H / 5) * (2 / np.sqrt(np.pi)) * alpha, 0.0)
+    _check(bd, f, e_ref, f_ref)
+
+
 @pytest.mark.parametrize("box_xy", [15.0, 11.0])
 def test_alpha_rc_beyond_erfcx_table(pk, box_xy):
     """s = alpha r_c = 6.5: pair distances reach past the erfcx table's end
