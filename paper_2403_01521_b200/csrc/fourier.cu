@@ -456,6 +456,39 @@ __global__ void __launch_bounds__(128) fourier_carry_segscan_kernel(
   }
 }
 
+// The same scan with one THREAD per chain, segments in sequence: used when
+// there are few segments (nseg <= kSegSeqMax) and many chains (small systems,
+// full mode sums), where the warp form's per-lane segment rows are uncoalesced
+// (cfg1: 0.079 ms).  Consecutive chains are consecutive in each segment row.
+constexpr int kSegSeqMax = 64;
+__global__ void __launch_bounds__(128) fourier_carry_segscan_seq_kernel(
+    AffC* __restrict__ segmap, int items, int nc, int nseg, const double2* __restrict__ tin,
+    AffC* __restrict__ total, int mode) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // chain
+  if (e >= items * nc) return;
+  const size_t stride = (size_t)nc * items;
+  AffC* m = segmap + e;
+  AffC pre{C2{1.0, 0.0}, C2{0.0, 0.0}};
+  if (mode == 0 && tin) {
+    const double2 t2 = tin[e];
+    pre.X = C2{t2.x, t2.y};
+  }
+  constexpr int B = 4;
+  for (int s0 = 0; s0 < nseg; s0 += B) {
+    AffC cur[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (s0 + j < nseg) cur[j] = m[(size_t)(s0 + j) * stride];
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (s0 + j < nseg) {
+        if (mode == 0) m[(size_t)(s0 + j) * stride].X = pre.X;
+        pre = acompose(pre, cur[j]);
+      }
+  }
+  if (mode == 1) total[e] = pre;
+}
+
 __global__ void __launch_bounds__(32 * kCarrySegs) fourier_carry_rewrite_kernel(
     double2* __restrict__ carry, int nch, int c0, int c1, int P, int items, int mh, int nseg,
     const double* __restrict__ modetab, const double2* __restrict__ Df,
@@ -746,40 +779,74 @@ __global__ void __launch_bounds__(256) fourier_mode_energy_kernel(
 
 // Kahan over modes in mode order exactly like soewald2d.py:204-207, one thread
 // per segment of seg_len consecutive modes (one segment = the whole sum)
-__global__ void kahan_modes_kernel(const double* __restrict__ se, int nseg, int seg_len,
-                                   double* __restrict__ out) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
+// Compensated sum of each segment of per-mode energies: one block per segment,
+// each thread a Kahan sum over a strided subset, then a fixed-order tree of
+// (sum, error) pairs combined with TwoSum -- deterministic, and as accurate as
+// the reference's sequential Kahan loop (a single thread walking 792 modes of
+// the cfg1 full sum in sequence took 0.029 ms).
+constexpr int kKahanThreads = 128;
+__device__ __forceinline__ void two_sum_acc(double& s, double& e, double s2, double e2) {
+  const double t = s + s2;
+  const double bp = t - s;
+  const double err = (s - (t - bp)) + (s2 - bp);
+  s = t;
+  e = e + e2 + err;
+}
+__global__ void __launch_bounds__(kKahanThreads) kahan_modes_kernel(
+    const double* __restrict__ se, int nseg, int seg_len, double* __restrict__ out) {
+  __shared__ double rs[kKahanThreads], re[kKahanThreads];
+  const int s = blockIdx.x;
   double u = 0.0, comp = 0.0;
-  for (int t = s * seg_len; t < (s + 1) * seg_len; ++t) {
-    const double y = se[t] - comp;
+  for (int t = threadIdx.x; t < seg_len; t += kKahanThreads) {
+    const double y = se[(size_t)s * seg_len + t] - comp;
     const double tt = u + y;
     comp = (tt - u) - y;
     u = tt;
   }
-  out[s] = u;
+  rs[threadIdx.x] = u;
+  re[threadIdx.x] = -comp;
+  __syncthreads();
+  for (int w = kKahanThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      double a = rs[threadIdx.x], b = re[threadIdx.x];
+      two_sum_acc(a, b, rs[threadIdx.x + w], re[threadIdx.x + w]);
+      rs[threadIdx.x] = a;
+      re[threadIdx.x] = b;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[s] = rs[0] + re[0];
 }
 
 // forces_sorted += sum of the per-warp partial buffers (fixed order)
 // Buffer b < ngroups * nwarps belongs to warp b % nwarps of item group
 // b / nwarps and is written only if that warp holds items; buffer
 // ngroups * nwarps (when nbuf exceeds the grid) is the mixed warp's backward one.
+// NS > 1 (few particles, many buffers: small systems with full mode sums): NS
+// lanes per element take the buffers round robin and combine by a fixed
+// xor-shuffle tree (deterministic).
+template <int NS>
 __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int nbuf,
                                             int ngroups, int nwarps, int ipg, int nitems,
                                             int64_t n3, double* __restrict__ out, int64_t e0,
                                             int64_t e1) {
-  int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= e1) return;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int sub = (int)(t % NS);
+  const int64_t e = e0 + t / NS;
+  const bool live = e < e1;
   double v = 0.0;
-  for (int b = 0; b < nbuf; ++b) {
-    if (b < ngroups * nwarps) {
-      const int g = b / nwarps, w = b - g * nwarps;
-      const int cnt = min(nitems, (g + 1) * ipg) - g * ipg;
-      if (32 * w >= cnt) continue;
+  if (live)
+    for (int b = sub; b < nbuf; b += NS) {
+      if (b < ngroups * nwarps) {
+        const int g = b / nwarps, w = b - g * nwarps;
+        const int cnt = min(nitems, (g + 1) * ipg) - g * ipg;
+        if (32 * w >= cnt) continue;
+      }
+      v += fpart[(size_t)b * n3 + e];
     }
-    v += fpart[(size_t)b * n3 + e];
-  }
-  out[e] += v;
+#pragma unroll
+  for (int o = 1; o < NS; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (live && sub == 0) out[e] += v;
 }
 
 // ---------------------------------------------------------------------------
@@ -929,9 +996,14 @@ static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const d
         w.dchunk + (size_t)p.nch * MH, w.zbound, reinterpret_cast<AffC*>(w.segmap));
     if (totals) {
       const int nchain = p.items * ncomp_of(MH);
-      fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(
-          reinterpret_cast<AffC*>(w.segmap), p.items, ncomp_of(MH), nseg, nullptr,
-          reinterpret_cast<AffC*>(totals), 1);
+      if (nseg <= kSegSeqMax)
+        fourier_carry_segscan_seq_kernel<<<(nchain + 127) / 128, 128, 0, st>>>(
+            reinterpret_cast<AffC*>(w.segmap), p.items, ncomp_of(MH), nseg, nullptr,
+            reinterpret_cast<AffC*>(totals), 1);
+      else
+        fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(
+            reinterpret_cast<AffC*>(w.segmap), p.items, ncomp_of(MH), nseg, nullptr,
+            reinterpret_cast<AffC*>(totals), 1);
     }
   } else {
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
@@ -955,8 +1027,12 @@ static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const d
     const int nseg = cg.z * kCarrySegs;
     const int nchain = p.items * ncomp_of(MH);
     AffC* segmap = reinterpret_cast<AffC*>(w.segmap);
-    fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(segmap, p.items, ncomp_of(MH),
-                                                                  nseg, tin, nullptr, 0);
+    if (nseg <= kSegSeqMax)
+      fourier_carry_segscan_seq_kernel<<<(nchain + 127) / 128, 128, 0, st>>>(
+          segmap, p.items, ncomp_of(MH), nseg, tin, nullptr, 0);
+    else
+      fourier_carry_segscan_kernel<<<(nchain + 3) / 4, 128, 0, st>>>(
+          segmap, p.items, ncomp_of(MH), nseg, tin, nullptr, 0);
     fourier_carry_rewrite_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
         w.carry, p.nch, p.c0, p.c1, p.P, p.items, MH, nseg, w.modetab, w.dchunk,
         w.dchunk + (size_t)p.nch * MH, w.zbound, segmap);
@@ -1019,15 +1095,20 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
   double* se = w.epart + (size_t)p.nch * p.P;  // P scratch doubles after the partials
   fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.c0, p.c1, p.P, p.mh, w.modetab, se);
   const int nseg = p.P / seg_len;
-  kahan_modes_kernel<<<(nseg + 127) / 128, 128, 0, st>>>(se, nseg, seg_len, energy_out);
+  if (nseg > 0) kahan_modes_kernel<<<nseg, kKahanThreads, 0, st>>>(se, nseg, seg_len, energy_out);
   if (want_forces) {
     const int64_t n3 = p.n * 3;
     const int64_t e0 = (int64_t)p.c0 * p.R * 3;
     int64_t e1 = (int64_t)p.c1 * p.R * 3;
     e1 = e1 < n3 ? e1 : n3;
-    if (e1 > e0)
-      fourier_force_reduce_kernel<<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
-          w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
+    if (e1 > e0) {
+      if ((e1 - e0) < (int64_t)148 * 2048 && p.nbuf >= 16)
+        fourier_force_reduce_kernel<8><<<(unsigned)((8 * (e1 - e0) + 255) / 256), 256, 0, st>>>(
+            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
+      else
+        fourier_force_reduce_kernel<1><<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
+            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
+    }
   }
   return cudaGetLastError();
 }
