@@ -50,6 +50,11 @@ struct SlabCtx {
   int64_t h_cap = -1;
   cudaStream_t up_stream = nullptr;
   cudaEvent_t ev_pos = nullptr, ev_q = nullptr;
+  // evaluation fork: the Fourier / k = 0 chain on a high-priority stream, the
+  // short range on a low-priority one (its CTAs fill the SMs the scan's small
+  // and tail kernels leave idle); joined back into the caller's stream
+  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_short = nullptr, ev_long = nullptr, ev_x = nullptr;
 };
 
 namespace {
@@ -208,6 +213,10 @@ int slab_ctx_destroy(SlabCtx* ctx) {
   if (ctx->h_dforces) cudaFree(ctx->h_dforces);
   if (ctx->h_denergy) cudaFree(ctx->h_denergy);
   if (ctx->up_stream) cudaStreamDestroy(ctx->up_stream);
+  if (ctx->hi) cudaStreamDestroy(ctx->hi);
+  if (ctx->lo) cudaStreamDestroy(ctx->lo);
+  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_short, ctx->ev_long, ctx->ev_x})
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_pos) cudaEventDestroy(ctx->ev_pos);
   if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
   delete ctx;
@@ -527,6 +536,26 @@ static int64_t home_bound(int64_t n, int r, int W) {
 static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
                          cudaEvent_t pos_ready, cudaEvent_t charge_ready);
 
+// Concurrent short range up to this many particles (cfg3, N = 1e5: 3.30 ->
+// 3.07 ms).  Beyond it both halves fill the GPU on their own: at N = 1e6 the
+// overlap bought 1.6% while stretching the scan kernels' measured span (its
+// roofline figure) by 45% as the short range's CTAs shared their SMs.
+#ifndef SLAB_FORK_MAX_N
+#define SLAB_FORK_MAX_N 400000
+#endif
+constexpr int64_t kForkMaxN = SLAB_FORK_MAX_N;
+
+static int ensure_fork(SlabCtx* ctx) {
+  if (ctx->hi) return SLAB_OK;
+  int least = 0, greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  CK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
+  CK(cudaStreamCreateWithPriority(&ctx->lo, cudaStreamNonBlocking, least));
+  for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_short, &ctx->ev_long, &ctx->ev_x})
+    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return SLAB_OK;
+}
+
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (!ctx || !a) return fail(SLAB_ERR_ARG, "null context or arguments");
   return evaluate_impl(ctx, a, (cudaStream_t)stream, nullptr, nullptr);
@@ -646,37 +675,66 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   const bool lead = srank == 0;  // the rank that owns the k = 0 mode and the constants
   int32_t* perm = nullptr;
 
+  // Fork: the short range runs on ctx->lo (lowest priority) concurrently with
+  // the sort / Fourier / k = 0 chain on ctx->hi (highest priority); both join
+  // back into `st` before the assembly.  (A z-split phase 1 returns with the
+  // short range possibly still running; phase 2 joins it.)
+  const bool fork = !a->skip_short_range && n > 0 && n <= kForkMaxN;
+  if (fork) {
+    rc = ensure_fork(ctx);
+    if (rc) return rc;
+  }
+  cudaStream_t sl = fork ? ctx->hi : st;  // the long (scan) chain's stream
   if (a->phase != 2) {  // ---- sort, short range, aggregates
     CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
     CK(cudaMemsetAsync(ctx->small, 0, 8 * sizeof(double), st));
     CK(cudaMemsetAsync(ctx->d_maxnn, 0, sizeof(int), st));
-    if (pos_ready) CK(cudaStreamWaitEvent(st, pos_ready, 0));
-    if (n > 0) {
-      CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, st, &perm, ctx->status));
-      if (charge_ready) CK(cudaStreamWaitEvent(st, charge_ready, 0));
-      CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm,
-                             st));
+    if (fork) {
+      CK(cudaEventRecord(ctx->ev_fork, st));
+      CK(cudaStreamWaitEvent(ctx->hi, ctx->ev_fork, 0));
+      CK(cudaStreamWaitEvent(ctx->lo, ctx->ev_fork, 0));
     }
-    ctx->zs_perm = perm;
     if (!a->skip_short_range) {
+      cudaStream_t ss = fork ? ctx->lo : st;
+      if (pos_ready) CK(cudaStreamWaitEvent(ss, pos_ready, 0));
+      if (charge_ready) CK(cudaStreamWaitEvent(ss, charge_ready, 0));
       const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
       CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
-                         a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, st));
+                         a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, ss));
+      if (fork) CK(cudaEventRecord(ctx->ev_short, ctx->lo));
     }
-    if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, st));
+    if (pos_ready) CK(cudaStreamWaitEvent(sl, pos_ready, 0));
+    if (n > 0) {
+      CK(slab::sort_by_z_device(a->d_pos + 2, 3, n, w.sw, sl, &perm, ctx->status));
+      if (charge_ready) CK(cudaStreamWaitEvent(sl, charge_ready, 0));
+      CK(slab::gather_sorted(a->d_pos, a->d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, a->d_perm,
+                             sl));
+    }
+    ctx->zs_perm = perm;
+    if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, sl));
     if (n >= 2) {
-      CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
-      if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, st));
+      CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, sl));
+      if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, sl));
       if (a->nmode > 0)
         CK(slab::fourier_phase1(fp, fw, w.xs, w.ys, w.zs, w.qs, a->d_modes, a->d_commonv,
                                 a->commonv_scalar, area, sh.b, sh.w, ctx->status,
-                                a->phase == 1 ? a->d_xchg : nullptr, st));
+                                a->phase == 1 ? a->d_xchg : nullptr, sl));
     } else if (forces) {
-      CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * N, st));
+      CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * N, sl));
     }
-    if (a->phase == 1) return SLAB_OK;
+    if (a->phase == 1) {  // the exchange payload is read on `st` by the caller
+      if (fork) {
+        CK(cudaEventRecord(ctx->ev_long, sl));
+        CK(cudaStreamWaitEvent(st, ctx->ev_long, 0));
+      }
+      return SLAB_OK;
+    }
   } else {
     perm = ctx->zs_perm;
+    if (fork) {  // the gathered exchange was written on `st`
+      CK(cudaEventRecord(ctx->ev_x, st));
+      CK(cudaStreamWaitEvent(sl, ctx->ev_x, 0));
+    }
   }
 
   // ---- carried-in states, sweep, k = 0 mode, assembly
@@ -684,17 +742,22 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     if (a->nmode > 0) {
       const double* tin = nullptr;
       if (a->phase == 2) {
-        CK(slab::fourier_zsplit_tin(fp, a->d_xchg, scount, srank, fw.tin, st));
+        CK(slab::fourier_zsplit_tin(fp, a->d_xchg, scount, srank, fw.tin, sl));
         tin = fw.tin;
       }
       CK(slab::fourier_phase2(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, sh.b, forces ? 1 : 0,
-                              u_sweep, w.fsorted, tin, st));
+                              u_sweep, w.fsorted, tin, sl));
     }
     if (lead)
       CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
-                          w.fzf, w.fzb, u_pair, st));
+                          w.fzf, w.fzb, u_pair, sl));
   }
-  if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, st));
+  if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, sl));
+  if (fork) {  // join
+    CK(cudaEventRecord(ctx->ev_long, sl));
+    CK(cudaStreamWaitEvent(st, ctx->ev_long, 0));
+    CK(cudaStreamWaitEvent(st, ctx->ev_short, 0));
+  }
   if (forces) {
     const double plane = lead ? box.sigma_top - box.sigma_bot : 0.0;
     CK(slab::assemble_forces(n, perm, w.qs, w.fsorted, (n >= 2 && lead) ? w.fzf : nullptr, w.fzb,
