@@ -53,8 +53,9 @@ struct SlabCtx {
   // evaluation fork: the Fourier / k = 0 chain on a high-priority stream, the
   // short range on a low-priority one (its CTAs fill the SMs the scan's small
   // and tail kernels leave idle); joined back into the caller's stream
-  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaStream_t hi = nullptr, lo = nullptr, aux = nullptr;  // aux: the k = 0 chain
   cudaEvent_t ev_fork = nullptr, ev_short = nullptr, ev_long = nullptr, ev_x = nullptr;
+  cudaEvent_t ev_dtab = nullptr, ev_zero = nullptr;
 };
 
 namespace {
@@ -215,7 +216,9 @@ int slab_ctx_destroy(SlabCtx* ctx) {
   if (ctx->up_stream) cudaStreamDestroy(ctx->up_stream);
   if (ctx->hi) cudaStreamDestroy(ctx->hi);
   if (ctx->lo) cudaStreamDestroy(ctx->lo);
-  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_short, ctx->ev_long, ctx->ev_x})
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_short, ctx->ev_long, ctx->ev_x, ctx->ev_dtab,
+                        ctx->ev_zero})
     if (e) cudaEventDestroy(e);
   if (ctx->ev_pos) cudaEventDestroy(ctx->ev_pos);
   if (ctx->ev_q) cudaEventDestroy(ctx->ev_q);
@@ -544,6 +547,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
 #define SLAB_FORK_MAX_N 400000
 #endif
 constexpr int64_t kForkMaxN = SLAB_FORK_MAX_N;
+#ifndef SLAB_PAR_ZERO
+#define SLAB_PAR_ZERO 1
+#endif
+constexpr bool kParZero = SLAB_PAR_ZERO;
 
 static int ensure_fork(SlabCtx* ctx) {
   if (ctx->hi) return SLAB_OK;
@@ -551,7 +558,9 @@ static int ensure_fork(SlabCtx* ctx) {
   CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
   CK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
   CK(cudaStreamCreateWithPriority(&ctx->lo, cudaStreamNonBlocking, least));
-  for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_short, &ctx->ev_long, &ctx->ev_x})
+  CK(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, greatest));
+  for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_short, &ctx->ev_long, &ctx->ev_x,
+                         &ctx->ev_dtab, &ctx->ev_zero})
     CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   return SLAB_OK;
 }
@@ -680,7 +689,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   // back into `st` before the assembly.  (A z-split phase 1 returns with the
   // short range possibly still running; phase 2 joins it.)
   const bool fork = !a->skip_short_range && n > 0 && n <= kForkMaxN;
-  if (fork) {
+  // the k = 0 chain (aggregate, carry, sweep: low-occupancy kernels) runs on
+  // ctx->aux beside the Fourier chain once the decay table exists
+  const bool par_zero = kParZero && a->phase == 0 && n >= 2 && lead;
+  if (fork || par_zero) {
     rc = ensure_fork(ctx);
     if (rc) return rc;
   }
@@ -714,6 +726,13 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, sl));
     if (n >= 2) {
       CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, sl));
+      if (par_zero) {
+        CK(cudaEventRecord(ctx->ev_dtab, sl));
+        CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_dtab, 0));
+        CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha,
+                            forces ? 1 : 0, w.fzf, w.fzb, u_pair, ctx->aux));
+        CK(cudaEventRecord(ctx->ev_zero, ctx->aux));
+      }
       if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, sl));
       if (a->nmode > 0)
         CK(slab::fourier_phase1(fp, fw, w.xs, w.ys, w.zs, w.qs, a->d_modes, a->d_commonv,
@@ -748,9 +767,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
       CK(slab::fourier_phase2(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, sh.b, forces ? 1 : 0,
                               u_sweep, w.fsorted, tin, sl));
     }
-    if (lead)
+    if (lead && !par_zero)
       CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
                           w.fzf, w.fzb, u_pair, sl));
+    if (par_zero) CK(cudaStreamWaitEvent(sl, ctx->ev_zero, 0));
   }
   if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, sl));
   if (fork) {  // join
