@@ -725,7 +725,11 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     ctx->zs_perm = perm;
     if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, sl));
     if (n >= 2) {
-      CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, sl));
+      if (zsplit && !lead)  // rows of this rank's chunk range only (no k = 0 mode here)
+        CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, sl, (int64_t)fp.c0 * fp.R,
+                             std::min<int64_t>(n, (int64_t)fp.c1 * fp.R)));
+      else
+        CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, sl));
       if (par_zero) {
         CK(cudaEventRecord(ctx->ev_dtab, sl));
         CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_dtab, 0));

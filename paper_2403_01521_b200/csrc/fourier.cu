@@ -57,9 +57,9 @@ __host__ __device__ inline int ncomp_of(int mh) { return 2 * mh + 1; }
 // ---------------------------------------------------------------------------
 // dtab[a*mh + l] = exp(-b_l (z_a - z_{a-1})), row 0 = 1, row n = 0 (backward guard)
 __global__ void decay_table_kernel(const double* __restrict__ zs, int64_t n, int mh, BVec b,
-                                   double2* __restrict__ dtab) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= (n + 1) * mh) return;
+                                   double2* __restrict__ dtab, int64_t a_lo, int64_t a_hi) {
+  int64_t e = a_lo * mh + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (a_hi + 1) * mh) return;
   int64_t a = e / mh;
   int l = (int)(e - a * mh);
   double2 d;
@@ -948,9 +948,13 @@ void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w) {
 }
 
 cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, double2* dtab,
-                        cudaStream_t st) {
-  const int64_t tot = (n + 1) * mh;
-  decay_table_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(zs, n, mh, b, dtab);
+                        cudaStream_t st, int64_t a_lo, int64_t a_hi) {
+  if (a_hi < 0 || a_hi > n) a_hi = n;
+  if (a_lo < 0) a_lo = 0;
+  if (a_lo > a_hi) return cudaGetLastError();
+  const int64_t tot = (a_hi - a_lo + 1) * mh;
+  decay_table_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(zs, n, mh, b, dtab, a_lo,
+                                                                     a_hi);
   return cudaGetLastError();
 }
 

@@ -70,8 +70,10 @@ struct FourierWork {
 };
 size_t fourier_work_doubles(const FourierPlan& p);
 void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w);
+// rows [a_lo, a_hi] of the (n + 1)-row table (default: all; a z-split rank
+// without the k = 0 mode needs only its chunk range's rows)
 cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, double2* dtab,
-                        cudaStream_t st);
+                        cudaStream_t st, int64_t a_lo = 0, int64_t a_hi = -1);
 cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double* xs,
                         const double* ys, const double* zs, const double* qs,
                         const double2* dtab, const double* modes, const double* commonv,
