@@ -173,14 +173,39 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
       : "d"(a), "d"(b));
 }
 
-__host__ __device__ constexpr int mma_mhp(int mh) { return (mh + 3) / 4 * 4; }
-static size_t agg_mma_smem(int R, int mh) {
-  return sizeof(double) * ((size_t)4 * mma_mhp(mh) * (R + 4) + 4 * (size_t)R);
-}
-
 #ifndef SLAB_AGG_MMA_MAXW
 #define SLAB_AGG_MMA_MAXW 13  // m-tiles (warps) per CTA: P <= 104 in one CTA per chunk
 #endif
+__host__ __device__ constexpr int mma_mhp(int mh) { return (mh + 3) / 4 * 4; }
+static size_t agg_mma_smem(int R, int mh) {
+  return sizeof(double) * ((size_t)4 * mma_mhp(mh) * (R + 4) + 4 * (size_t)R +
+                           3 * 32 * (size_t)SLAB_AGG_MMA_MAXW);
+}
+
+#ifndef SLAB_AGG_RCP
+#define SLAB_AGG_RCP 1
+#endif
+constexpr bool kAggRcp = SLAB_AGG_RCP;
+// 1/x for a normal, finite x > 0 without the IEEE division's special-case
+// branch: the hardware estimate refined by two Newton steps (~1 ulp)
+__device__ __forceinline__ double rcp_normal(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// a per-lane constant re-read from shared memory at every use (volatile: kept
+// out of the register file of the 72-register aggregate, which spilled its
+// accumulators around the transcendentals)
+__device__ __forceinline__ double lds_volatile(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 constexpr int kAggMaxWarps = SLAB_AGG_MMA_MAXW;
 #ifndef SLAB_AGG_MMA_CB
 #define SLAB_AGG_MMA_CB 1  // constant-bank polynomial coefficients in the main loop
@@ -201,8 +226,9 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
   double* wt = reinterpret_cast<double*>(smem4);  // [NCOL][RP]
   double* sx = wt + (size_t)NCOL * RP;
   double* sy = sx + R;
-  double* sz = sy + R;
+  double* sz = sy + R;  // z_end - z_j
   double* sq = sz + R;
+  double* sk = sq + R;   // per-lane (kx, ky, k): [3][blockDim]
   const int c = c0 + blockIdx.x;
   const int64_t a0 = (int64_t)c * R;
   const int len = (int)(a0 + R < n ? R : n - a0);
@@ -210,7 +236,7 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
   for (int i = threadIdx.x; i < len; i += blockDim.x) {
     sx[i] = xs[a0 + i];
     sy[i] = ys[a0 + i];
-    sz[i] = zs[a0 + i];
+    sz[i] = z_end - zs[a0 + i];
     sq[i] = qs[a0 + i];
   }
   // weights, column (dir * MHP + l) * 2 + e
@@ -240,7 +266,11 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
   const int t = tile * 8 + nn;
   const bool tv = t < P;
   const double* mt = modetab + (size_t)(tv ? t : 0) * mode_stride(MH);
-  const double kx = mt[0], ky = mt[1], k = mt[2];
+  const double k = mt[2];
+  sk[threadIdx.x] = mt[0];
+  sk[blockDim.x + threadIdx.x] = mt[1];
+  sk[2 * blockDim.x + threadIdx.x] = k;
+  __syncwarp();
   double acc[2][NT][2];
 #pragma unroll
   for (int s = 0; s < 2; ++s)
@@ -248,24 +278,34 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
     for (int u = 0; u < NT; ++u) acc[s][u][0] = acc[s][u][1] = 0.0;
   double gfr = 0.0, gfi = 0.0, gbr = 0.0, gbi = 0.0;
   const double* wk = wt + nn * RP + kk;
-  const bool span_ok = k * (z_end - z_start) < 600.0;
-  const double ekspan = exp_neg(k * (z_end - z_start));
+  const double span = z_end - z_start;
+  const bool span_ok = k * span < 600.0;
+  const double ekspan = exp_neg(k * span);
+  const double* skl = sk + threadIdx.x;
   for (int k0 = 0; k0 < len; k0 += 4) {
     const int j = k0 + kk;
     double ur = 0.0, ui = 0.0;
     if (tv && j < len) {
-      const double th = __dadd_rn(__dmul_rn(kx, sx[j]), __dmul_rn(ky, sy[j]));
+      const double th = __dadd_rn(__dmul_rn(lds_volatile(skl), sx[j]),
+                                  __dmul_rn(lds_volatile(skl + blockDim.x), sy[j]));
       double sn, cs;
-      const double q = sq[j], z = sz[j];
+      const double q = sq[j], ze = sz[j];  // ze = z_end - z_j
+      const double kj = lds_volatile(skl + 2 * blockDim.x);
 #if SLAB_AGG_MMA_CB
       sincos_fast_cb(th, &sn, &cs);
       // e^{-k (z - z_start)} = e^{-k (z_end - z_start)} / e^{-k (z_end - z)} (one exp
       // and a reciprocal instead of two exps) while both factors stay normal
-      const double wf = exp_neg_cb(k * (z_end - z));
-      const double wb = span_ok ? ekspan / wf : exp_neg_cb(k * (z - z_start));
+      const double wf = exp_neg_cb(kj * ze);
+      // (Newton reciprocal vs IEEE division: register allocation decides --
+      // measured 1.18 -> 1.10 ms for 8 pairs, 0.36 -> 0.39 ms for 12)
+      double wb;
+      if constexpr (kAggRcp && MH <= 8)
+        wb = span_ok ? ekspan * rcp_normal(wf) : exp_neg_cb(kj * (span - ze));
+      else
+        wb = span_ok ? ekspan / wf : exp_neg_cb(kj * (span - ze));
 #else
       sincos_fast(th, &sn, &cs);
-      const double wf = exp_neg(k * (z_end - z)), wb = exp_neg(k * (z - z_start));
+      const double wf = exp_neg(kj * ze), wb = exp_neg(kj * (span - ze));
 #endif
       ur = q * cs;
       ui = -q * sn;
