@@ -342,6 +342,49 @@ def test_nonfinite_z_rejected_by_device_status(pk, bad):
     pk.soe_energy_forces(good, box, params, soe8)
 
 
+def test_device_sampler_handover_and_host_buffers(pk):
+    """rb_energy_forces with a ModeSampler takes the k-set on device
+    (batch_device) and evaluates through slab_evaluate_host; a twin sampler's
+    host batch(P) through the stub path and the device-buffer evaluate agree,
+    for pageable and page-locked inputs, and the chain state advances alike."""
+    from paper_2403_01521_b200.engine import pinned_like
+    box = pk.BoxGeometry(14.0, 14.0, 7.0)
+    s = _slab_system(pk, 3000, box, 5)
+    params = pk.make_ewald_params(0.7, 3.0, box)
+    soe8 = pk.build_soe_contour(8)
+    H = pk.normalization_H(0.7, box)
+    a, b = pk.ModeSampler(0.7, box, seed=9), pk.ModeSampler(0.7, box, seed=9)
+
+    class Stub:
+        def __init__(self, m):
+            self.m = m
+
+        def batch(self, P):
+            return self.m
+
+    for pinned in (False, True):
+        sys_ = s
+        if pinned:
+            sys_ = pk.make_system(s.charge, s.mass, s.pos, box)
+            sys_.pos, sys_.charge = pinned_like(s.pos), pinned_like(s.charge)
+        bd1, f1 = pk.rb_energy_forces(sys_, box, params, soe8, a, 12, H=H, c_q=0.0)
+        modes = b.batch(12)
+        bd2, f2 = pk.rb_energy_forces(s, box, params, soe8, Stub(modes), 12, H=H, c_q=0.0)
+        assert bd1.total == pytest.approx(bd2.total, rel=1e-12, abs=1e-12)
+        np.testing.assert_allclose(f1, f2, rtol=0, atol=1e-12 * np.max(np.abs(f2)))
+    assert a.accepted == b.accepted and a.steps == b.steps
+    # the device-buffer entry (slab_evaluate) on the same k-set
+    from paper_2403_01521_b200.engine import get_engine, to_device
+    eng = get_engine()
+    cv = (H / 12) * (2 / np.sqrt(np.pi)) * 0.7
+    e_d, f_d = eng.evaluate(to_device(s.pos), to_device(s.charge), box, 0.7, params.r_c, soe8,
+                            to_device(modes), cv, 0.0)
+    e_d = e_d.cpu().numpy()
+    assert float(e_d[0] + e_d[1] + e_d[2] - e_d[3] + e_d[4]) == pytest.approx(bd2.total,
+                                                                            rel=1e-12)
+    np.testing.assert_array_equal(f_d.cpu().numpy(), f2)
+
+
 # --------------------------------------------------------------- device evaluator
 def test_graph_replay_and_shard_sum_equal_single_eval(pk):
     import torch
