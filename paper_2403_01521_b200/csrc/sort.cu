@@ -17,8 +17,12 @@
 namespace slab {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per tile
+constexpr int kSortItems = 16;  // 4096 keys per tile
+// small inputs: 4 keys per thread (1024 per tile): 4x the tiles and a quarter of
+// the per-tile rounds, for the latency-bound passes of a few-tile sort
+constexpr int kSortItemsSmall = 4;
+constexpr int64_t kSortSmallN = 1 << 18;
+static int sort_items(int64_t n) { return n < kSortSmallN ? kSortItemsSmall : kSortItems; }
 
 __global__ void zkey_init_kernel(const double* __restrict__ z, int64_t stride, int64_t n,
                                  uint64_t* __restrict__ keys, int32_t* __restrict__ idx,
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(256) radix_digit_bases_kernel(const uint32_t* 
   bases[ps * 256 + d] = s[d] - counts[ps * 256 + d];
 }
 
-template <typename K>
+template <typename K, int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(
     const K* __restrict__ kin, const int32_t* __restrict__ vin, K* __restrict__ kout,
     int32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ bases,
@@ -98,10 +102,10 @@ __global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(
   tcnt[tid] = 0u;
   __syncthreads();
   const int tile = tile_s;
-  const int64_t tile0 = (int64_t)tile * kSortTile;
-  K keys[kSortItems];
+  const int64_t tile0 = (int64_t)tile * (kSortThreads * ITEMS);
+  K keys[ITEMS];
 #pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     const int64_t p = tile0 + r * kSortThreads + tid;
     keys[r] = p < n ? kin[p] : K(0);
     if (p < n) atomicAdd(&tcnt[(unsigned)(keys[r] >> shift) & 255u], 1u);
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(
   }
   const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
 #pragma unroll
     for (int w = 0; w < kSortThreads / 32; ++w) wcnt[w][tid] = 0;
     __syncthreads();
@@ -189,7 +193,9 @@ template <typename K>
 cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_alt,
                              int32_t* hist, int64_t n, int key_bits, cudaStream_t st,
                              K** keys_out, int32_t** vals_out) {
-  const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+  const int items = sort_items(n);
+  const int tile_keys = kSortThreads * items;
+  const int ntiles = (int)((n + tile_keys - 1) / tile_keys);
   const int passes = (key_bits + 7) / 8;
   K *ki = keys, *ko = keys_alt;
   int32_t *vi = vals, *vo = vals_alt;
@@ -208,9 +214,14 @@ cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_
     radix_digit_counts_kernel<K><<<grid, kSortThreads, 0, st>>>(ki, n, passes, counts);
     radix_digit_bases_kernel<<<passes, 256, 0, st>>>(counts, bases);
     for (int ps = 0; ps < passes; ++ps) {
-      radix_onesweep_kernel<K><<<ntiles, kSortThreads, 0, st>>>(
-          ki, vi, ko, vo, n, 8 * ps, bases + ps * 256, look + (size_t)ps * ntiles * 256,
-          tctr + ps);
+      if (items == kSortItems)
+        radix_onesweep_kernel<K, kSortItems><<<ntiles, kSortThreads, 0, st>>>(
+            ki, vi, ko, vo, n, 8 * ps, bases + ps * 256, look + (size_t)ps * ntiles * 256,
+            tctr + ps);
+      else
+        radix_onesweep_kernel<K, kSortItemsSmall><<<ntiles, kSortThreads, 0, st>>>(
+            ki, vi, ko, vo, n, 8 * ps, bases + ps * 256, look + (size_t)ps * ntiles * 256,
+            tctr + ps);
       K* tk = ki; ki = ko; ko = tk;
       int32_t* tv = vi; vi = vo; vo = tv;
     }
@@ -221,7 +232,8 @@ cudaError_t radix_sort_pairs(K* keys, int32_t* vals, K* keys_alt, int32_t* vals_
 }
 
 int64_t radix_hist_entries(int64_t n) {
-  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  const int64_t tile_keys = (int64_t)kSortThreads * sort_items(n);
+  const int64_t ntiles = (n + tile_keys - 1) / tile_keys;
   return (int64_t)kMaxPasses * 256 * 2 + 64 + (int64_t)kMaxPasses * (ntiles > 0 ? ntiles : 1) * 256;
 }
 
