@@ -21,7 +21,10 @@ constexpr int kSortItems = 16;  // 4096 keys per tile
 // small inputs: 4 keys per thread (1024 per tile): 4x the tiles and a quarter of
 // the per-tile rounds, for the latency-bound passes of a few-tile sort
 constexpr int kSortItemsSmall = 4;
-constexpr int64_t kSortSmallN = 1 << 18;
+#ifndef SLAB_SORT_SMALL_LOG2
+#define SLAB_SORT_SMALL_LOG2 18
+#endif
+constexpr int64_t kSortSmallN = (int64_t)1 << SLAB_SORT_SMALL_LOG2;
 static int sort_items(int64_t n) { return n < kSortSmallN ? kSortItemsSmall : kSortItems; }
 
 __global__ void zkey_init_kernel(const double* __restrict__ z, int64_t stride, int64_t n,
