@@ -537,7 +537,7 @@ static int64_t home_bound(int64_t n, int r, int W) {
 }
 
 static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
-                         cudaEvent_t pos_ready, cudaEvent_t charge_ready);
+                         cudaEvent_t pos_ready, cudaEvent_t charge_ready, bool host_entry);
 
 // Concurrent short range up to this many particles (cfg3, N = 1e5: 3.30 ->
 // 3.07 ms).  Beyond it both halves fill the GPU on their own: at N = 1e6 the
@@ -547,6 +547,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
 #define SLAB_FORK_MAX_N 400000
 #endif
 constexpr int64_t kForkMaxN = SLAB_FORK_MAX_N;
+#ifndef SLAB_FORK_HOST
+#define SLAB_FORK_HOST 1
+#endif
+constexpr bool kForkHost = SLAB_FORK_HOST;
 #ifndef SLAB_PAR_ZERO
 #define SLAB_PAR_ZERO 1
 #endif
@@ -567,7 +571,7 @@ static int ensure_fork(SlabCtx* ctx) {
 
 int slab_evaluate(SlabCtx* ctx, const SlabEvalArgs* a, void* stream) {
   if (!ctx || !a) return fail(SLAB_ERR_ARG, "null context or arguments");
-  return evaluate_impl(ctx, a, (cudaStream_t)stream, nullptr, nullptr);
+  return evaluate_impl(ctx, a, (cudaStream_t)stream, nullptr, nullptr, false);
 }
 
 int slab_evaluate_host(SlabCtx* ctx, const SlabEvalArgs* args, const double* h_pos,
@@ -618,7 +622,7 @@ int slab_evaluate_host(SlabCtx* ctx, const SlabEvalArgs* args, const double* h_p
   a.d_charge = ctx->h_dq;
   a.d_forces = args->want_forces ? ctx->h_dforces : nullptr;
   a.d_energy = ctx->h_denergy;
-  const int rc = evaluate_impl(ctx, &a, st, ctx->ev_pos, ctx->ev_q);
+  const int rc = evaluate_impl(ctx, &a, st, ctx->ev_pos, ctx->ev_q, true);
   if (rc) {
     cudaStreamSynchronize(ctx->up_stream);
     cudaStreamSynchronize(st);
@@ -633,7 +637,7 @@ int slab_evaluate_host(SlabCtx* ctx, const SlabEvalArgs* args, const double* h_p
 }
 
 static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
-                         cudaEvent_t pos_ready, cudaEvent_t charge_ready) {
+                         cudaEvent_t pos_ready, cudaEvent_t charge_ready, bool host_entry) {
   const int64_t n = a->n;
   if (n < 0 || a->nmode < 0 || !a->d_energy || (n > 0 && (!a->d_pos || !a->d_charge)))
     return fail(SLAB_ERR_ARG, "bad evaluation arguments");
@@ -688,7 +692,7 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   // the sort / Fourier / k = 0 chain on ctx->hi (highest priority); both join
   // back into `st` before the assembly.  (A z-split phase 1 returns with the
   // short range possibly still running; phase 2 joins it.)
-  const bool fork = !a->skip_short_range && n > 0 && n <= kForkMaxN;
+  const bool fork = !a->skip_short_range && n > 0 && (n <= kForkMaxN || (host_entry && kForkHost));
   // the k = 0 chain (aggregate, carry, sweep: low-occupancy kernels) runs on
   // ctx->aux beside the Fourier chain once the decay table exists
   const bool par_zero = kParZero && a->phase == 0 && n >= 2 && lead;
