@@ -46,6 +46,12 @@ constexpr int kSB = SLAB_SWEEP_SB;
 // sweep CTA size cap: 2 CTAs/SM at 65536 / (2 * cap) registers per thread
 constexpr int kSweepMaxThreads = SLAB_SWEEP_MAXT;  // force staging batch (particles)
 constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
+// CTAs per SM the sweep is compiled for: 2 (128 registers) up to SLAB_SWEEP_BIG_MH
+// pairs; 1 above it, where 128 registers spill hundreds of bytes per lane
+#ifndef SLAB_SWEEP_BIG_MH
+#define SLAB_SWEEP_BIG_MH 10  // cfg3 (M = 24, 12 pairs): sweep 1.90 -> 1.31 ms; 8 pairs stay at 2 CTAs (4.14 vs 4.86 ms)
+#endif
+__host__ __device__ constexpr int sweep_min_blocks(int mh) { return mh >= SLAB_SWEEP_BIG_MH ? 1 : 2; }
 constexpr int kMaxR = 256;
 constexpr size_t kSmemPerSM = 227 * 1024;  // usable shared memory per SM (B200)
 constexpr int kAggRegs = 72;               // fourier_aggregate_mma_kernel (ptxas)
@@ -609,7 +615,7 @@ static int carry_groups(int nch, int items, int mh) {
 // (forward and backward lanes to separate buffers), reduced in fixed order
 // afterwards: deterministic, no atomics.
 template <int MH>
-__global__ void __launch_bounds__(kSweepMaxThreads, 2) fourier_sweep_kernel(
+__global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
     const double* __restrict__ modetab, int P, int items, int ipg, BVec b,
@@ -933,9 +939,10 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
       const int by_regs = 65536 / (regs * threads);
       return by_smem < by_regs ? (by_smem < 32 ? by_smem : 32) : (by_regs < 32 ? by_regs : 32);
     };
-    const int sw_full = 65536 / (128 * 32 * p.warps);
+    const int sw_regs = sweep_min_blocks(mh) == 1 ? 255 : 128;
+    const int sw_full = 65536 / (sw_regs * 32 * p.warps) > 0 ? 65536 / (sw_regs * 32 * p.warps) : 1;
     const int ag_full = 65536 / (kAggRegs * 32 * tpc);
-    while (R > 16 && (ctas(sweep_smem(R, mh, p.warps), 32 * p.warps, 128) < sw_full ||
+    while (R > 16 && (ctas(sweep_smem(R, mh, p.warps), 32 * p.warps, sw_regs) < sw_full ||
                       ctas(agg_mma_smem(R, mh), 32 * tpc, kAggRegs) < ag_full))
       R /= 2;
   }
