@@ -121,6 +121,10 @@ typedef struct SlabEvalArgs {
   int shard_mode;
   int phase;
   double* d_xchg;
+  /* cudaEvent_t or NULL: d_modes is complete once this event has fired (e.g. a
+   * device sampler on another stream).  The evaluation waits on it only before
+   * its first use of the k-set, so the sampler overlaps the z sort. */
+  void* ev_modes_ready;
 } SlabEvalArgs;
 
 enum { SLAB_SHARD_MODES = 0, SLAB_SHARD_ZSPLIT = 1 };

@@ -82,6 +82,7 @@ class SlabEvalArgs(ctypes.Structure):
         ("shard_mode", ctypes.c_int),
         ("phase", ctypes.c_int),
         ("d_xchg", ctypes.c_void_p),
+        ("ev_modes_ready", ctypes.c_void_p),
     ]
 
 

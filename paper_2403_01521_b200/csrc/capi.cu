@@ -742,6 +742,8 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
         CK(cudaEventRecord(ctx->ev_zero, ctx->aux));
       }
       if (forces) CK(cudaMemsetAsync(w.fsorted, 0, sizeof(double) * 3 * n, sl));
+      if (a->nmode > 0 && a->ev_modes_ready)
+        CK(cudaStreamWaitEvent(sl, (cudaEvent_t)a->ev_modes_ready, 0));
       if (a->nmode > 0)
         CK(slab::fourier_phase1(fp, fw, w.xs, w.ys, w.zs, w.qs, a->d_modes, a->d_commonv,
                                 a->commonv_scalar, area, sh.b, sh.w, ctx->status,

@@ -87,7 +87,7 @@ class Engine:
     def evaluate(self, pos, charge, box, alpha, r_c, soe, modes, commonv, charge_const,
                  forces=None, energy=None, want_forces=True, skip_short_range=False,
                  perm=None, soe_pack=None, shard=(0, 1), scan_events=None, shard_mode=0,
-                 phase=0, xchg=None):
+                 phase=0, xchg=None, modes_ready=None):
         """Enqueue one energy/force evaluation.  ``commonv`` is a float (RB) or a
         (P,) device tensor (full mode sum).  Writes energy (8,) and forces (n,3).
 
@@ -118,7 +118,8 @@ class Engine:
             d_perm=_ptr(perm), shard_rank=int(shard[0]), shard_count=int(shard[1]),
             ev_scan_begin=ctypes.c_void_p(scan_events[0].cuda_event) if scan_events else None,
             ev_scan_end=ctypes.c_void_p(scan_events[1].cuda_event) if scan_events else None,
-            shard_mode=int(shard_mode), phase=int(phase), d_xchg=_ptr(xchg))
+            shard_mode=int(shard_mode), phase=int(phase), d_xchg=_ptr(xchg),
+            ev_modes_ready=ctypes.c_void_p(modes_ready.cuda_event) if modes_ready else None)
         check(self.lib.slab_evaluate(self.ctx, ctypes.byref(args), self._stream()),
               "slab_evaluate")
         return energy, forces
@@ -386,6 +387,11 @@ class DeviceEvaluator:
             if self.sample:
                 self.eng.sample_modes(self.state, self.seed, self.alpha, box.lx, box.ly,
                                       self.thin, burn_in, 0)
+                # the chain for each step runs on a side stream, overlapping the
+                # z sort; the evaluation waits on this event before the k-set's
+                # first use
+                self.side = torch.cuda.Stream(dev)
+                self.ev_modes = torch.cuda.Event()
         # multi-GPU split: "zsplit" (default) -- every rank scans all modes over its
         # contiguous range of the z-sorted particles, one all-gather of the chunk-range
         # maps between the two phases; "modes" -- each rank scans its slice of the
@@ -408,9 +414,16 @@ class DeviceEvaluator:
 
     def _enqueue(self, scan_events=None):
         torch = _torch()
+        ready = None
         if self.sample:
-            self.eng.sample_modes(self.state, self.seed, self.alpha, self.box.lx, self.box.ly,
-                                  self.thin, 0, self.P, self.modes)
+            # after everything queued so far (the previous step still reads the
+            # k-set buffer), concurrently with this step's sort
+            self.side.wait_stream(torch.cuda.current_stream(self.eng.device))
+            with torch.cuda.stream(self.side):
+                self.eng.sample_modes(self.state, self.seed, self.alpha, self.box.lx,
+                                      self.box.ly, self.thin, 0, self.P, self.modes)
+            self.ev_modes.record(self.side)
+            ready = self.ev_modes
         modes = self.modes[self.t0:self.t1] if self.t1 > self.t0 else None
         cv = self.commonv[self.t0:self.t1] if torch.is_tensor(self.commonv) else self.commonv
         args = (self.pos, self.charge, self.box, self.alpha, self.params.r_c, self.soe, modes,
@@ -418,11 +431,12 @@ class DeviceEvaluator:
         kw = dict(forces=self.forces, energy=self.energy, soe_pack=self.pack,
                   shard=(self.rank, self.world), scan_events=scan_events)
         if self.zsplit:
-            self.eng.evaluate(*args, shard_mode=1, phase=1, xchg=self.xloc, **kw)
+            self.eng.evaluate(*args, shard_mode=1, phase=1, xchg=self.xloc, modes_ready=ready,
+                              **kw)
             self.exchange(self.xloc, self.xall)
             self.eng.evaluate(*args, shard_mode=1, phase=2, xchg=self.xall, **kw)
         else:
-            self.eng.evaluate(*args, **kw)
+            self.eng.evaluate(*args, modes_ready=ready, **kw)
         if self.reduce:
             import torch.distributed as dist
             dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
