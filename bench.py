@@ -253,7 +253,9 @@ def run_reference(args, rank, world):
 def profile_step(ev, torch):
     """One step under torch.profiler (CUPTI): (kernel launches of OUR library,
     {kernel name: device ms}).  Outside the timed region."""
+    import warnings
     from torch.profiler import ProfilerActivity, profile
+    warnings.filterwarnings("ignore", message=".*Profiler clears events.*")
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         ev.step()
         torch.cuda.synchronize()
