@@ -59,6 +59,12 @@ def full_metrics(rep):
         "smsp__thread_inst_executed_per_inst_executed.ratio": "threads_per_inst",
         "launch__grid_size": "grid",
         "launch__block_size": "block",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active":
+            "dmma_pipe_pct",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active": "shared_pipe_pct",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1_pct",
+        "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct": "l1_hit_pct",
+        "launch__occupancy_limit_registers": "occ_limit_regs",
     }
     scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "usecond": 1e-3,
              "msecond": 1.0, "nsecond": 1e-6, "us": 1e-3, "ms": 1.0, "ns": 1e-6}
@@ -115,6 +121,26 @@ def main():
                        "dram__bytes_write.sum from ncu --set full")
     with open(os.path.join(REPO, "profiles", f"ncu_{tag}_summary.json"), "w") as fh:
         json.dump(summary, fh, indent=1)
+    # one markdown table of the per-kernel limiters (the numbers DESIGN.md cites)
+    tbl = [f"# ncu full captures, round {tag}", "",
+           "`ncu --set full --clock-control none --import-source on` of one launch per kernel "
+           "on a cfg4 step (`tools/profile_round.sh`).  fp64 = DFMA pipe; DMMA = the FP64 "
+           "tensor sub-pipe; shared = the pipe both issue to; L1 = l1tex throughput.", "",
+           "| kernel | ms | fp64 % | DMMA % | shared % | issue % | L1 % | L1 hit % | occupancy % "
+           "| regs | DRAM MB |", "|---|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|"]
+
+    def f(d, k, fmt="{:.1f}"):
+        v = d.get(k)
+        return fmt.format(v) if isinstance(v, float) else "-"
+    for k, d in sorted(summary["kernels"].items(), key=lambda kv: -(kv[1].get("duration_ms")
+                                                                    or 0)):
+        mb = ((d.get("dram_read") or 0) + (d.get("dram_write") or 0)) / 1e6
+        tbl.append(f"| {k} | {f(d, 'duration_ms', '{:.3f}')} | {f(d, 'fp64_pipe_pct')} | "
+                   f"{f(d, 'dmma_pipe_pct')} | {f(d, 'shared_pipe_pct')} | "
+                   f"{f(d, 'issue_active_pct')} | {f(d, 'l1_pct')} | {f(d, 'l1_hit_pct')} | "
+                   f"{f(d, 'occupancy_pct')} | {f(d, 'registers', '{:.0f}')} | {mb:.0f} |")
+    with open(os.path.join(REPO, "profiles", f"ncu_{tag}_kernels.md"), "w") as fh:
+        fh.write("\n".join(tbl) + "\n")
     print("\n".join(lines[-12:]))
     print(json.dumps(summary, indent=1)[:3000])
 
