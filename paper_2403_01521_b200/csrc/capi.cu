@@ -98,30 +98,60 @@ int ensure_arena(SlabCtx* c, size_t bytes) {
 
 struct SOEHost {
   int m = 0, mh = 0;
+  int real_terms = 0;  // self-conjugate terms carried as pairs (mh = (m + real_terms) / 2)
   slab::BVec b{};
   slab::WVec w{};
   slab::ZCoef z{};
 };
 
+// The kernels run over conjugate PAIRS (s, w), (conj s, conj w): per pair two
+// complex recurrences with real inputs carry both terms.  A table is accepted
+// when every term is either real (s and w real: carried as the pair
+// (s, w/2), (s, w/2) -- halving is exact, so c G + c G = (w / (b^2 - k^2)) G)
+// or has its conjugate elsewhere in the table (bitwise).  Built contours are
+// conjugate-symmetric in mirrored order; m = 1 real-exponent tables are what
+// soe.py's removable-singularity tests use.
 int prepare_soe(const SlabSOE& soe, double alpha, SOEHost& out) {
-  if (soe.m < 2 || soe.m % 2 || soe.m > 24)
-    return fail(SLAB_ERR_ARG, "SOE term count must be even and in [2, 24]");
+  if (soe.m < 1 || soe.m > 24) return fail(SLAB_ERR_ARG, "SOE term count must be in [1, 24]");
   if (!soe.h_w_re || !soe.h_w_im || !soe.h_s_re || !soe.h_s_im)
     return fail(SLAB_ERR_ARG, "SOE arrays must be given");
-  const int m = soe.m, mh = m / 2;
-  for (int l = 0; l < mh; ++l) {
-    const int r = m - 1 - l;
-    if (soe.h_s_re[r] != soe.h_s_re[l] || soe.h_s_im[r] != -soe.h_s_im[l] ||
-        soe.h_w_re[r] != soe.h_w_re[l] || soe.h_w_im[r] != -soe.h_w_im[l])
-      return fail(SLAB_ERR_UNSUPPORTED,
-                  "SOE table is not conjugate-paired (term M-1-l must equal conj(term l))");
-  }
+  const int m = soe.m;
   for (int l = 0; l < m; ++l)
     if (!(soe.h_s_re[l] > 0)) return fail(SLAB_ERR_ARG, "every exponent must have positive real part");
+  bool used[24] = {false};
+  cd ps[24], pw[24];
+  int mh = 0;
+  out.real_terms = 0;
+  for (int l = 0; l < m; ++l) {
+    if (used[l]) continue;
+    used[l] = true;
+    if (soe.h_s_im[l] == 0.0 && soe.h_w_im[l] == 0.0) {  // self-conjugate: half weight twice
+      ps[mh] = cd(soe.h_s_re[l], 0.0);
+      pw[mh] = cd(0.5 * soe.h_w_re[l], 0.0);
+      ++mh;
+      ++out.real_terms;
+      continue;
+    }
+    int r = -1;
+    for (int j = m - 1; j > l; --j)  // mirrored order first (built contours)
+      if (!used[j] && soe.h_s_re[j] == soe.h_s_re[l] && soe.h_s_im[j] == -soe.h_s_im[l] &&
+          soe.h_w_re[j] == soe.h_w_re[l] && soe.h_w_im[j] == -soe.h_w_im[l]) {
+        r = j;
+        break;
+      }
+    if (r < 0)
+      return fail(SLAB_ERR_UNSUPPORTED,
+                  "SOE table is not conjugate-symmetric (a complex term without its conjugate)");
+    used[r] = true;
+    ps[mh] = cd(soe.h_s_re[l], soe.h_s_im[l]);
+    pw[mh] = cd(soe.h_w_re[l], soe.h_w_im[l]);
+    ++mh;
+  }
+  if (mh > 12) return fail(SLAB_ERR_UNSUPPORTED, "more than 12 SOE pairs");
   out.m = m;
   out.mh = mh;
   for (int l = 0; l < mh; ++l) {
-    const cd s(soe.h_s_re[l], soe.h_s_im[l]), w(soe.h_w_re[l], soe.h_w_im[l]);
+    const cd s = ps[l], w = pw[l];
     out.b.re[l] = alpha * s.real();
     out.b.im[l] = alpha * s.imag();
     out.w.re[l] = w.real();
@@ -659,6 +689,8 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   if (a->phase != 0 && !zsplit) return fail(SLAB_ERR_ARG, "phases belong to the z-split mode");
   if (zsplit && a->phase == 0) return fail(SLAB_ERR_ARG, "z-split runs as phase 1 + phase 2");
   if (zsplit && a->nmode > 0 && !a->d_xchg) return fail(SLAB_ERR_ARG, "z-split needs d_xchg");
+  if (zsplit && sh.real_terms)  // the exchange is sized for m = 2 mh (slab_zsplit_exchange_doubles)
+    return fail(SLAB_ERR_UNSUPPORTED, "z-split needs a table of conjugate pairs (no real terms)");
   const bool forces = a->want_forces && n > 0;
   auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, forces ? 2 : 1, zsplit ? scount : 1);
   if (zsplit) {  // this rank's contiguous chunk range of the z-sorted particles

@@ -1108,7 +1108,7 @@ cudaError_t fourier_phase1(const FourierPlan& p, const FourierWork& w, const dou
   switch (p.mh) {
 #define FCASE(K) \
   case K: return phase1_mh<K>(p, w, xs, ys, zs, qs, b, totals, st);
-    FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
+    FCASE(1) FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
     FCASE(12)
 #undef FCASE
     default: return cudaErrorInvalidValue;
@@ -1137,7 +1137,7 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
   switch (p.mh) {
 #define FCASE(K) \
   case K: e = phase2_mh<K>(p, w, xs, ys, zs, qs, dtab, b, want_forces, tin2, st); break;
-    FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
+    FCASE(1) FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
     FCASE(12)
 #undef FCASE
     default: return cudaErrorInvalidValue;

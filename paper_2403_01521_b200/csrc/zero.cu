@@ -376,7 +376,7 @@ cudaError_t zero_run_b(const ZeroPlan& p, double* work, const double* zs, const 
   switch (p.mh) {
 #define ZCASE(K) \
   case K: zero_launch<K>(p, work, zs, qs, dtab, zc, b, alpha, want_forces, fzf, fzb, upair, st); break;
-    ZCASE(2) ZCASE(3) ZCASE(4) ZCASE(5) ZCASE(6) ZCASE(7) ZCASE(8) ZCASE(9) ZCASE(10) ZCASE(11)
+    ZCASE(1) ZCASE(2) ZCASE(3) ZCASE(4) ZCASE(5) ZCASE(6) ZCASE(7) ZCASE(8) ZCASE(9) ZCASE(10) ZCASE(11)
     ZCASE(12)
 #undef ZCASE
     default: return cudaErrorInvalidValue;

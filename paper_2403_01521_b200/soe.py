@@ -9,9 +9,11 @@ Reference: ``pkg/src/slabewald/soe.py`` -- contour nodes ``_contour_nodes``
 ``certify_soe_raw`` (119-143), CSV tables (151-177).  The hot path only consumes
 ``SOEApprox.w`` and ``.s``; this module is per-run setup.
 
-The device kernels rely on the exact conjugate pairing
-``s[M-1-l] == conj(s[l])`` and ``w[M-1-l] == conj(w[l])`` (bitwise), which every
-contour built here satisfies; ``is_conjugate_paired`` checks it.
+The device kernels carry conjugate PAIRS of terms: a table is accepted when
+every term is real (carried as two half-weight copies) or has its bitwise
+conjugate elsewhere in the table.  Every contour built here is paired in
+mirrored order, ``s[M-1-l] == conj(s[l])`` (``is_conjugate_paired``); a table
+with a complex term lacking its conjugate raises ``NotImplementedError``.
 """
 
 from __future__ import annotations

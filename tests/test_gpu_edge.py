@@ -84,6 +84,39 @@ def test_single_mode_and_full_sum_small(pk):
     _check(bd, f, e_ref, f_ref)
 
 
+@pytest.mark.parametrize("table", ["real_m1", "shuffled_plus_real"])
+def test_real_and_unordered_soe_tables_match_oracle(pk, table):
+    """Tables beyond the built contours: the single real-exponent term of the
+    reference's soe tests (w = 1, s = 2), and a built 8-term table in shuffled
+    order plus a real term -- every term real or with its conjugate somewhere;
+    a complex term without its conjugate is rejected."""
+    rng = np.random.default_rng(21)
+    box = pk.BoxGeometry(15.0, 15.0, 6.0)
+    n = 900
+    s = pk.make_system(np.where(np.arange(n) % 2 == 0, 1.0, -1.0), np.ones(n),
+                       rng.uniform([0, 0, 0.2], [15, 15, 5.8], size=(n, 3)), box)
+    alpha = 0.9
+    params = pk.make_ewald_params(alpha, 3.0, box)
+    if table == "real_m1":
+        w, sv = np.array([1.0 + 0j]), np.array([2.0 + 0j])
+    else:
+        b8 = pk.build_soe_contour(8)
+        order = rng.permutation(8)
+        w = np.concatenate([b8.w[order], [0.25 + 0j]])
+        sv = np.concatenate([b8.s[order], [3.5 + 0j]])
+    soe = pk.SOEApprox(m=len(w), w=w, s=sv, eps_certified=1.0, domain_max=20.0)
+    modes = pk.ModeSampler(alpha, box, seed=2).batch(7)
+    H = pk.normalization_H(alpha, box)
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 7, H=H, c_q=0.0)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
+                                (H / 7) * (2 / np.sqrt(np.pi)) * alpha, 0.0)
+    _check(bd, f, e_ref, f_ref)
+    bad = pk.SOEApprox(m=2, w=np.array([1.0 + 0.5j, 1.0 + 0j]),
+                       s=np.array([2.0 + 1j, 3.0 + 0j]), eps_certified=1.0, domain_max=20.0)
+    with pytest.raises(NotImplementedError, match="conjugate"):
+        pk.rb_energy_forces(s, box, params, bad, _Stub(modes), 7, H=H, c_q=0.0)
+
+
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
 def test_run_to_run_bit_reproducible(pk, name):
     """Fixed-order sums everywhere (no atomics on values), also with the short
