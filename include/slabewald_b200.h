@@ -52,7 +52,8 @@ enum {
 /* device status word bits (written by kernels, read by the host after sync) */
 enum {
   SLAB_STATUS_COINCIDENT = 1, /* d2 < 1e-24 pair: ewald2d.py:207-209,301-302 */
-  SLAB_STATUS_SINGULAR = 2,   /* |b_l - k| < 2e-6 k: soewald2d.py:118-121 (analytic branch) */
+  SLAB_STATUS_SINGULAR = 2,   /* reserved: singular terms (|b_l - k| < 2e-6 k) are now
+                               * evaluated (soewald2d.py:116-124), this bit is never set */
   SLAB_STATUS_NBR_OVERFLOW = 4, /* a short-range neighbour row exceeded its capacity: results
                                    are invalid; raise it (slab_ctx_neighbor_capacity) and rerun */
   SLAB_STATUS_NONFINITE = 8,    /* a z coordinate is not finite (core.py:206-207): results invalid */
@@ -203,7 +204,7 @@ int64_t slab_zsplit_exchange_doubles(int64_t nmode, int soe_terms, int want_forc
  * d_modes[b*P .. (b+1)*P) (rows kx, ky, |k|), commonv = commonv_scalar for every
  * mode, no charge constant.  Particles in input order (pos AoS, charge): sorted
  * once, decay table once, modes swept in groups on device.  ORs status bits
- * (SINGULAR, NONFINITE) into d_status. */
+  * (NONFINITE) into d_status. */
 int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
                         SlabSOE soe, double alpha, double area, const double* d_modes,
                         int64_t nbatch, int64_t P, double commonv_scalar, double* d_out,

@@ -122,12 +122,12 @@ __global__ void mode_table_kernel(const double* __restrict__ modes,
   const double ct = commonv ? commonv[t] : commonv_scalar;
   double* r = tab + (size_t)t * mode_stride(mh);
   double kappa = 0.0;
-  int singular = 0;
+  double wsing = 0.0;  // W_s: weights of the singular terms (a pair carries w + conj w)
   for (int l = 0; l < mh; ++l) {
     const double br = b.re[l], bi = b.im[l];
     double cr = 0.0, ci = 0.0;
     if (hypot(br - k, bi) < kSingularTol * k) {
-      singular = 1;  // analytic-limit branch (soewald2d.py:118-121) not on device
+      wsing += 2.0 * w.re[l];  // analytic-limit branch (soewald2d.py:116-124): c_l = 0
     } else {
       // c = w / (b^2 - k^2)
       const double dr = br * br - bi * bi - k * k, di = 2.0 * br * bi;
@@ -150,9 +150,127 @@ __global__ void mode_table_kernel(const double* __restrict__ modes,
   r[3] = pref * ct / k;
   r[4] = pref * ct;
   r[5] = kappa;
-  r[6] = singular;
+  r[6] = wsing;  // consumed by fourier_singular_kernel
   r[7] = 0.0;
-  if (singular) atomicOr(status, SLAB_STATUS_SINGULAR_DEV);
+  (void)status;
+}
+
+// ---------------------------------------------------------------------------
+// the singular-term correction (soewald2d.py:116-124, 146-149, 162-170)
+// ---------------------------------------------------------------------------
+// A term with |b_l - k| < 2e-6 k leaves the G recurrences (c_l = 0) and its
+// weight W_s enters through an extra chain h_a = (h_{a-1} + dz_a (g_{a-1} +
+// u_{a-1})) e^{-k dz_a}: p += W_s (g / k + h), zeta -= W_s h.  Everything is
+// linear in (p, zeta), so the main sweep runs without the term and this pass
+// adds its contribution.  Singular terms only exist for (near-)real exponents
+// -- never in built contours; the host launches this only for tables that have
+// such a term.  One block: per singular item, each thread composes the affine
+// map of (g, h) over its contiguous particle segment, a block scan gives each
+// segment its state, and the segment is re-walked with the readout.  Items run
+// in sequence and each particle's force belongs to one thread: deterministic.
+struct SingMap {  // (g, h) -> D [[1, 0], [del, 1]] (g, h) + (Xg, Xh)
+  double D, del;
+  C2 Xg, Xh;
+};
+__device__ __forceinline__ SingMap sing_compose(const SingMap& a, const SingMap& b) {  // b after a
+  SingMap r;
+  r.D = a.D * b.D;
+  r.del = a.del + b.del;
+  r.Xg = C2{b.D * a.Xg.re + b.Xg.re, b.D * a.Xg.im + b.Xg.im};
+  r.Xh = C2{b.D * (b.del * a.Xg.re + a.Xh.re) + b.Xh.re,
+            b.D * (b.del * a.Xg.im + a.Xh.im) + b.Xh.im};
+  return r;
+}
+constexpr int kSingThreads = 512;
+__global__ void __launch_bounds__(kSingThreads) fourier_singular_kernel(
+    const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
+    const double* __restrict__ qs, int64_t n, const double* __restrict__ modetab, int mh, int P,
+    int items, int want_forces, double* __restrict__ esing, double* __restrict__ forces) {
+  __shared__ SingMap sm[kSingThreads];
+  __shared__ double red[kSingThreads];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + kSingThreads - 1) / kSingThreads;
+  for (int item = 0; item < items; ++item) {
+    const bool fwd = item < P;
+    const int t = fwd ? item : item - P;
+    const double* mt = modetab + (size_t)t * mode_stride(mh);
+    const double ws = mt[6];
+    if (fwd && tid == 0) esing[t] = 0.0;
+    if (ws == 0.0) continue;  // block-uniform
+    const double kx = mt[0], ky = mt[1], k = mt[2], ck = mt[3], cz = mt[4];
+    // positions s = 0 .. n-1 along the sweep direction
+    const int64_t s0 = tid * per, s1 = min(n, s0 + per);
+    auto idx = [&](int64_t sidx) { return fwd ? sidx : n - 1 - sidx; };
+    // the step INTO position sidx (sidx >= 1) from sidx - 1
+    auto step = [&](int64_t sidx, C2 u_prev) {
+      const int64_t a = idx(sidx), ap = idx(sidx - 1);
+      const double dz = fwd ? zs[a] - zs[ap] : zs[ap] - zs[a];
+      const double D = exp(-k * dz);
+      return SingMap{D, dz, C2{D * u_prev.re, D * u_prev.im},
+                     C2{D * dz * u_prev.re, D * dz * u_prev.im}};
+    };
+    auto input = [&](int64_t sidx) {  // u (forward) or v (backward) of the particle at sidx
+      const int64_t a = idx(sidx);
+      double sn, cs;
+      sincos(kx * xs[a] + ky * ys[a], &sn, &cs);
+      return C2{qs[a] * cs, fwd ? -qs[a] * sn : qs[a] * sn};
+    };
+    SingMap M{1.0, 0.0, C2{0.0, 0.0}, C2{0.0, 0.0}};
+    for (int64_t si = s0; si < s1; ++si)
+      if (si >= 1) M = sing_compose(M, step(si, input(si - 1)));
+    sm[tid] = M;
+    __syncthreads();
+    for (int o = 1; o < kSingThreads; o <<= 1) {  // inclusive scan (Hillis-Steele)
+      const SingMap prev = tid >= o ? sm[tid - o] : SingMap{1.0, 0.0, C2{0, 0}, C2{0, 0}};
+      __syncthreads();
+      if (tid >= o) sm[tid] = sing_compose(prev, sm[tid]);
+      __syncthreads();
+    }
+    // state at position s0 - 1 = the previous segments' composed map applied to (0, 0)
+    C2 g{0.0, 0.0}, hh{0.0, 0.0};
+    if (tid > 0) {
+      g = sm[tid - 1].Xg;
+      hh = sm[tid - 1].Xh;
+    }
+    __syncthreads();
+    double e = 0.0;
+    for (int64_t si = s0; si < s1; ++si) {
+      const int64_t a = idx(si);
+      if (si >= 1) {  // the state at position si from the one at si - 1
+        const SingMap st1 = step(si, input(si - 1));
+        const C2 g0 = g;
+        g = C2{st1.D * g0.re + st1.Xg.re, st1.D * g0.im + st1.Xg.im};
+        hh = C2{st1.D * (st1.del * g0.re + hh.re) + st1.Xh.re,
+                st1.D * (st1.del * g0.im + hh.im) + st1.Xh.im};
+      }
+      // p_x = W_s (g / k + h), zeta_x = -W_s h; phase e^{+-i theta}
+      const C2 px{ws * (g.re / k + hh.re), ws * (g.im / k + hh.im)};
+      const C2 zx{-ws * hh.re, -ws * hh.im};
+      double sn, cs;
+      sincos(kx * xs[a] + ky * ys[a], &sn, &cs);
+      const double ps = fwd ? sn : -sn;
+      const double epr = cs * px.re - ps * px.im, epi = cs * px.im + ps * px.re;
+      const double q = qs[a];
+      if (fwd) e += q * epr;
+      if (want_forces) {
+        const double zr = cs * zx.re - ps * zx.im;
+        const double sgn = fwd ? 1.0 : -1.0;
+        forces[3 * a + 0] += sgn * ck * q * kx * epi;
+        forces[3 * a + 1] += sgn * ck * q * ky * epi;
+        forces[3 * a + 2] -= sgn * cz * q * zr;
+      }
+    }
+    if (fwd) {
+      red[tid] = e;
+      __syncthreads();
+      for (int w2 = kSingThreads / 2; w2 > 0; w2 >>= 1) {
+        if (tid < w2) red[tid] += red[tid + w2];
+        __syncthreads();
+      }
+      if (tid == 0) esing[t] = ck * red[0];
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -809,7 +927,8 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
 // over modes in mode order exactly like soewald2d.py:204-207
 __global__ void __launch_bounds__(256) fourier_mode_energy_kernel(
     const double* __restrict__ epart, int c0, int c1, int P, int mh,
-    const double* __restrict__ modetab, double* __restrict__ se) {
+    const double* __restrict__ modetab, const double* __restrict__ esing,
+    double* __restrict__ se) {
   __shared__ double red[256];
   const int t = blockIdx.x;
   double s = 0.0;
@@ -820,7 +939,8 @@ __global__ void __launch_bounds__(256) fourier_mode_energy_kernel(
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) se[t] = modetab[(size_t)t * mode_stride(mh) + 3] * red[0];
+  if (threadIdx.x == 0)
+    se[t] = modetab[(size_t)t * mode_stride(mh) + 3] * red[0] + (esing ? esing[t] : 0.0);
 }
 
 // Kahan over modes in mode order exactly like soewald2d.py:204-207, one thread
@@ -965,7 +1085,7 @@ size_t fourier_work_doubles(const FourierPlan& p) {
   d += 2 * (size_t)p.nch * ncomp_of(p.mh) * nitems;  // carry (double2)
   d += 2 * 2 * (size_t)p.nch * p.mh;                 // Df, Db (double2)
   d += 2 * (size_t)p.nch;                            // zbound
-  d += (size_t)p.nch * p.P + p.P;                    // epart + per-mode sums
+  d += (size_t)p.nch * p.P + 2 * (size_t)p.P;        // epart + per-mode sums + singular terms
   d += (size_t)(p.nbuf + 1) * p.n * 3;               // fpart
   d += 4 * (size_t)carry_groups(p.nch, p.items, p.mh) * 32 * ncomp_of(p.mh) * p.items;  // segmap
   d += 8 * (size_t)ncomp_of(p.mh) * p.items;  // z-split carried-in states (double2) + spare
@@ -985,7 +1105,7 @@ void fourier_work_carve(const FourierPlan& p, double* base, FourierWork& w) {
   w.zbound = q;
   q += 2 * (size_t)p.nch;
   w.epart = q;
-  q += (size_t)p.nch * p.P + p.P;
+  q += (size_t)p.nch * p.P + 2 * (size_t)p.P;
   w.fpart = q;
   q += (size_t)(p.nbuf + 1) * p.n * 3;
   q += (reinterpret_cast<uintptr_t>(q) / 8) & 1;
@@ -1144,7 +1264,18 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
   }
   if (e != cudaSuccess) return e;
   double* se = w.epart + (size_t)p.nch * p.P;  // P scratch doubles after the partials
-  fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.c0, p.c1, p.P, p.mh, w.modetab, se);
+  double* esing = se + p.P;                    // and P for the singular-term energies
+  // tables with a (near-)real exponent can put a term within 2e-6 k of a mode
+  // (soewald2d.py:116-124); complex pairs with |Im b| >= 1e-5 Re b never can
+  bool near_real = false;
+  for (int l = 0; l < p.mh; ++l) near_real |= fabs(b.im[l]) < 1e-5 * b.re[l];
+  const bool sing = near_real && p.c0 == 0 && p.c1 == p.nch;
+  if (sing)
+    fourier_singular_kernel<<<1, kSingThreads, 0, st>>>(xs, ys, zs, qs, p.n, w.modetab, p.mh,
+                                                         p.P, p.items, want_forces, esing,
+                                                         forces_sorted);
+  fourier_mode_energy_kernel<<<p.P, 256, 0, st>>>(w.epart, p.c0, p.c1, p.P, p.mh, w.modetab,
+                                                  sing ? esing : nullptr, se);
   const int nseg = p.P / seg_len;
   if (nseg > 0) kahan_modes_kernel<<<nseg, kKahanThreads, 0, st>>>(se, nseg, seg_len, energy_out);
   if (want_forces) {

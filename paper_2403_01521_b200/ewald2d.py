@@ -62,15 +62,11 @@ def status_of(energy, summed: bool = False) -> int:
 
 
 def raise_on_status(status: int) -> None:
-    from ._native import SLAB_STATUS_COINCIDENT, SLAB_STATUS_NONFINITE, SLAB_STATUS_SINGULAR
+    from ._native import SLAB_STATUS_COINCIDENT, SLAB_STATUS_NONFINITE
     if status & SLAB_STATUS_NONFINITE:  # checked first, like sort_by_z (core.py:206-207)
         raise ValueError("z coordinates must be finite")
     if status & SLAB_STATUS_COINCIDENT:
         raise ValueError("coincident particles: short-range energy is singular")
-    if status & SLAB_STATUS_SINGULAR:
-        raise NotImplementedError(
-            "an SOE exponent alpha*s_l lies within 2e-6 k of a sampled |k|: the analytic-limit "
-            "branch of soewald2d.py:116-124 is not implemented on device")
 
 
 def short_range_energy_forces(system: ParticleSystem, box: BoxGeometry, alpha: float,

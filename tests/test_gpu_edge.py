@@ -117,6 +117,40 @@ def test_real_and_unordered_soe_tables_match_oracle(pk, table):
         pk.rb_energy_forces(s, box, params, bad, _Stub(modes), 7, H=H, c_q=0.0)
 
 
+@pytest.mark.parametrize("table", ["real_m1", "pairs_plus_real"])
+def test_singular_soe_terms_match_oracle(pk, table):
+    """A mode with |k| within 2e-6 k of a real exponent alpha*s_l takes the
+    reference's analytic-limit branch (soewald2d.py:116-124: c_l = 0, the term's
+    weight through the extra h chain); checked against the oracle, which
+    restates that branch, with forces (both directions) and energies."""
+    rng = np.random.default_rng(33)
+    box = pk.BoxGeometry(12.0, 12.0, 6.0)
+    n = 700
+    s = pk.make_system(np.where(np.arange(n) % 2 == 0, 1.0, -1.0), np.ones(n),
+                       rng.uniform([0, 0, 0.2], [12, 12, 5.8], size=(n, 3)), box)
+    alpha = 0.9
+    params = pk.make_ewald_params(alpha, 3.0, box)
+    if table == "real_m1":
+        w, sv = np.array([1.0 + 0j]), np.array([2.0 + 0j])
+        kc = alpha * 2.0
+    else:
+        b8 = pk.build_soe_contour(8)
+        w = np.concatenate([b8.w, [0.25 + 0j]])
+        sv = np.concatenate([b8.s, [3.5 + 0j]])
+        kc = alpha * 3.5
+    soe = pk.SOEApprox(m=len(w), w=w, s=sv, eps_certified=1.0, domain_max=20.0)
+    other = pk.ModeSampler(alpha, box, seed=5).batch(5)
+    ks = kc * (1.0 + 3e-7)  # singular: |alpha s - k| < 2e-6 k
+    sing = np.array([[ks * 0.6, ks * 0.8, ks], [-ks, 0.0, ks]])
+    modes = np.vstack([other[:2], sing, other[2:]])
+    P = len(modes)
+    H = pk.normalization_H(alpha, box)
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), P, H=H, c_q=0.0)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
+                                (H / P) * (2 / np.sqrt(np.pi)) * alpha, 0.0)
+    _check(bd, f, e_ref, f_ref)
+
+
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
 def test_run_to_run_bit_reproducible(pk, name):
     """Fixed-order sums everywhere (no atomics on values), also with the short
