@@ -196,3 +196,27 @@ def test_status_survives_the_sum_allreduce():
     assert status_of(sum(ranks), summed=True) == 5
     assert status_of(vec(8)) == 8
     assert status_of(sum(vec(0) for _ in range(8)), summed=True) == 0
+
+
+def test_bench_reference_arm_json_line():
+    """bench.py --impl reference (the CPU arm: the C restatement on the host
+    cores) runs without a GPU and prints ONE JSON line with the contract keys."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "cfg2",
+                          "--steps", "1", "--warmup", "0"], cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "cfg2"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
