@@ -84,6 +84,34 @@ def test_single_mode_and_full_sum_small(pk):
     _check(bd, f, e_ref, f_ref)
 
 
+def test_boundary_heights_and_z_ties_match_oracle(pk):
+    """Particles exactly on both walls (z = 0, z = Lz, -0.0), whole layers of
+    equal z (ties resolved by input order, like the reference's stable sort)
+    and charged walls: energies, forces and the permutation against the
+    oracle."""
+    rng = np.random.default_rng(44)
+    box = pk.BoxGeometry(14.0, 14.0, 6.0, sigma_top=0.002, sigma_bot=-0.001)
+    n = 1200
+    pos = rng.uniform([0, 0, 0], [14.0, 14.0, 6.0], size=(n, 3))
+    pos[:40, 2] = 0.0
+    pos[40:60, 2] = -0.0
+    pos[60:100, 2] = 6.0
+    pos[100:400, 2] = np.repeat(rng.uniform(0.5, 5.5, 30), 10)  # 30 layers of 10
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    s = pk.make_system(q, np.ones(n), pos, box)
+    perm = pk.sort_by_z(s, box.lz)
+    np.testing.assert_array_equal(perm, np.argsort(s.pos[:, 2], kind="stable"))
+    params = pk.make_ewald_params(0.8, 3.2, box)
+    soe = pk.build_soe_contour(16)
+    modes = pk.ModeSampler(0.8, box, seed=8).batch(9)
+    H = pk.normalization_H(0.8, box)
+    cq = pk.charge_term_sum(0.8, box, float(np.sum(q ** 2)))
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 9, H=H, c_q=cq)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
+                                (H / 9) * (2 / np.sqrt(np.pi)) * 0.8, cq)
+    _check(bd, f, e_ref, f_ref)
+
+
 @pytest.mark.parametrize("table", ["real_m1", "shuffled_plus_real"])
 def test_real_and_unordered_soe_tables_match_oracle(pk, table):
     """Tables beyond the built contours: the single real-exponent term of the
