@@ -25,6 +25,19 @@ from .core import BoxGeometry, choose_alpha, make_ewald_params, make_system
 
 DENSITY = 0.1
 
+DESCRIPTIONS = {
+    "cfg1": "N=1000 +-1 charges in a 20^3 box, alpha=0.5, r_c=10, full mode set (k <= k_c)",
+    "cfg2": "N=1e4 neutral +-1 charges, Lx=Ly=L, Lz=L/2, density 0.1, RB",
+    "cfg3": "N=1e5 +-1 charges, thin slab Lz=0.1 Lx, exponential wall layers (0.05 Lz), RB",
+    "cfg4": "N=999999 2:1 electrolyte, Lx=Ly=2Lz, density 0.1, RB",
+    "cfg5": "neutral +-1 charges in a cube at density 0.1, RB (throughput sweep)",
+}
+
+
+def describe(name: str) -> str:
+    """One-line recipe of a workload (bench.py's config.workload)."""
+    return DESCRIPTIONS.get(name.split("_")[0], name)
+
 
 @dataclass
 class Workload:
