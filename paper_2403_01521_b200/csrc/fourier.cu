@@ -27,6 +27,7 @@
 //    smem and row-summed (forward and backward lanes separately), accumulated
 //    per warp, then summed over warps in fixed order: deterministic, no atomics.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -1046,6 +1047,10 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   int64_t rf = n * p.ngroups / target_ctas;
   int R = 16;
   while (R * 2 <= rf && R * 2 <= kMaxR) R *= 2;
+  if (const char* env = getenv("SLAB_CHUNK_R")) {  // tuning knob (power of two, 16..256)
+    const int r = atoi(env);
+    if (r >= 16 && r <= kMaxR && (r & (r - 1)) == 0) R = r;
+  }
   // Few items per chunk (a multi-GPU rank's mode slice, small P) means small
   // CTAs whose shared memory -- dominated by the R-particle decay and weight
   // tables -- would cap the SM at a handful of warps: shrink R until both the
