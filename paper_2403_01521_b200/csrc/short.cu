@@ -439,6 +439,19 @@ __global__ void __launch_bounds__(kSRThreads) nbr_cells_kernel(
 // thread: deterministic.
 // KIND 0: erfc Coulomb (alpha); KIND 2: the same with alpha r_c inside the erfcx table
 // (branch-free); KIND 1: WCA core (eps, sig2 = sigma^2).
+#ifndef SLAB_PAIR_WIDE
+#define SLAB_PAIR_WIDE 1
+#endif
+struct __align__(32) Idx8 {
+  int32_t a0, a1, a2, a3, a4, a5, a6, a7;
+};
+struct __align__(32) Rec4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ double4 ld_rec(const double4* p) {  // one 256-bit load
+  const Rec4 r = *reinterpret_cast<const Rec4*>(p);
+  return make_double4(r.x, r.y, r.z, r.w);
+}
 // SPLIT > 1 (small systems, fewer homes than one resident wave of threads):
 // SPLIT consecutive lanes share a home, taking its row's 4-entry blocks round
 // robin, and combine their partial forces with a fixed xor-shuffle tree
@@ -480,6 +493,36 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     const int cnt = active ? nn[a - a_begin] : 0;
     const int32_t* row = nbr + (active ? a - a_begin : 0) * (int64_t)kcap;
     acc.fx = acc.fy = acc.fz = 0.0;
+#if SLAB_PAIR_WIDE
+    // 8 row entries per 256-bit load (rows are 32-byte aligned: kcap is a
+    // multiple of 8) and one 256-bit load per neighbour record: half the L1
+    // requests of 128-bit loads on this L1-bound kernel
+    int k = 8 * sub;
+    for (; k + 8 <= cnt; k += 8 * SPLIT) {
+      const Idx8 j8 = *reinterpret_cast<const Idx8*>(row + k);
+      {
+        const double4 p0 = ld_rec(cp + j8.a0), p1 = ld_rec(cp + j8.a1), p2 = ld_rec(cp + j8.a2),
+                      p3 = ld_rec(cp + j8.a3);
+        PAIR(pi, p0);
+        PAIR(pi, p1);
+        PAIR(pi, p2);
+        PAIR(pi, p3);
+      }
+      {
+        const double4 p0 = ld_rec(cp + j8.a4), p1 = ld_rec(cp + j8.a5), p2 = ld_rec(cp + j8.a6),
+                      p3 = ld_rec(cp + j8.a7);
+        PAIR(pi, p0);
+        PAIR(pi, p1);
+        PAIR(pi, p2);
+        PAIR(pi, p3);
+      }
+    }
+    if (sub == 0)
+      for (k = cnt & ~7; k < cnt; ++k) {
+        const double4 pj = ld_rec(cp + row[k]);
+        PAIR(pi, pj);
+      }
+#else
     int k = 4 * sub;
     for (; k + 4 <= cnt; k += 4 * SPLIT) {
       const int4 j4 = *reinterpret_cast<const int4*>(row + k);
@@ -494,6 +537,7 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
         const double4 pj = cp[row[k]];
         PAIR(pi, pj);
       }
+#endif
 #pragma unroll
     for (int o = 1; o < SPLIT; o <<= 1) {
       acc.fx += __shfl_xor_sync(0xffffffffu, acc.fx, o);
