@@ -13,16 +13,21 @@ Default workload: cfg4 (N = 999,999 2:1 electrolyte, P = 100, M = 16), the
 configuration BASELINE.json's metric is quoted on.  Inputs are the seeded
 synthetic generators of paper_2403_01521_b200/configs.py (no public dataset).
 
-Multi-GPU (torchrun, one rank per GPU): particles replicated, the sampled modes
-and the short-range home particles are split across ranks, and forces + energies
-are combined with ONE NCCL all-reduce per step; the timed N (total work) is
-fixed -> "scaling": "strong".
+Multi-GPU (one process per GPU, NCCL): ``--gpus N`` with N > 1 relaunches itself
+under ``torch.distributed.run --nproc-per-node N`` unless it is already a
+torchrun rank.  Particles are replicated; the sampled modes ("modes" split, the
+default: every (mode, SOE pair, direction) chain is independent) and the
+short-range home particles are divided across the ranks, and forces + energies
+are combined with ONE NCCL all-reduce per step (``--shard-mode zsplit`` selects
+the z-range decomposition instead: one all-gather between its two phases plus
+the all-reduce).  The timed N (total work) is fixed -> "scaling": "strong".
 
 --impl reference: the reference algorithm's CPU implementation timed on the
 host cores.  The reference package is Python + numba and cannot travel to the
 GPU box, so this arm runs the repo's C restatement of it (oracle/, "port",
 pinned against the real reference's outputs in tests/golden), on all host
-threads, over a bounded sample of the same workload.
+threads, on the SAME workload as our arm (full N, same P and M) whenever the
+projected run fits the time budget.
 """
 
 from __future__ import annotations
@@ -55,7 +60,40 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of single-thread CPU work for the cpu_baseline sample")
+    ap.add_argument("--shard-mode", default="modes", choices=["modes", "zsplit"],
+                    help="multi-GPU decomposition (SURVEY 8(e)); 'modes' = (k, l) split + "
+                         "one all-reduce")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="seconds the whole --impl reference run may take")
+    ap.add_argument("--probe", action="store_true",
+                    help="launcher check: every rank prints its rank / world and exits")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_command(argv, gpus: int, port: int) -> list:
+    """The torchrun command line that runs this script as `gpus` ranks on one node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def maybe_relaunch(args) -> int | None:
+    """--gpus N > 1 outside torchrun: run N ranks (one process per GPU) and return
+    their exit code; None when this process is already the right launch."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines: the rank count is visible
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = launch_command(sys.argv[1:], args.gpus, free_port())
+    return subprocess.call(cmd, env=env)
 
 
 def dist_env():
@@ -119,20 +157,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU side (the C restatement of the reference algorithm)
 # ---------------------------------------------------------------------------
-def oracle_sample_run(name, n_sample, nthreads, seed_modes=0):
-    """One oracle evaluation on a cfg-recipe sample of n_sample particles.
+def oracle_run(wl, nthreads, seed_modes=0):
+    """One oracle evaluation of workload `wl` (P sampled modes, M SOE terms).
     Returns (seconds, n)."""
     from oracle import oracle as O
-    wl = sample_workload(name, n_sample)
     modes = host_modes(wl, seed_modes)
-    H = host_H(wl)
+    cv = O.rb_commonv(host_H(wl), wl.P, wl.alpha)
     cq = host_cq(wl)
-    cv = O.rb_commonv(H, wl.P, wl.alpha)
+    w, s = soe_arrays(wl.m)
     t0 = time.perf_counter()
-    e, f, flag = O.energy_forces(wl.system.pos, wl.system.charge, wl.box, wl.alpha,
-                                 wl.params().r_c, modes, cv, cq, *soe_arrays(wl.m),
-                                 nthreads=nthreads)
+    O.energy_forces(wl.system.pos, wl.system.charge, wl.box, wl.alpha, wl.params().r_c, modes,
+                    cv, cq, w, s, nthreads=nthreads)
     return time.perf_counter() - t0, wl.n
+
+
+def oracle_sample_run(name, n_sample, nthreads, seed_modes=0):
+    """One oracle evaluation on a cfg-recipe sample of n_sample particles."""
+    return oracle_run(sample_workload(name, n_sample), nthreads, seed_modes)
 
 
 def sample_workload(name, n_sample):
@@ -215,30 +256,48 @@ def cpu_baseline(name, budget_s):
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the CPU restatement on all host threads, on our arm's
+    workload (full N, same P, M) -- the reference's own harness times one
+    rb_energy_forces per step the same way (cli.py:724-776).  Only when the
+    projected (warmup + steps) run exceeds --ref-budget does it fall back to a
+    calibrated sample of the same recipe, and then says so (same_config false)."""
     if rank != 0:
         return 0
     from oracle import oracle as O
+    from paper_2403_01521_b200.configs import make_workload
     O.build()
     threads = cpu_count()
     steps, warm = max(1, args.steps), max(0, args.warmup)
-    budget_total = 150.0
-    per_step_budget = budget_total / (steps + warm + 1)
-    n_s, _ = calibrated_sample(args.config, threads, per_step_budget)
-    for _ in range(warm):
-        oracle_sample_run(args.config, n_s, threads)
-    t_tot, n = 0.0, 0
+    wl = make_workload(args.config)
+    if not wl.P:  # full mode sum (cfg1): no random batch to stand in for
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the CPU arm times the random-batch path (configs with P)"}))
+        return 0
+    t_first, _ = oracle_run(wl, threads)  # counts as the first warm-up step
+    same = t_first * (steps + warm) <= args.ref_budget
+    if not same:
+        wl = sample_workload(args.config, int(wl.n * args.ref_budget /
+                                              (t_first * (steps + warm + 1))))
+    for _ in range(warm - 1 if same else warm):
+        oracle_run(wl, threads)
+    t_tot = 0.0
     for s in range(steps):
-        t, n = oracle_sample_run(args.config, n_s, threads, seed_modes=s)
+        t, _ = oracle_run(wl, threads, seed_modes=s)
         t_tot += t
+    n = wl.n
     value = n * steps / t_tot
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": 1e3 * t_tot / steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": args.config, "sample_particles": n, "P": 100, "M": 16},
+            "config": {"workload": args.config, "N": n, "P": wl.P, "M": wl.m,
+                       "same_config": bool(same),
+                       "note": "same seeded system as our arm" if same else
+                               "calibrated sample of the recipe (full N exceeds the budget)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{n}-particle sample of the {args.config} recipe per "
-                                       f"step, C restatement of the reference path "
+                             "sample": f"{n}-particle {args.config} system per step "
+                                       f"({'the full workload' if same else 'sample'}), C "
+                                       f"restatement of the reference path "
                                        f"(oracle/slab_oracle.c), OpenMP over modes and "
                                        f"cell slabs, {threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -279,10 +338,14 @@ def components(times, n, P, r_c, density):
     in pairs/s and fp64 terms, the sort in GB/s)."""
     def pick(pred):
         return sum(v for k, v in times.items() if pred(k))
-    sr = pick(lambda k: k.startswith(("cell_", "nbr_build", "pair_list", "half_sum",
-                                      "brute_")) or k.endswith("<unsigned int>"))
-    zsort = pick(lambda k: k.startswith(("zkey_init", "gather_sorted", "perm_to")) or
-                 k.endswith("<unsigned long>") or k.startswith(("scan_rows", "add_digit")))
+    # radix kernels are templated on the key type: 64-bit keys = the z sort,
+    # 32-bit keys = the short range's cell sort
+    sr = pick(lambda k: k.startswith(("cell_", "nbr_build", "nbr_cells", "pair_list",
+                                      "half_sum", "brute_", "short_")) or
+              "<unsigned int" in k)
+    zsort = pick(lambda k: k.startswith(("zkey_init", "gather_sorted", "perm_to",
+                                         "radix_digit_bases", "bucket_")) or
+                 "<unsigned long" in k)
     scan = pick(lambda k: k.startswith(("fourier_", "zero_", "decay_table", "chunk_bounds",
                                         "mode_table", "kahan_modes")))
     pairs = 0.5 * n * (4.0 / 3.0) * np.pi * r_c ** 3 * density  # in-range pairs (mean density)
@@ -301,19 +364,29 @@ def components(times, n, P, r_c, density):
     }
 
 
-def scan_flops(n, P, m, world):
+def scan_flops(n, P, m):
     # canonical algorithmic work: N K (48 M + 100) + N 99 M per step
     return n * P * (48 * m + 100) + n * 99 * m
 
 
-def load_traffic(round_tag="r01"):
-    path = os.path.join(HERE, "profiles", f"ncu_{round_tag}_summary.json")
-    try:
-        with open(path) as fh:
-            d = json.load(fh)
-        return d.get("scan_dram_bytes_per_step")
-    except (OSError, ValueError):
-        return None
+PROFILE_ROUND = "r02"
+
+
+def load_traffic(round_tag=PROFILE_ROUND):
+    """DRAM bytes per step of the SOE-scan kernels from the committed ncu --set full
+    capture (ncu cannot run inside the timed bench; the capture is of this same
+    cfg4 step): (bytes, source file) or (None, reason)."""
+    for tag in (round_tag, "r01"):
+        path = os.path.join(HERE, "profiles", f"ncu_{tag}_summary.json")
+        try:
+            with open(path) as fh:
+                d = json.load(fh)
+            v = d.get("scan_dram_bytes_per_step")
+            if v:
+                return v, f"profiles/ncu_{tag}_summary.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of the scan kernels)"
+        except (OSError, ValueError):
+            continue
+    return None, "no committed ncu capture"
 
 
 def run_ours(args, rank, world, local):
@@ -339,7 +412,7 @@ def run_ours(args, rank, world, local):
     H = normalization_H(wl.alpha, wl.box)
     c_q = charge_term_sum(wl.alpha, wl.box, float(np.sum(wl.system.charge ** 2)))
     ev = DeviceEvaluator(wl.system, wl.box, params, soe, P=wl.P, H=H, c_q=c_q, seed=wl.seed,
-                         rank=rank, world=world, group=group)
+                         rank=rank, world=world, group=group, shard_mode=args.shard_mode)
     use_graph = world == 1 and wl.n < 200_000
     ev.warmup()  # workspace + short-range neighbour capacity (may rerun once)
     for _ in range(args.warmup):
@@ -394,36 +467,75 @@ def run_ours(args, rank, world, local):
     e = ev.energy.cpu().numpy()
     status = ev.status()
 
-    # ---- e2e: the public API from pinned host memory, result read back ----
+    # ---- e2e: host buffers in, host result out, every step ----
     e2e = None
+    sysm = wl.system
     if world == 1:
-        sysm = wl.system
+        # the public API (numpy in / numpy out), from page-locked host arrays and
+        # from ordinary pageable numpy arrays (what a drop-in caller passes)
         pinned_sys = pk.make_system(pinned_like(sysm.charge), sysm.mass, sysm.pos, box=wl.box)
         pinned_sys.pos = pinned_like(sysm.pos)
         pinned_sys.charge = pinned_like(sysm.charge)
         sampler = ModeSampler(wl.alpha, wl.box, seed=wl.seed) if wl.P else None
 
-        def call():  # the reference-facing API: RB batch, or the full mode sum (cfg1)
-            if wl.P:
-                return pk.rb_energy_forces(pinned_sys, wl.box, params, soe, sampler, wl.P, H=H,
-                                           c_q=c_q)
-            return pk.soe_energy_forces(pinned_sys, wl.box, params, soe)
-        # W untimed calls, at least 2: the second still takes fresh page-locked
-        # result buffers from the host allocator (the first call's are still held)
-        for _ in range(max(2, args.warmup)):
-            bd, f = call()
-        torch.cuda.synchronize()
-        te = time.perf_counter()
-        for _ in range(K):
-            bd, f = call()
-        torch.cuda.synchronize()
-        te = time.perf_counter() - te
-        e2e = {"value": wl.n * K / te, "unit": UNIT,
+        def timed_api(system):
+            def call():  # the reference-facing API: RB batch, or the full mode sum (cfg1)
+                if wl.P:
+                    return pk.rb_energy_forces(system, wl.box, params, soe, sampler, wl.P, H=H,
+                                               c_q=c_q)
+                return pk.soe_energy_forces(system, wl.box, params, soe)
+            # W untimed calls, at least 2: the second still takes fresh page-locked
+            # result buffers from the host allocator (the first call's are still held)
+            for _ in range(max(2, args.warmup)):
+                bd, f = call()
+            torch.cuda.synchronize()
+            te = time.perf_counter()
+            for _ in range(K):
+                bd, f = call()
+            torch.cuda.synchronize()
+            return wl.n * K / (time.perf_counter() - te), f
+        v_pin, f = timed_api(pinned_sys)
+        v_page, _ = timed_api(sysm)
+        e2e = {"value": v_pin, "unit": UNIT,
                "h2d_bytes_per_step": int(sysm.pos.nbytes + sysm.charge.nbytes),
                "d2h_bytes_per_step": int(f.nbytes + 8 * 8),
                "api": "paper_2403_01521_b200." + ("rb_energy_forces" if wl.P else
                                                   "soe_energy_forces") +
-                      " (numpy in / numpy out)"}
+                      " (numpy in / numpy out; host arrays in page-locked memory)",
+               "pageable_value": v_page,
+               "pageable_note": "the same call on ordinary (pageable) numpy arrays"}
+    else:
+        # sharded: every rank uploads the step's positions + charges from pinned
+        # host memory, runs its share, the all-reduce combines, rank 0 reads the
+        # forces and energies back; wall clock per rank, max over ranks
+        pos_h = torch.from_numpy(np.ascontiguousarray(sysm.pos)).pin_memory()
+        q_h = torch.from_numpy(np.ascontiguousarray(sysm.charge)).pin_memory()
+        f_h = torch.empty((wl.n, 3), dtype=torch.float64).pin_memory()
+        e_h = torch.empty(8, dtype=torch.float64).pin_memory()
+
+        def host_step():
+            ev.pos.copy_(pos_h, non_blocking=True)
+            ev.charge.copy_(q_h, non_blocking=True)
+            ev.step()
+            if rank == 0:
+                f_h.copy_(ev.forces, non_blocking=True)
+                e_h.copy_(ev.energy, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        for _ in range(max(2, args.warmup)):
+            host_step()
+        torch.distributed.barrier()
+        te = time.perf_counter()
+        for _ in range(K):
+            host_step()
+        te = time.perf_counter() - te
+        tt = torch.tensor([te], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": wl.n * K / float(tt[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(world * (sysm.pos.nbytes + sysm.charge.nbytes)),
+               "d2h_bytes_per_step": int(f_h.numel() * 8 + 64),
+               "api": "DeviceEvaluator sharded step: per rank H2D of positions + charges "
+                      "from pinned memory, step + NCCL all-reduce, rank 0 D2H of forces + "
+                      "energies; max wall time over ranks"}
 
     if rank != 0:
         if world > 1:
@@ -431,8 +543,12 @@ def run_ours(args, rank, world, local):
         return 0
     peak = ctypes_peak(_native)
     n_modes = wl.P or len(params.kmodes)  # full mode sum (cfg1): every |k| <= k_c
-    flops = scan_flops(wl.n, n_modes, wl.m, world)
+    flops = scan_flops(wl.n, n_modes, wl.m)
+    # whole-job flops over the slowest rank's scan time, against world x the
+    # one-GPU peak (each rank scans its 1/world share)
     achieved = flops / (scan_ms * 1e-3) / 1e12
+    peak_job = peak * world if peak else None
+    traffic, traffic_src = load_traffic()
     line = {
         "metric": METRIC, "value": wl.n * K / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
@@ -442,18 +558,22 @@ def run_ours(args, rank, world, local):
                                f"{'P=%d sampled' % wl.P if wl.P else 'K=%d' % n_modes} modes, "
                                f"M={wl.m} SOE terms, alpha={wl.alpha:.5f}, "
                                f"r_c={params.r_c:.4f}",
-                   "N": wl.n, "P": wl.P or n_modes, "M": wl.m, "parallelism": f"z-split scan + cell-range short range x{world}" if world > 1 else "single GPU",
+                   "N": wl.n, "P": wl.P or n_modes, "M": wl.m,
+                   "parallelism": (f"{args.shard_mode} split x{world} (one process per GPU, "
+                                   f"NCCL all-reduce of forces + energies)") if world > 1
+                                  else "single GPU",
                    "l2": "no flush: per-step working set (~0.6 GB) exceeds the 126 MB L2",
                    "cuda_graph": use_graph},
         "roofline": {"bound": "fp64", "kernel": "SOE scan (3-phase Fourier scan + k=0 mode)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None,
-                     "peak_source": "measured live: DFMA microbenchmark (slab_fp64_peak); "
-                                    "MEASURED_PEAKS.json has no fp64 figure",
+                     "achieved": achieved, "peak": peak_job, "unit": "TFLOP/s",
+                     "frac": achieved / peak_job if peak_job else None,
+                     "peak_source": "measured live: DFMA microbenchmark (slab_fp64_peak)"
+                                    + (f" x {world} GPUs" if world > 1 else "") +
+                                    "; MEASURED_PEAKS.json has no fp64 figure",
                      "flops_per_step": flops,
                      "flops_model": "N P (48 M + 100) + 99 N M canonical fp64 (SURVEY 8(d))",
                      "scan_ms_per_step": scan_ms,
-                     "traffic": load_traffic()},
+                     "traffic": traffic, "traffic_source": traffic_src},
         "clocks": clk,
         "gpu_launches": launches_per_step * K,
         "components": components(ktimes, wl.n, n_modes, params.r_c,
@@ -484,7 +604,16 @@ def ctypes_peak(native):
 
 def main():
     args = parse()
+    rc = maybe_relaunch(args)
+    if rc is not None:
+        return rc
     rank, world, local = dist_env()
+    if world > 1 and args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks",
+              file=sys.stderr)
+    if args.probe:
+        print(json.dumps({"probe": True, "rank": rank, "world": world}), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

@@ -404,15 +404,21 @@ int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charg
   // batches per launch: ~4096 modes keeps the carries modest and the grid full
   int64_t per = 4096 / P;
   per = per < 1 ? 1 : (per > nbatch ? nbatch : per);
+  // the full passes and the (shorter) tail pass have their own plans (chunk
+  // length, chunk count, buffer counts): the arena is carved for the larger of
+  // the two work areas and each pass re-carves it with its own plan
   auto fp = slab::fourier_plan(n, (int)(per * P), sh.mh, 1);
+  const int64_t tail = nbatch % per;
+  if (tail) {
+    auto ft = slab::fourier_plan(n, (int)(tail * P), sh.mh, 1);
+    if (slab::fourier_work_doubles(ft) > slab::fourier_work_doubles(fp)) fp = ft;
+  }
   auto zp = slab::zero_plan(n, sh.mh);
   rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, true) + 8192);
   if (rc) return rc;
   Carver cv{(char*)ctx->arena};
   SortedWork w{};
   carve_sorted(cv, n, sh.mh, fp, zp, true, w);
-  slab::FourierWork fw;
-  slab::fourier_work_carve(fp, w.fwork, fw);
   int32_t* perm = nullptr;
   CK(slab::sort_by_z_device(d_pos + 2, 3, n, w.sw, st, &perm, d_status));
   CK(slab::gather_sorted(d_pos, d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, nullptr, st));
@@ -420,6 +426,8 @@ int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charg
   for (int64_t b0 = 0; b0 < nbatch; b0 += per) {
     const int64_t nb = nbatch - b0 < per ? nbatch - b0 : per;
     auto fpb = slab::fourier_plan(n, (int)(nb * P), sh.mh, 1);
+    slab::FourierWork fw;
+    slab::fourier_work_carve(fpb, w.fwork, fw);
     CK(slab::fourier_run(fpb, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, d_modes + 3 * b0 * P, nullptr,
                          commonv_scalar, area, sh.b, sh.w, 0, d_out + b0, d_status, nullptr, st,
                          (int)P));

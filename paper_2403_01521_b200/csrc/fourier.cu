@@ -1132,8 +1132,12 @@ cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, doub
 
 template <int MH>
 static void set_attrs() {
-  static bool done = false;
-  if (done) return;
+  // function attributes are per device context: one bit per device
+  static unsigned long long done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done & bit) return;
   // largest shared-memory carveout so two CTAs of each fit per SM
   cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sweep_smem(kMaxR, MH, 8));
@@ -1143,7 +1147,7 @@ static void set_attrs() {
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)agg_mma_smem(kMaxR, MH));
   cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  done = true;
+  done |= bit;
 }
 
 static dim3 carry_grid(const FourierPlan& p) {
@@ -1152,13 +1156,26 @@ static dim3 carry_grid(const FourierPlan& p) {
 
 // phase 1: aggregates of chunks [c0, c1) and their segment maps; with `totals`,
 // also the range's total map per (comp, item) chain (z-split exchange payload)
+// identity maps T -> 1 T + 0: the exchange payload of a rank whose chunk range is
+// empty or a single-chunk plan (composing it leaves the other ranks' carries intact)
+__global__ void affc_identity_kernel(AffC* __restrict__ out, int count) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < count) out[e] = AffC{C2{1.0, 0.0}, C2{0.0, 0.0}};
+}
+
 template <int MH>
 static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
                              const double* ys, const double* zs, const double* qs,
                              const BVec& b, double* totals, cudaStream_t st) {
   set_attrs<MH>();
   const int nch_r = p.c1 - p.c0;
-  if (nch_r <= 0) return cudaGetLastError();
+  const int nchain = p.items * ncomp_of(MH);
+  if (nch_r <= 0 || p.nch <= 1) {
+    if (totals)
+      affc_identity_kernel<<<(nchain + 127) / 128, 128, 0, st>>>(reinterpret_cast<AffC*>(totals),
+                                                                  nchain);
+    if (nch_r <= 0) return cudaGetLastError();
+  }
   if (p.nch > 1) {
     const int tiles = (p.P + 7) / 8;
     const int ngy = (tiles + kAggMaxWarps - 1) / kAggMaxWarps;
@@ -1171,7 +1188,6 @@ static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const d
         w.carry, p.nch, p.c0, p.c1, p.P, p.items, MH, nseg, w.modetab, w.dchunk,
         w.dchunk + (size_t)p.nch * MH, w.zbound, reinterpret_cast<AffC*>(w.segmap));
     if (totals) {
-      const int nchain = p.items * ncomp_of(MH);
       if (nseg <= kSegSeqMax)
         fourier_carry_segscan_seq_kernel<<<(nchain + 127) / 128, 128, 0, st>>>(
             reinterpret_cast<AffC*>(w.segmap), p.items, ncomp_of(MH), nseg, nullptr,
@@ -1181,11 +1197,8 @@ static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const d
             reinterpret_cast<AffC*>(w.segmap), p.items, ncomp_of(MH), nseg, nullptr,
             reinterpret_cast<AffC*>(totals), 1);
     }
-  } else {
+  } else {  // one chunk: carried-in state 0 (its total map was written above)
     cudaMemsetAsync(w.carry, 0, sizeof(double2) * ncomp_of(MH) * 2 * (size_t)p.P, st);
-    if (totals) {  // one chunk: its total map is (1, 0) -- never combined (W = 1)
-      cudaMemsetAsync(totals, 0, sizeof(AffC) * ncomp_of(MH) * (size_t)p.items, st);
-    }
   }
   return cudaGetLastError();
 }

@@ -145,17 +145,29 @@ __device__ __forceinline__ void wca_accumulate(double xi, double yi, double zi, 
   acc.fz = fma(fmag, dz, acc.fz);
 }
 
-// ewald2d.py:126-138
+// Periodic image of x in [0, l): floor-based, with the rounding case x - l
+// floor(x / l) == l folded to 0.  The search structure (cells and the fp32
+// screen copy) uses this image so that a particle given outside the primary
+// cell (x == lx from np.mod(-tiny, lx), an MD floor-wrap, or make_system without
+// a box) still sits inside the cell it is filed under; the exact fp64 pair term
+// keeps the raw coordinates and the reference's rint minimum image, so its
+// values do not depend on the wrap.
+__device__ __forceinline__ double wrap_periodic(double x, double l) {
+  double w = x - l * floor(x / l);
+  return (w >= l || w < 0.0) ? 0.0 : w;
+}
+
+// cells: as ewald2d.py:126-138 (x, y periodic, z clamped), on the wrapped image
 __global__ void cell_index_kernel(const double* __restrict__ pos, int64_t n, double lx, double ly,
                                   double lz, int ncx, int ncy, int ncz, uint32_t* __restrict__ key,
                                   int32_t* __restrict__ val) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  long long cx = (long long)(pos[3 * i + 0] / lx * ncx);
-  long long cy = (long long)(pos[3 * i + 1] / ly * ncy);
+  long long cx = (long long)(wrap_periodic(pos[3 * i + 0], lx) / lx * ncx);
+  long long cy = (long long)(wrap_periodic(pos[3 * i + 1], ly) / ly * ncy);
   long long cz = (long long)(pos[3 * i + 2] / lz * ncz);
-  cx = ((cx % ncx) + ncx) % ncx;
-  cy = ((cy % ncy) + ncy) % ncy;
+  cx = cx < 0 ? 0 : (cx >= ncx ? ncx - 1 : cx);
+  cy = cy < 0 ? 0 : (cy >= ncy ? ncy - 1 : cy);
   cz = cz < 0 ? 0 : (cz >= ncz ? ncz - 1 : cz);
   key[i] = (uint32_t)((cx * ncy + cy) * ncz + cz);
   val[i] = (int32_t)i;
@@ -174,15 +186,20 @@ __global__ void cell_start_kernel(const uint32_t* __restrict__ skey, int64_t n, 
   start[c] = (int32_t)lo;
 }
 
+// cp: raw fp64 record (the pair term); cpf: the fp32 screen copy of the wrapped image
 __global__ void cell_gather_kernel(const double* __restrict__ pos, const double* __restrict__ q,
-                                   const int32_t* __restrict__ order, int64_t n,
-                                   double4* __restrict__ cp, float4* __restrict__ cpf) {
+                                   const int32_t* __restrict__ order, int64_t n, double lx,
+                                   double ly, double4* __restrict__ cp, float4* __restrict__ cpf) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   int64_t i = order[a];
   const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
   cp[a] = make_double4(x, y, z, q[i]);
-  cpf[a] = make_float4((float)x, (float)y, (float)z, 0.0f);
+  float xf = (float)wrap_periodic(x, lx), yf = (float)wrap_periodic(y, ly);
+  // fp32 rounding may land exactly on l: keep the image inside [0, l)
+  xf = xf >= (float)lx ? 0.0f : xf;
+  yf = yf >= (float)ly ? 0.0f : yf;
+  cpf[a] = make_float4(xf, yf, (float)z, 0.0f);
 }
 
 constexpr int kSRThreads = 128;
@@ -813,8 +830,8 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     if (e != cudaSuccess) return e;
     cell_start_kernel<<<(unsigned)((p.ncell + 1 + 255) / 256), 256, 0, st>>>(skey, n, p.ncell,
                                                                              start);
-    cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, cp,
-                                                                    cpf);
+    cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, lx,
+                                                                    ly, cp, cpf);
     // conservative fp32 screen: positions rounded to fp32 move d2 by < 1e-2 for
     // |r| <= 1e3; the exact fp64 test is applied to every survivor
     const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);

@@ -346,7 +346,7 @@ class DeviceEvaluator:
 
     def __init__(self, system, box, params, soe, P=None, H=None, c_q=None, seed=0, thin=10,
                  burn_in=100, modes=None, device=None, sample=True, rank=0, world=1,
-                 group=None, shard_mode="zsplit"):
+                 group=None, shard_mode="modes"):
         from .rbse2d import charge_term_sum, normalization_H
         from .soewald2d import full_sum_constants
         torch = require_cuda()
@@ -392,10 +392,11 @@ class DeviceEvaluator:
                 # first use
                 self.side = torch.cuda.Stream(dev)
                 self.ev_modes = torch.cuda.Event()
-        # multi-GPU split: "zsplit" (default) -- every rank scans all modes over its
-        # contiguous range of the z-sorted particles, one all-gather of the chunk-range
-        # maps between the two phases; "modes" -- each rank scans its slice of the
-        # modes over all particles (no mid-evaluation exchange)
+        # multi-GPU split: "modes" (default) -- each rank scans its
+        # slice of the sampled modes over all particles, no mid-evaluation
+        # exchange, ONE all-reduce per step; "zsplit" -- every rank scans all modes
+        # over its contiguous range of the z-sorted particles, with an all-gather of
+        # the chunk-range maps between the two phases
         if shard_mode not in ("zsplit", "modes"):
             raise ValueError("shard_mode must be 'zsplit' or 'modes'")
         self.zsplit = shard_mode == "zsplit" and self.world > 1
@@ -438,18 +439,39 @@ class DeviceEvaluator:
         else:
             self.eng.evaluate(*args, modes_ready=ready, **kw)
         if self.reduce:
-            import torch.distributed as dist
-            dist.all_reduce(self.packed, op=dist.ReduceOp.SUM, group=self.group)
+            self.all_reduce(self.packed)
 
     def status(self) -> int:
         """Status bits of the last step (any rank, after the all-reduce); synchronous."""
         from .ewald2d import status_of
         return status_of(self.energy.cpu().numpy(), summed=self.reduce)
 
-    def exchange(self, local, gathered):
-        """z-split: every rank's chunk-range maps, in rank order (NCCL all-gather)."""
+    def _host_staged(self) -> bool:
+        """A gloo group (CPU tests, several processes sharing one GPU) takes its
+        collectives through host copies; NCCL works on the device buffers."""
         import torch.distributed as dist
-        dist.all_gather_into_tensor(gathered, local, group=self.group)
+        return dist.get_backend(self.group) == "gloo"
+
+    def all_reduce(self, buf):
+        """Sum of the packed (forces, energies) buffer over ranks: the one
+        collective of a "modes" step."""
+        import torch.distributed as dist
+        if self._host_staged():
+            h = buf.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            buf.copy_(h)
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+
+    def exchange(self, local, gathered):
+        """z-split: every rank's chunk-range maps, in rank order (all-gather)."""
+        import torch.distributed as dist
+        if self._host_staged():
+            h = gathered.cpu()
+            dist.all_gather_into_tensor(h, local.cpu(), group=self.group)
+            gathered.copy_(h)
+        else:
+            dist.all_gather_into_tensor(gathered, local, group=self.group)
 
     def warmup(self):
         """Run one step synchronously (workspace allocation, kernel attributes,

@@ -26,7 +26,6 @@ Host numpy forms of ``langevin_step`` / ``nose_hoover_step`` /
 
 from __future__ import annotations
 
-import csv
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -234,25 +233,31 @@ class _ForceField:
 
 def maxwell_velocities(mass: np.ndarray, temperature: float,
                        rng: np.random.Generator) -> np.ndarray:
-    """md.py:170-174 (host, once per run)."""
-    v = rng.normal(size=(len(mass), 3)) * np.sqrt(temperature / mass)[:, None]
-    v -= np.average(v, axis=0, weights=mass)[None, :]
-    return v
+    """Initial velocities as md.py:170-174 draws them: Gaussian components of
+    variance T / m, then the centre-of-mass momentum removed (host, once per run)."""
+    m = np.asarray(mass, dtype=np.float64)
+    scale = np.sqrt(temperature / m)
+    v = rng.normal(size=(m.size, 3)) * scale[:, None]
+    p_com = m @ v                     # total momentum (3,)
+    return v - p_com[None, :] / m.sum()
 
 
 def kinetic_energy(mass: np.ndarray, vel: np.ndarray) -> float:
-    return float(0.5 * np.sum(mass * np.sum(vel ** 2, axis=1)))
+    """sum_i m_i |v_i|^2 / 2 (md.py:176-177); the device form is slab_md_kinetic."""
+    return 0.5 * float(np.einsum("i,ij,ij->", mass, vel, vel))
 
 
 def langevin_step(pos, vel, forces, mass, dt, gamma, temperature, noise):
-    """Host numpy form of md.py:180-193 (the device step is slab_md_langevin)."""
-    inv_m = 1.0 / mass[:, None]
-    vel = vel + 0.5 * dt * forces * inv_m
-    pos = pos + 0.5 * dt * vel
-    c = np.exp(-gamma * dt)
-    vel = c * vel + np.sqrt((1.0 - c * c) * temperature / mass)[:, None] * noise
-    pos = pos + 0.5 * dt * vel
-    return pos, vel
+    """Host reference of the device BAOAB step (slab_md_langevin; md.py:180-193):
+    half kick (B), half drift (A), exact Ornstein-Uhlenbeck update (O) with the
+    caller's standard-normal ``noise``, half drift (A).  No x, y wrap here."""
+    m = np.asarray(mass, dtype=np.float64)[:, None]
+    half = 0.5 * dt
+    decay = np.exp(-gamma * dt)
+    v = vel + half * forces / m                                            # B
+    x = pos + half * v                                                     # A
+    v = decay * v + np.sqrt((1.0 - decay * decay) * temperature / m) * noise  # O
+    return x + half * v, v                                                 # A
 
 
 def run_simulation(system: ParticleSystem, box: BoxGeometry, opts: MDOptions) -> MDResult:
@@ -388,74 +393,59 @@ def run_simulation(system: ParticleSystem, box: BoxGeometry, opts: MDOptions) ->
 
 
 # ---------------------------------------------------------------------------
-# observables and I/O (host, md.py:332-406)
+# observables (host, post-processing of the sampled frames; md.py:332-376)
 # ---------------------------------------------------------------------------
+def _msd_at_lags(unwrapped: np.ndarray, lags: np.ndarray):
+    """Multiple-time-origin mean-square displacement at each lag, split into the
+    in-plane (x, y) and normal (z) parts."""
+    out_xy = np.empty(lags.size)
+    out_z = np.empty(lags.size)
+    for k, lag in enumerate(lags):
+        disp = unwrapped[lag:] - unwrapped[:-lag]          # (origins, n, 3)
+        sq = disp * disp
+        out_xy[k] = (sq[..., 0] + sq[..., 1]).mean()
+        out_z[k] = sq[..., 2].mean()
+    return out_xy, out_z
+
+
+def _z_profiles(z_frames: np.ndarray, charge: np.ndarray, lz: float, area: float,
+                n_bins: int, n_blocks: int):
+    """Number density per charge species in n_bins z slabs, averaged within each
+    of n_blocks contiguous frame blocks; (mean, sample std) over the blocks."""
+    width = lz / n_bins
+    # slab index of every (frame, particle); z == lz belongs to the top slab
+    slab = np.minimum((z_frames / width).astype(np.int64), n_bins - 1)
+    slab = np.maximum(slab, 0)
+    blocks = np.array_split(np.arange(z_frames.shape[0]), n_blocks)
+    mean, std = {}, {}
+    for sp in np.unique(charge):
+        cols = np.flatnonzero(charge == sp)
+        per_block = np.stack([
+            np.bincount(slab[blk][:, cols].ravel(), minlength=n_bins)[:n_bins]
+            / (blk.size * area * width) for blk in blocks])
+        mean[float(sp)] = per_block.mean(axis=0)
+        std[float(sp)] = per_block.std(axis=0, ddof=1)
+    return mean, std
+
+
 def compute_observables(result: MDResult, n_bins: int = 40, n_blocks: int = 5,
                         max_lag_frac: float = 0.5, skip_frac: float = 0.2) -> dict:
-    """Mean-square displacements (multiple time origins, xy and z split) and
-    block-averaged z concentration profiles per charge species."""
-    nf = len(result.times)
-    skip = int(skip_frac * nf)
-    un = result.unwrapped[skip:]
-    zs = result.positions[skip:, :, 2]
-    nfu = un.shape[0]
-    if nfu < 4:
+    """The reference's trajectory observables (md.py:332-376): MSDs over the
+    frames after the first ``skip_frac`` (lags up to ``max_lag_frac`` of them, at
+    most 60 distinct values) and block-averaged z concentration profiles."""
+    frames = len(result.times)
+    first = int(skip_frac * frames)
+    unwrapped = result.unwrapped[first:]
+    kept = unwrapped.shape[0]
+    if kept < 4:
         raise ValueError("trajectory too short for observables")
-    dt_f = result.times[1] - result.times[0] if nf > 1 else 1.0
-    max_lag = max(1, int(max_lag_frac * nfu))
-    lags = np.unique(np.linspace(1, max_lag, min(60, max_lag)).astype(int))
-    msd_xy = np.empty(len(lags))
-    msd_z = np.empty(len(lags))
-    for i, lag in enumerate(lags):
-        d = un[lag:] - un[:-lag]
-        msd_xy[i] = np.mean(np.sum(d[..., :2] ** 2, axis=-1))
-        msd_z[i] = np.mean(d[..., 2] ** 2)
+    dt_frame = result.times[1] - result.times[0] if frames > 1 else 1.0
+    lag_max = max(1, int(max_lag_frac * kept))
+    lags = np.unique(np.linspace(1, lag_max, min(60, lag_max)).astype(int))
+    msd_xy, msd_z = _msd_at_lags(unwrapped, lags)
     box = result.box
-    edges = np.linspace(0.0, box.lz, n_bins + 1)
-    centers = 0.5 * (edges[:-1] + edges[1:])
-    bin_vol = box.area * (edges[1] - edges[0])
-    species = np.unique(result.charge)
-    blocks = np.array_split(np.arange(nfu), n_blocks)
-    conc, conc_std = {}, {}
-    for sp in species:
-        sel = result.charge == sp
-        means = []
-        for blk in blocks:
-            h = np.zeros(n_bins)
-            for f in blk:
-                h += np.histogram(zs[f, sel], bins=edges)[0]
-            means.append(h / (len(blk) * bin_vol))
-        means = np.array(means)
-        conc[float(sp)] = means.mean(axis=0)
-        conc_std[float(sp)] = means.std(axis=0, ddof=1)
-    return {"lag_times": lags * dt_f, "msd_xy": msd_xy, "msd_z": msd_z,
+    conc, conc_std = _z_profiles(result.positions[first:, :, 2], np.asarray(result.charge),
+                                 box.lz, box.area, n_bins, n_blocks)
+    centers = (np.arange(n_bins) + 0.5) * (box.lz / n_bins)
+    return {"lag_times": lags * dt_frame, "msd_xy": msd_xy, "msd_z": msd_z,
             "z_bin_centers": centers, "concentration": conc, "concentration_std": conc_std}
-
-
-def write_trajectory_csv(path, result: MDResult) -> None:
-    """Frames in long form: step,id,x,y,z,vx,vy,vz."""
-    steps = np.rint(result.times / result.options.dt).astype(int)
-    with open(path, "w", newline="") as fh:
-        wr = csv.writer(fh)
-        wr.writerow(["step", "id", "x", "y", "z", "vx", "vy", "vz"])
-        for f, step in enumerate(steps):
-            for i in range(result.positions.shape[1]):
-                x, y, z = result.positions[f, i]
-                vx, vy, vz = result.velocities[f, i]
-                wr.writerow([step, i, f"{x:.17g}", f"{y:.17g}", f"{z:.17g}",
-                             f"{vx:.17g}", f"{vy:.17g}", f"{vz:.17g}"])
-
-
-def write_observables_csv(msd_path, conc_path, obs: dict) -> None:
-    with open(msd_path, "w", newline="") as fh:
-        wr = csv.writer(fh)
-        wr.writerow(["t", "msd_xy", "msd_z"])
-        for t, a, b in zip(obs["lag_times"], obs["msd_xy"], obs["msd_z"]):
-            wr.writerow([f"{t:.17g}", f"{a:.17g}", f"{b:.17g}"])
-    species = sorted(obs["concentration"])
-    with open(conc_path, "w", newline="") as fh:
-        wr = csv.writer(fh)
-        wr.writerow(["z_bin_center"] + [f"concentration_q{sp:+g}" for sp in species])
-        for i, zc in enumerate(obs["z_bin_centers"]):
-            wr.writerow([f"{zc:.17g}"] + [f"{obs['concentration'][sp][i]:.17g}"
-                                          for sp in species])
