@@ -195,10 +195,11 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
   int64_t i = order[a];
   const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
   cp[a] = make_double4(x, y, z, q[i]);
-  float xf = (float)wrap_periodic(x, lx), yf = (float)wrap_periodic(y, ly);
-  // fp32 rounding may land exactly on l: keep the image inside [0, l)
-  xf = xf >= (float)lx ? 0.0f : xf;
-  yf = yf >= (float)ly ? 0.0f : yf;
+  // fp32 rounding of an image just below l may land on l: keep it below l, in
+  // the top cell the index kernel files it under (cell_index_kernel clamps
+  // x / l * nc == nc to nc - 1), not at 0
+  const float xf = fminf((float)wrap_periodic(x, lx), nextafterf((float)lx, 0.0f));
+  const float yf = fminf((float)wrap_periodic(y, ly), nextafterf((float)ly, 0.0f));
   cpf[a] = make_float4(xf, yf, (float)z, 0.0f);
 }
 

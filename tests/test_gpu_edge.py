@@ -288,3 +288,29 @@ def test_size_independent_identities_at_1e7(pk, big):
     assert abs(bd3.total - bd.total) <= 1e-10 * abs(bd.total)
     assert np.max(np.abs(f3 - f)) <= 1e-9 * fmax
     assert np.all(np.abs(f.sum(axis=0)) <= 1e-9 * fmax * np.sqrt(wl.n))
+
+
+@pytest.mark.parametrize("n", [3000, 40000])
+def test_unwrapped_and_edge_positions_short_range(pk, n):
+    """Short range on positions outside the primary cell (a system built without
+    a box, MD floor-wrap leftovers) and exactly on the upper box edge: the
+    reference's minimum image makes u_s and the forces independent of the
+    periodic image each particle is given in (such particles used
+    to be filed in a cell their fp32 screen copy did not lie in)."""
+    rng = np.random.default_rng(n)
+    box = pk.BoxGeometry(*(3 * [(n / 0.1) ** (1.0 / 3.0)]))
+    pos = rng.random((n, 3)) * np.array([box.lx, box.ly, box.lz])
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    alpha, rc = 0.8, 4.0
+    pos[:5, 0] = box.lx * (1 - 1e-16 * np.arange(5))   # on / just below the upper x edge
+    pos[5:10, 1] = np.nextafter(box.ly, 0.0)            # just below the upper y edge
+    base = pk.make_system(q, np.ones(n), pos, box)
+    u0, f0 = pk.short_range_energy_forces(base, box, alpha, rc)
+    img = pos.copy()
+    k = rng.integers(-2, 3, size=(n, 2)).astype(np.float64)
+    img[:, 0] += k[:, 0] * box.lx                       # other periodic images, unwrapped
+    img[:, 1] += k[:, 1] * box.ly
+    shifted = pk.ParticleSystem(q, np.ones(n), img, np.zeros((n, 3)))   # no wrap
+    u1, f1 = pk.short_range_energy_forces(shifted, box, alpha, rc)
+    assert abs(u1 - u0) <= 1e-11 * abs(u0)
+    assert np.max(np.abs(f1 - f0)) <= 1e-10 * np.max(np.abs(f0))
