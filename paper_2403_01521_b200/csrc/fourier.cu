@@ -1047,10 +1047,6 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   int64_t rf = n * p.ngroups / target_ctas;
   int R = 16;
   while (R * 2 <= rf && R * 2 <= kMaxR) R *= 2;
-  if (const char* env = getenv("SLAB_CHUNK_R")) {  // tuning knob (power of two, 16..256)
-    const int r = atoi(env);
-    if (r >= 16 && r <= kMaxR && (r & (r - 1)) == 0) R = r;
-  }
   // Few items per chunk (a multi-GPU rank's mode slice, small P) means small
   // CTAs whose shared memory -- dominated by the R-particle decay and weight
   // tables -- would cap the SM at a handful of warps: shrink R until both the
@@ -1067,9 +1063,17 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
     const int sw_regs = sweep_min_blocks(mh) == 1 ? 255 : 128;
     const int sw_full = 65536 / (sw_regs * 32 * p.warps) > 0 ? 65536 / (sw_regs * 32 * p.warps) : 1;
     const int ag_full = 65536 / (kAggRegs * 32 * tpc);
-    while (R > 16 && (ctas(sweep_smem(R, mh, p.warps), 32 * p.warps, sw_regs) < sw_full ||
+    // ... but not below 64 particles: shorter chunks multiply the chunk count and
+    // with it the carry scan's traffic (cfg4 at 13 modes per rank: R = 16 ->
+    // 64 took the rank from 2.72 to 2.30 ms, the carries from 0.51 to 0.10 ms)
+    const int r_floor = R < 64 ? R : 64;
+    while (R > r_floor && (ctas(sweep_smem(R, mh, p.warps), 32 * p.warps, sw_regs) < sw_full ||
                       ctas(agg_mma_smem(R, mh), 32 * tpc, kAggRegs) < ag_full))
       R /= 2;
+  }
+  if (const char* env = getenv("SLAB_CHUNK_R")) {  // tuning knob (power of two, 16..256)
+    const int r = atoi(env);
+    if (r >= 16 && r <= kMaxR && (r & (r - 1)) == 0) R = r;
   }
   p.R = R;
   p.nch = (int)((n + R - 1) / R);

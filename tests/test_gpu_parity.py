@@ -70,7 +70,7 @@ def test_energy_forces_match_reference(name):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["cfg3", "cfg5_1e5", "cfg4", "cfg5_1e6"])
+@pytest.mark.parametrize("name", ["cfg3", "cfg5_1e5", "cfg4", "cfg5_1e6", "cfg5_1e7"])
 def test_energy_forces_match_reference_large(name):
     g, wl, bd, f = _run(name)
     _check(g, bd, f)
@@ -87,7 +87,7 @@ def test_sort_perm_bit_exact_configs(name):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5_1e6"])
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5_1e6", "cfg5_1e7"])
 def test_sort_perm_bit_exact_large(name):
     import paper_2403_01521_b200 as pk
     from paper_2403_01521_b200.configs import make_workload
