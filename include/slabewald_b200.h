@@ -261,6 +261,16 @@ int slab_recursive_pair_sum(SlabCtx* ctx, const double* d_q, const double* d_the
                             const double* d_z, int64_t n, double beta_re, double beta_im,
                             double* d_out, void* stream);
 
+/* The position-only constants of an evaluation, by the same device reduction
+ * slab_evaluate's assembly uses (ewald2d.py:527-545 self_energy and
+ * slab_energy_forces): d_energy[3] = u_self = alpha/sqrt(pi) sum q^2,
+ * d_energy[4] = u_ps = sum q phi(z); other slots as slab_evaluate with no
+ * short-range, Fourier or k = 0 terms.  (Lets the O(N^2 K) reference solver
+ * report bitwise the same u_self / u_ps as the SOE paths, as the reference's
+ * total_breakdown test requires.)  d_energy: >= 8 doubles. */
+int slab_constant_terms(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                        SlabBox box, double alpha, double* d_energy, void* stream);
+
 /* FP64 roofline denominator: DFMA throughput microbenchmark on the current
  * device (TFLOP/s, 2 flops per DFMA).  Synchronous. */
 int slab_fp64_peak(double* tflops);

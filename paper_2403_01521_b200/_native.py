@@ -35,7 +35,7 @@ EXPORTED = (
     "slab_ctx_neighbor_capacity", "slab_ctx_last_max_neighbors", "slab_batch_energies",
     "slab_wca", "slab_walls", "slab_md_langevin", "slab_md_kick", "slab_md_drift",
     "slab_md_scale", "slab_md_kinetic", "slab_zsplit_exchange_doubles",
-    "slab_ewald_ref_fourier", "slab_ewald_ref_zero", "slab_evaluate_host",
+    "slab_ewald_ref_fourier", "slab_ewald_ref_zero", "slab_evaluate_host", "slab_constant_terms",
 )
 
 
@@ -129,6 +129,7 @@ def load():
                                            cint, cint, cint, vp, vp, vp]
     lib.slab_ewald_ref_zero.argtypes = [vp, vp, vp, i64, dbl, vp, vp, vp]
     lib.slab_fp64_peak.argtypes = [ctypes.POINTER(dbl)]
+    lib.slab_constant_terms.argtypes = [vp, vp, vp, i64, SlabBox, dbl, vp, vp]
     lib.slab_ctx_neighbor_capacity.argtypes = [vp, cint]
     lib.slab_ctx_last_max_neighbors.argtypes = [vp, ctypes.POINTER(cint)]
 

@@ -841,6 +841,21 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   return SLAB_OK;
 }
 
+int slab_constant_terms(SlabCtx* ctx, const double* d_pos, const double* d_charge, int64_t n,
+                        SlabBox box, double alpha, double* d_energy, void* stream) {
+  if (!ctx || n < 0 || !d_energy || (n > 0 && (!d_pos || !d_charge)))
+    return fail(SLAB_ERR_ARG, "bad constant-term arguments");
+  if (!(alpha > 0)) return fail(SLAB_ERR_ARG, "alpha must be positive");
+  int rc = ensure_arena(ctx, 4096);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
+  CK(slab::assemble_energy(n, d_charge, d_pos, box.lz, box.sigma_top, box.sigma_bot, alpha,
+                           box.lx * box.ly, 0.0, nullptr, nullptr, nullptr, ctx->status, d_energy,
+                           ctx->small + 64, 1, st));
+  return SLAB_OK;
+}
+
 int64_t slab_zsplit_exchange_doubles(int64_t nmode, int soe_terms, int want_forces) {
   if (nmode <= 0 || soe_terms <= 0) return 0;
   return 4 * (int64_t)(soe_terms + 1) * (want_forces ? 2 : 1) * nmode;

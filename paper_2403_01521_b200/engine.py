@@ -258,6 +258,17 @@ class Engine:
         check(self.lib.slab_md_kinetic(self.ctx, _ptr(vel), _ptr(mass), vel.shape[0], _ptr(out),
                                        self._stream()), "slab_md_kinetic")
 
+    def constant_terms(self, pos, charge, box, alpha):
+        """Device (8,) energy vector with u_self (slot 3) and u_ps (slot 4) from the
+        assembly's own reduction."""
+        torch = _torch()
+        energy = torch.zeros(8, dtype=torch.float64, device=self.device)
+        check(self.lib.slab_constant_terms(
+            self.ctx, _ptr(pos), _ptr(charge), charge.numel(),
+            SlabBox(box.lx, box.ly, box.lz, box.sigma_top, box.sigma_bot), float(alpha),
+            _ptr(energy), self._stream()), "slab_constant_terms")
+        return energy
+
     def recursive_pair_sum(self, q, theta, z, beta):
         torch = _torch()
         out = torch.empty((q.numel(), 2), dtype=torch.float64, device=self.device)

@@ -205,8 +205,15 @@ def ref_energy_forces(system: ParticleSystem, box: BoxGeometry, params,
     u_s, f_s = short_range_energy_forces(system, box, params.alpha, params.r_c)
     u_k, f_k = fourier_energy_forces_ref(system, box, params, variant)
     u_0, f_0 = zero_mode_energy_forces_ref(system, box, params.alpha)
-    u_ps, f_ps = slab_energy_forces(system, box)
-    u_self = self_energy(system, params.alpha)
+    _, f_ps = slab_energy_forces(system, box)
+    # u_self and u_ps from the same device reduction as the SOE / RB assembly, so
+    # every solver reports the shared terms bitwise alike (reference
+    # test_total_breakdown_shares_short_range_and_slab_with_reference)
+    from .engine import get_engine, to_device
+    eng = get_engine()
+    e = eng.constant_terms(to_device(system.pos), to_device(system.charge), box,
+                           params.alpha).cpu().numpy()
+    u_self, u_ps = float(e[3]), float(e[4])
     return (EnergyBreakdown(u_s=u_s, u_l_k=u_k, u_l_0=u_0, u_self=u_self, u_ps=u_ps),
             f_s + f_k + f_0 + f_ps)
 
