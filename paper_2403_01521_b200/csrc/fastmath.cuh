@@ -189,6 +189,54 @@ __device__ __forceinline__ void erfc_gauss(double x, const double* __restrict__ 
   *g_out = g;
 }
 
+// erfcx(x) on [0, 6] with no table: one degree-19 polynomial in the rational
+// map u = (7/3 x - 4) / (x + 4) (= (t + 0.4) / 0.6, t = (x - 4)/(x + 4)), max
+// relative error 6e-16 (tools/gen_erfcx_rational.py).  Every lane uses the same
+// coefficients, so they come from uniform registers / the constant bank -- a
+// per-lane table in shared memory costs >= 2 wavefronts per coefficient load,
+// which made the table forms of this kernel shared-memory bound.
+__device__ __forceinline__ double rcp_fast(double x) {  // 1/x, x normal > 0, ~1 ulp
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// constant bank: LDCU.128 brings two coefficients into uniform registers per
+// instruction (literals cost two UMOVs each, re-issued for every pair)
+static __constant__ __align__(16) double kErfcxRat[20] = {
+    2.89722116323464229e-01,  -3.30725380025229221e-01, 2.07401177991509089e-01,
+    -1.06646031140752912e-01, 4.50108550943799507e-02,  -1.54181897135370650e-02,
+    4.16094898189511321e-03,  -8.24498405499286065e-04, 9.61294917405419497e-05,
+    2.04972504298114117e-06,  -2.99897570926783762e-06, 3.49340377437571895e-07,
+    5.58422862486972409e-08,  -1.64955693655007643e-08, -8.63453257340785243e-10,
+    6.39416928898986440e-10,  1.46431537907270747e-11,  -2.48249270445082579e-11,
+    -4.86601666694534958e-13, 8.44604731366168551e-13};
+
+__device__ __forceinline__ double erfcx_rat(double x) {
+  const double u = fma(7.0 / 3.0, x, -4.0) * rcp_fast(x + 4.0);
+  double p = kErfcxRat[19];
+#pragma unroll
+  for (int j = 18; j >= 0; --j) p = fma(p, u, kErfcxRat[j]);
+  return p;
+}
+
+constexpr double kErfcxRatMax = 6.0;
+
+// erfc(x) and e^{-x^2} sharing one exp (as fastmath.cuh's erfc_gauss)
+template <bool kTabOnly>
+__device__ __forceinline__ void erfc_gauss_rat(double x, double* erfc_out, double* g_out) {
+  const double hi = x * x;
+  const double lo = fma(x, x, -hi);
+  double g = exp_neg_cb(hi);
+  g = fma(-lo, g, g);
+  const double ex = (kTabOnly || x <= kErfcxRatMax) ? erfcx_rat(x) : erfcx(x);
+  *erfc_out = ex * g;
+  *g_out = g;
+}
+
 constexpr int kErfcxTabSize = SLAB_ERFCX_NINT * SLAB_ERFCX_NCOEF;
 
 __device__ __forceinline__ void load_erfcx_table(double* tab) {

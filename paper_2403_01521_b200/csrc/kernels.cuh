@@ -121,7 +121,19 @@ struct ShortPlan {
   int64_t nblk;   // energy partial count
   int kcap;       // neighbour-row capacity (multiple of 8)
   int span;       // cell search span S: cells of edge >= r_c / S, (2S+1)^2 columns
+  int tile;       // 1: fused screen + pair kernel (short_tile.cu), no neighbour rows
 };
+// short_tile.cu: homes in brick order, fused screen + exact pair terms
+int64_t tile_home_slots(int ncx, int ncy, int ncz);
+size_t tile_work_bytes(int64_t n, int ncx, int ncy, int ncz);
+int tile_grid(int64_t nhomes);
+cudaError_t tile_homes(const int32_t* start, const uint32_t* skey, int64_t n, int ncx, int ncy,
+                       int ncz, void* work, int32_t** hperm_out, cudaStream_t st);
+cudaError_t tile_pairs(const double4* cp, const float4* cpf, const int32_t* start,
+                       const int32_t* hperm, const int32_t* order, int64_t h0, int64_t h1,
+                       int ncx, int ncy, int ncz, double lx, double ly, double lz, double alpha,
+                       double rc, double* forces, double* eblk, int grid, int* status,
+                       cudaStream_t st);
 // max_span 1: cells of edge >= rc (fewer cells: the short WCA cutoff of a big box
 // would otherwise need ~6e7 half-edge cells at N = 1e6)
 ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int max_span = 3);

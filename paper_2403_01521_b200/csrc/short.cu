@@ -75,6 +75,9 @@ __device__ __forceinline__ double min_image(double d, double l, double il) {
   return __dsub_rn(d, __dmul_rn(l, rint(__dmul_rn(d, il))));
 }
 
+#ifndef SLAB_PAIR_RAT
+#define SLAB_PAIR_RAT 0  // table-free erfcx: pair_list 2.2 -> 2.97 ms at cfg4 (fp64-bound once L1 is not)
+#endif
 template <bool kTabOnly>
 __device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, double zi, double qi,
                                                        double xj, double yj, double zj, double qj,
@@ -96,7 +99,16 @@ __device__ __forceinline__ void pair_accumulate_masked(double xi, double yi, dou
   const double d = d2u * inv_d;
   const double qq = use ? qi * qj : 0.0;
   double e, g;
+#if SLAB_PAIR_RAT
+  // table-free erfcx (fastmath.cuh): uniform coefficients, no per-lane
+  // shared-memory reads on this L1-bound kernel
+  if constexpr (kTabOnly)
+    erfc_gauss_rat<true>(alpha * d, &e, &g);
+  else
+    erfc_gauss<false>(alpha * d, etab, &e, &g);
+#else
   erfc_gauss<kTabOnly>(alpha * d, etab, &e, &g);
+#endif
   acc.e = fma(qq * e, inv_d, acc.e);
   const double fmag = qq * (e * inv_d + c * g) * (inv_d * inv_d);
   acc.fx = fma(fmag, dx, acc.fx);
@@ -481,9 +493,10 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2, double eps,
     double sig2, double* __restrict__ forces, double* __restrict__ eblk,
     int* __restrict__ status, int accumulate) {
-  __shared__ double etab[KIND != 1 ? kErfcxTabSize : 1];
+  constexpr bool kTable = KIND == 0 || (KIND == 2 && !SLAB_PAIR_RAT);
+  __shared__ double etab[kTable ? kErfcxTabSize : 1];
   __shared__ double red[kSRThreads];
-  if constexpr (KIND != 1) load_erfcx_table(etab);
+  if constexpr (kTable) load_erfcx_table(etab);
   __syncthreads();
   const double c = kTwoOverSqrtPi * alpha;
   const double ilx = 1.0 / lx, ily = 1.0 / ly;
@@ -702,6 +715,15 @@ static void launch_pair_list(int kind, int split, unsigned grid, cudaStream_t st
 #endif
 constexpr int kShortSpan = SLAB_SHORT_SPAN_DEFAULT;
 
+#ifndef SLAB_TILE_MIN_N
+#define SLAB_TILE_MIN_N 40000
+#endif
+constexpr int64_t kTileMinN = SLAB_TILE_MIN_N;
+#ifndef SLAB_TILE_DEFAULT
+#define SLAB_TILE_DEFAULT 0  // cfg4: tile 4.5 ms vs neighbour rows 3.2 ms (DESIGN 4.3)
+#endif
+constexpr bool kTileDefault = SLAB_TILE_DEFAULT;
+
 ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int max_span) {
   ShortPlan p{};
   p.n = n;
@@ -732,6 +754,17 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int 
   p.ncy = ncy;
   p.ncz = ncz;
   p.ncell = (int64_t)ncx * ncy * ncz;
+  // the fused tile kernel (short_tile.cu) for the erfc Coulomb sum of larger
+  // systems: its column window (a warp's ~2 x 2-cell box +- S cells) must fit in
+  // the box without aliasing; small systems keep the neighbour-row kernels tuned
+  // for them.  SLAB_SHORT_TILE=0/1 overrides (A/B timing).
+  p.tile = 0;
+  if (kTileDefault && !p.brute && max_span >= 3 && p.span == 3 && ncx >= 2 * p.span + 6 &&
+      ncy >= 2 * p.span + 6 && n >= kTileMinN)
+    p.tile = 1;
+  if (const char* env = getenv("SLAB_SHORT_TILE"))
+    p.tile = (env[0] == '1' && !p.brute && max_span >= 3 && p.span >= 2) ? 1 :
+             (env[0] == '0' ? 0 : p.tile);
   const int64_t nbx = (n + 127) / 128;
   int js = (int)(592 / (nbx > 0 ? nbx : 1));
   p.jsplit = p.brute ? (js < 1 ? 1 : (js > 64 ? 64 : js)) : 1;
@@ -758,7 +791,10 @@ size_t short_work_bytes(const ShortPlan& p) {
     b += align256(sizeof(int32_t) * radix_hist_entries(p.n));
     b += align256(sizeof(int32_t) * (p.ncell + 1));
     b += align256(sizeof(double4) * n) + align256(sizeof(float4) * n);
-    b += align256(sizeof(int32_t) * n * (size_t)p.kcap) + align256(sizeof(int32_t) * n);
+    if (p.tile)
+      b += tile_work_bytes(p.n, p.ncx, p.ncy, p.ncz);
+    else
+      b += align256(sizeof(int32_t) * n * (size_t)p.kcap) + align256(sizeof(int32_t) * n);
     b += align256(sizeof(int));
   }
   return b + 256;
@@ -816,10 +852,6 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     w += align256(sizeof(double4) * n);
     float4* cpf = reinterpret_cast<float4*>(w);
     w += align256(sizeof(float4) * n);
-    int32_t* nbr = reinterpret_cast<int32_t*>(w);
-    w += align256(sizeof(int32_t) * n * (size_t)p.kcap);
-    int32_t* nn = reinterpret_cast<int32_t*>(w);
-    w += align256(sizeof(int32_t) * n);
     int* maxnn = maxnn_out;
     cell_index_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, n, lx, ly, lz, p.ncx,
                                                                   p.ncy, p.ncz, k0, v0);
@@ -833,6 +865,22 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
                                                                              start);
     cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, lx,
                                                                     ly, cp, cpf);
+    if (p.tile) {  // fused screen + pair kernel: no neighbour rows
+      if (accumulate) return cudaErrorInvalidValue;  // Coulomb callers overwrite
+      int32_t* hperm = nullptr;
+      e = tile_homes(start, skey, n, p.ncx, p.ncy, p.ncz, w, &hperm, st);
+      if (e != cudaSuccess) return e;
+      const int grid = tile_grid(nh) < p.nblk ? tile_grid(nh) : (int)p.nblk;
+      e = tile_pairs(cp, cpf, start, hperm, order, h0, h1, p.ncx, p.ncy, p.ncz, lx, ly, lz,
+                     alpha, rc, forces, eblk, grid, status, st);
+      if (e != cudaSuccess) return e;
+      half_sum_kernel<<<1, 1024, 0, st>>>(eblk, grid, energy_out);
+      return cudaGetLastError();
+    }
+    int32_t* nbr = reinterpret_cast<int32_t*>(w);
+    w += align256(sizeof(int32_t) * n * (size_t)p.kcap);
+    int32_t* nn = reinterpret_cast<int32_t*>(w);
+    w += align256(sizeof(int32_t) * n);
     // conservative fp32 screen: positions rounded to fp32 move d2 by < 1e-2 for
     // |r| <= 1e3; the exact fp64 test is applied to every survivor
     const float rc2f = (float)(rc2 * (1.0 + 1e-3) + 1e-2);
@@ -862,7 +910,8 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     const int split = pair_split(nh);
     const int64_t pgrid = pair_grid((nh * split + kSRThreads - 1) / kSRThreads);
     // every pair has alpha d <= alpha r_c: below the table end -> branch-free form
-    const bool tab_only = alpha * sqrt(rc2) < 0.999 * SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W;
+    const bool tab_only = alpha * sqrt(rc2) < 0.999 * SLAB_ERFCX_NINT / SLAB_ERFCX_INV_W &&
+                          (!SLAB_PAIR_RAT || alpha * sqrt(rc2) <= 0.999 * kErfcxRatMax);
     const int kk = kind == 0 ? (tab_only ? 2 : 0) : 1;
     launch_pair_list(kk, split, (unsigned)pgrid, st, cp, order, nbr, nn, h0, h1, p.kcap, lx, ly,
                      kind == 0 ? alpha : 0.0, rc2, kind == 0 ? 0.0 : lj_eps,
