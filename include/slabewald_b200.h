@@ -54,8 +54,10 @@ enum {
   SLAB_STATUS_COINCIDENT = 1, /* d2 < 1e-24 pair: ewald2d.py:207-209,301-302 */
   SLAB_STATUS_SINGULAR = 2,   /* reserved: singular terms (|b_l - k| < 2e-6 k) are now
                                * evaluated (soewald2d.py:116-124), this bit is never set */
-  SLAB_STATUS_NBR_OVERFLOW = 4, /* a short-range neighbour row exceeded its capacity: results
-                                   are invalid; raise it (slab_ctx_neighbor_capacity) and rerun */
+  SLAB_STATUS_NBR_OVERFLOW = 4, /* a short-range neighbour row exceeded its capacity; those
+                                   homes were evaluated in-stream by the overflow kernel, so the
+                                   results are COMPLETE -- raising the capacity
+                                   (slab_ctx_neighbor_capacity) only makes later runs faster */
   SLAB_STATUS_NONFINITE = 8,    /* a z coordinate is not finite (core.py:206-207): results invalid */
   SLAB_STATUS_WALL = 16         /* a particle at or beyond a wall (md.py:72) */
 };

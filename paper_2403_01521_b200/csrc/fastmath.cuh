@@ -151,6 +151,45 @@ __device__ __forceinline__ void sincos_fast_cb(double th, double* s, double* c) 
   *c = ((q + 1) & 2) ? -cc : cc;
 }
 
+// *_sm variants: the same polynomials with the coefficients read from a
+// shared-memory copy (c = kFmExp for exp; c = kFmSin then kFmCos for sincos),
+// every lane the same address: broadcast loads, two constants per LDS.128
+__device__ __forceinline__ double exp_neg_sm(double t, const double* __restrict__ c) {
+  const bool tiny = !(t < 700.0);
+  t = tiny ? 0.0 : t;
+  const double n = rint(-t * 1.4426950408889634);
+  double r = fma(n, -c[14], -t);
+  r = fma(n, -c[15], r);
+  double p = c[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) p = fma(p, r, c[i]);
+  const long long e = tiny ? 0ll : (long long)((int)n + 1023) << 52;
+  return p * __longlong_as_double(e);
+}
+
+__device__ __forceinline__ void sincos_fast_sm(double th, double* s, double* co,
+                                               const double* __restrict__ c) {
+  // c[0..7] = kFmSin, c[8..19] = kFmCos
+  const double n = rint(th * c[7]);
+  double r = fma(n, c[8 + 9], th);
+  r = fma(n, c[8 + 10], r);
+  r = fma(n, c[8 + 11], r);
+  const double z = r * r;
+  double ps = c[0];
+#pragma unroll
+  for (int i = 1; i < 7; ++i) ps = fma(ps, z, c[i]);
+  const double sr = fma(ps * z, r, r);
+  double pc = c[8];
+#pragma unroll
+  for (int i = 1; i < 9; ++i) pc = fma(pc, z, c[8 + i]);
+  const double cr = pc;
+  const int q = ((int)(long long)n) & 3;
+  const double ss = (q & 1) ? cr : sr;
+  const double cc = (q & 1) ? sr : cr;
+  *s = (q & 2) ? -ss : ss;
+  *co = ((q + 1) & 2) ? -cc : cc;
+}
+
 // tab: shared-memory copy of kErfcxCoef, coefficient-major (tab[k * NINT + i]):
 // the lanes of a warp evaluate different intervals i, and with consecutive
 // intervals in consecutive 8-byte words only rows 16 apart share a bank (pair

@@ -37,6 +37,9 @@ namespace slab {
 #ifndef SLAB_SWEEP_SB
 #define SLAB_SWEEP_SB 4
 #endif
+#ifndef SLAB_SWEEP_CB
+#define SLAB_SWEEP_CB 0
+#endif
 #ifndef SLAB_SWEEP_PIPE
 #define SLAB_SWEEP_PIPE 0  // 1: next particle's sincos/exp issued one iteration ahead (measured 2.5% slower since exp_neg went branch-free)
 #endif
@@ -749,6 +752,14 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
   double* sq = sy + R;
   double* sz = sq + R;                                     // R + 2 (halo below / above)
   double* stage = sz + R + 2;                              // nwarps * kSB*3 * 33
+#if SLAB_SWEEP_CB == 2
+  // transcendental coefficients, broadcast from shared memory (one LDS.128 per
+  // two constants instead of two UMOVs per constant)
+  __shared__ __align__(16) double scoef[40];
+  if (threadIdx.x < 16) scoef[threadIdx.x] = kFmExp[threadIdx.x];
+  else if (threadIdx.x < 24) scoef[threadIdx.x] = kFmSin[threadIdx.x - 16];
+  else if (threadIdx.x < 36) scoef[threadIdx.x] = kFmCos[threadIdx.x - 24];
+#endif
 
   const int c = c0 + blockIdx.x, g = blockIdx.y;
   const int64_t a0 = (int64_t)c * R;
@@ -816,9 +827,17 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
   auto phase = [&](int i, double& cs_, double& sn_, double& dk_, double& q_) {
     const int ia = fwd ? i : len - 1 - i;
     const double dz = fwd ? (sz[ia + 1] - sz[ia]) : (sz[ia + 2] - sz[ia + 1]);
-    dk_ = exp_neg(k * dz);
     const double th = __dadd_rn(__dmul_rn(kx, sx[ia]), __dmul_rn(ky, sy[ia]));
+#if SLAB_SWEEP_CB == 1
+    dk_ = exp_neg_cb(k * dz);
+    sincos_fast_cb(th, &sn_, &cs_);
+#elif SLAB_SWEEP_CB == 2
+    dk_ = exp_neg_sm(k * dz, scoef);
+    sincos_fast_sm(th, &sn_, &cs_, scoef + 16);
+#else
+    dk_ = exp_neg(k * dz);
     sincos_fast(th, &sn_, &cs_);
+#endif
     q_ = sq[ia];
   };
   double cs, sn, dk, q;

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
   }
   if (cnt <= kcap)
     for (int k = done; k < cnt; ++k) row[k] = st[(k & (kRing - 1)) * kSRThreads];
-  nn[a - a_begin] = cnt < kcap ? cnt : kcap;
+  nn[a - a_begin] = cnt <= kcap ? cnt : -1;  // -1: overflowed, evaluated by overflow_pairs_kernel
   if (cnt > kcap) {
     atomicOr(status, SLAB_STATUS_NBR_OVERFLOW_DEV);
     atomicMax(maxnn, cnt);
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kSRThreads) nbr_cells_kernel(
 #pragma unroll
     for (int h = 0; h < kCellHomes; ++h)
       if (h < ng && lane == h) {
-        nn[g0 + h - a_begin] = cnt[h] < kcap ? cnt[h] : kcap;
+        nn[g0 + h - a_begin] = cnt[h] <= kcap ? cnt[h] : -1;
         if (cnt[h] > kcap) {
           atomicOr(status, SLAB_STATUS_NBR_OVERFLOW_DEV);
           atomicMax(maxnn, cnt[h]);
@@ -521,7 +521,9 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
     const int64_t a = base + threadIdx.x / SPLIT;
     const bool active = a < a_end;
     const double4 pi = active ? cp[a] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const int cnt = active ? nn[a - a_begin] : 0;
+    const int cnt_raw = active ? nn[a - a_begin] : 0;
+    const bool own = active && cnt_raw >= 0;  // overflowed homes: overflow_pairs_kernel
+    const int cnt = cnt_raw > 0 ? cnt_raw : 0;
     const int32_t* row = nbr + (active ? a - a_begin : 0) * (int64_t)kcap;
     acc.fx = acc.fy = acc.fz = 0.0;
 #if SLAB_PAIR_WIDE
@@ -575,7 +577,7 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
       acc.fy += __shfl_xor_sync(0xffffffffu, acc.fy, o);
       acc.fz += __shfl_xor_sync(0xffffffffu, acc.fz, o);
     }
-    if (active && sub == 0) {
+    if (own && sub == 0) {
       const int64_t i = order[a];
       if (accumulate) {  // one thread owns particle i: += is race-free and deterministic
         acc.fx += forces[3 * i + 0];
@@ -590,6 +592,92 @@ __global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
 #undef PAIR
   if (flag) atomicOr(status, SLAB_STATUS_COINCIDENT_DEV);
   red[threadIdx.x] = acc.e;
+  __syncthreads();
+  for (int w = kSRThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) eblk[blockIdx.x] = red[0];
+}
+
+// Homes whose neighbour row overflowed its capacity (nn = -1): one thread per
+// such home searches its (2S+1)^2 trimmed columns again and evaluates every
+// pair directly (same fp32 screen and exact fp64 term as the row path), writing
+// the home's force and a per-block energy partial.  Always launched, in-stream
+// and graph-safe; a run without overflow just scans nn.  The home's pair order
+// (columns, then z) is fixed, so results stay deterministic.
+constexpr int kOvfBlocks = 148;
+template <int S, int KIND>
+__global__ void __launch_bounds__(kSRThreads) overflow_pairs_kernel(
+    const double4* __restrict__ cp, const float4* __restrict__ cpf,
+    const uint32_t* __restrict__ skey, const int32_t* __restrict__ start,
+    const int32_t* __restrict__ order, const int32_t* __restrict__ nn, int64_t a_begin,
+    int64_t a_end, int ncx, int ncy, int ncz, float lxf, float lyf, float lzf, float rc2f,
+    double lx, double ly, double alpha, double rc2, double eps, double sig2,
+    double* __restrict__ forces, double* __restrict__ eblk, int* __restrict__ status,
+    int accumulate) {
+  __shared__ double etab[KIND != 1 ? kErfcxTabSize : 1];
+  __shared__ double red[kSRThreads];
+  if constexpr (KIND != 1) load_erfcx_table(etab);
+  __syncthreads();
+  const double c = kTwoOverSqrtPi * alpha, ilx = 1.0 / lx, ily = 1.0 / ly;
+  const float ex = lxf / ncx, ey = lyf / ncy, izc = ncz / lzf;
+  double e_sum = 0.0;
+  int flag = 0;
+  for (int64_t a = a_begin + blockIdx.x * (int64_t)kSRThreads + threadIdx.x; a < a_end;
+       a += (int64_t)gridDim.x * kSRThreads) {
+    if (nn[a - a_begin] >= 0) continue;
+    const int cid = (int)skey[a];
+    const int cy = (cid / ncz) % ncy, cx = cid / (ncz * ncy);
+    const float4 pi = cpf[a];
+    const double4 pd = cp[a];
+    PairAcc acc{0.0, 0.0, 0.0, 0.0};
+    for (int ox = -S; ox <= S; ++ox) {
+      const int ux = cx + ox;
+      const int nx = ux < 0 ? ux + ncx : (ux >= ncx ? ux - ncx : ux);
+      const float px = pi.x + (ux < 0 ? lxf : (ux >= ncx ? -lxf : 0.0f));
+      for (int oy = -S; oy <= S; ++oy) {
+        const int uy = cy + oy;
+        const int ny = uy < 0 ? uy + ncy : (uy >= ncy ? uy - ncy : uy);
+        const float py = pi.y + (uy < 0 ? lyf : (uy >= ncy ? -lyf : 0.0f));
+        const float dxr = fmaxf(0.0f, fmaxf(nx * ex - px, px - (nx + 1) * ex));
+        const float dyr = fmaxf(0.0f, fmaxf(ny * ey - py, py - (ny + 1) * ey));
+        const float dxy2 = fmaf(dxr, dxr, dyr * dyr);
+        if (dxy2 > rc2f) continue;
+        const float h = sqrtf(rc2f - dxy2);
+        int zlo = (int)floorf((pi.z - h) * izc - 1e-3f);
+        int zhi = (int)floorf((pi.z + h) * izc + 1e-3f);
+        zlo = zlo < 0 ? 0 : (zlo >= ncz ? ncz - 1 : zlo);
+        zhi = zhi < 0 ? 0 : (zhi >= ncz ? ncz - 1 : zhi);
+        const int col = (nx * ncy + ny) * ncz;
+        for (int jj = start[col + zlo]; jj < start[col + zhi + 1]; ++jj) {
+          if (jj == (int)a) continue;
+          const float4 pj = cpf[jj];
+          const float dx = px - pj.x, dy = py - pj.y, dz = pi.z - pj.z;
+          if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) > rc2f) continue;
+          const double4 q = cp[jj];
+          if constexpr (KIND != 1)
+            pair_accumulate(pd.x, pd.y, pd.z, pd.w, q.x, q.y, q.z, q.w, lx, ly, ilx, ily, alpha,
+                            rc2, c, etab, acc, flag);
+          else
+            wca_accumulate<false>(pd.x, pd.y, pd.z, q.x, q.y, q.z, lx, ly, ilx, ily, rc2, eps,
+                                  sig2, acc, flag);
+        }
+      }
+    }
+    const int64_t i = order[a];
+    if (accumulate) {
+      acc.fx += forces[3 * i + 0];
+      acc.fy += forces[3 * i + 1];
+      acc.fz += forces[3 * i + 2];
+    }
+    forces[3 * i + 0] = acc.fx;
+    forces[3 * i + 1] = acc.fy;
+    forces[3 * i + 2] = acc.fz;
+    e_sum += acc.e;
+  }
+  if (flag) atomicOr(status, SLAB_STATUS_COINCIDENT_DEV);
+  red[threadIdx.x] = e_sum;
   __syncthreads();
   for (int w = kSRThreads / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
@@ -773,7 +861,9 @@ ShortPlan short_plan(int64_t n, double lx, double ly, double lz, double rc, int 
   // neighbour-row capacity: 1.6x the mean-density sphere count + slack, rounded to
   // whole 32-byte sectors; grown by the caller after an overflow report
   const double dens = n / (lx * ly * lz);
-  int64_t kc = (int64_t)(1.6 * 4.18879 * rc * rc * rc * dens) + 96;
+  // (rows past capacity are evaluated by overflow_pairs_kernel, so this only
+  // trades row memory -- 21 GB at N = 1e7 with 1.6x + 96 -- against fallback work)
+  int64_t kc = (int64_t)(1.3 * 4.18879 * rc * rc * rc * dens) + 48;
   if (kc > n + 8) kc = n + 8;
   p.kcap = (int)((kc + 7) / 8 * 8);  // whole 32-byte sectors
   return p;
@@ -783,7 +873,7 @@ static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 size_t short_work_bytes(const ShortPlan& p) {
   const size_t n = (size_t)(p.n > 0 ? p.n : 1);
-  size_t b = align256(sizeof(double) * (p.nblk > 0 ? p.nblk : 1));  // eblk
+  size_t b = align256(sizeof(double) * ((p.nblk > 0 ? p.nblk : 1) + kOvfBlocks));  // eblk
   if (p.brute) {
     b += align256(sizeof(double) * 3 * n * p.jsplit);
   } else {
@@ -819,7 +909,7 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
   const int64_t nh = h1 - h0;
   char* w = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(work) + 255) & ~(uintptr_t)255);
   double* eblk = reinterpret_cast<double*>(w);
-  w += align256(sizeof(double) * p.nblk);
+  w += align256(sizeof(double) * (p.nblk + kOvfBlocks));
   const double rc2 = rc * rc;
   if (p.brute) {
     double* fbuf = reinterpret_cast<double*>(w);
@@ -916,7 +1006,24 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     launch_pair_list(kk, split, (unsigned)pgrid, st, cp, order, nbr, nn, h0, h1, p.kcap, lx, ly,
                      kind == 0 ? alpha : 0.0, rc2, kind == 0 ? 0.0 : lj_eps,
                      kind == 0 ? 0.0 : sig2, forces, eblk, status, accumulate);
-    half_sum_kernel<<<1, 1024, 0, st>>>(eblk, pgrid, energy_out);
+    // homes whose row overflowed (nn = -1), evaluated directly; in-stream, so
+    // no pair is dropped and no host rerun is needed
+#define SLAB_OVF_LAUNCH(S_, K_)                                                              \
+  overflow_pairs_kernel<S_, K_><<<kOvfBlocks, kSRThreads, 0, st>>>(                          \
+      cp, cpf, skey, start, order, nn, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly,    \
+      (float)lz, rc2f, lx, ly, kind == 0 ? alpha : 0.0, rc2, kind == 0 ? 0.0 : lj_eps,        \
+      kind == 0 ? 0.0 : sig2, forces, eblk + pgrid, status, accumulate)
+    if (kind == 1) {
+      if (p.span == 3) SLAB_OVF_LAUNCH(3, 1);
+      else if (p.span == 2) SLAB_OVF_LAUNCH(2, 1);
+      else SLAB_OVF_LAUNCH(1, 1);
+    } else {
+      if (p.span == 3) SLAB_OVF_LAUNCH(3, 0);
+      else if (p.span == 2) SLAB_OVF_LAUNCH(2, 0);
+      else SLAB_OVF_LAUNCH(1, 0);
+    }
+#undef SLAB_OVF_LAUNCH
+    half_sum_kernel<<<1, 1024, 0, st>>>(eblk, pgrid + kOvfBlocks, energy_out);
   }
   return cudaGetLastError();
 }

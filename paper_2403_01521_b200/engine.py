@@ -60,7 +60,11 @@ class Engine:
 
     def handle_overflow(self, status: int) -> bool:
         """After a synchronised run: if a short-range neighbour row overflowed, grow the
-        capacity to the longest row seen and report that the evaluation must be rerun."""
+        capacity to the longest row seen, so that later runs keep every home on the
+        row path.  Returns False: the overflowed homes were already evaluated
+        in-stream by the overflow kernel (short.cu), the results are complete and
+        nothing needs to be rerun -- a device-resident / graph-replayed step never
+        drops a pair, whatever the local density does between host checks."""
         if not int(status) & _native.SLAB_STATUS_NBR_OVERFLOW:
             return False
         need = ctypes.c_int(0)
@@ -68,7 +72,7 @@ class Engine:
               "slab_ctx_last_max_neighbors")
         check(self.lib.slab_ctx_neighbor_capacity(self.ctx, int(need.value * 1.1) + 16),
               "slab_ctx_neighbor_capacity")
-        return True
+        return False
 
     def _stream(self):
         torch = _torch()

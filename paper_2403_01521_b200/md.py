@@ -330,9 +330,9 @@ def run_simulation(system: ParticleSystem, box: BoxGeometry, opts: MDOptions) ->
         st_ = int(status.cpu().item())
         if st_:
             _status_errors(st_, "lj")
-            from ._native import SLAB_STATUS_NBR_OVERFLOW
-            if st_ & SLAB_STATUS_NBR_OVERFLOW:
-                raise RuntimeError("short-range neighbour capacity exceeded during the run")
+            # a row overflow was evaluated in-stream (complete results): only
+            # grow the capacity for the steps that follow
+            eng.handle_overflow(st_)
         e = ebuf.cpu().numpy()
         p = pos.cpu().numpy()
         sh = shift.cpu().numpy()
