@@ -11,6 +11,23 @@
     if (_e != cudaSuccess) return slab_record_cuda(_e);    \
   } while (0)
 
+// Checked build (make variant NAME=checked DEFS=-DSLAB_CHECKED): device-side bounds
+// asserts on the arena indexing of the hot kernels (compute-sanitizer is not
+// available on this pool); a violation prints its site and traps.
+#ifdef SLAB_CHECKED
+#include <cstdio>
+#define SLAB_BOUND(i, n)                                                               \
+  do {                                                                                 \
+    if ((unsigned long long)(i) >= (unsigned long long)(n)) {                          \
+      printf("slab bound violated %s:%d: %lld >= %lld\n", __FILE__, __LINE__,           \
+             (long long)(i), (long long)(n));                                          \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define SLAB_BOUND(i, n) ((void)0)
+#endif
+
 namespace slab {
 
 constexpr double kPi = 3.141592653589793;

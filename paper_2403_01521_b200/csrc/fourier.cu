@@ -468,6 +468,8 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
     if (l < MH) {
       const int item = dir == 0 ? t : P + t;
       const double sgn = dir == 0 ? 1.0 : -1.0;  // backward I input is +q sin = -ui
+      SLAB_BOUND((size_t)c * nc * nitems + (size_t)(MH + l) * nitems + item,
+                 (size_t)(c + 1) * nc * nitems);
       out[(size_t)l * nitems + item] = make_double2(acc[0][u][0], acc[0][u][1]);
       out[(size_t)(MH + l) * nitems + item] =
           make_double2(sgn * acc[1][u][0], sgn * acc[1][u][1]);
@@ -915,6 +917,8 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
         sb += __shfl_down_sync(0xffffffffu, sb, 3 * kSB);
         if (lane < nrow) {
           const int sl = lane / 3, comp = lane - 3 * sl;
+          SLAB_BOUND(a0 + ibase + sl, n);
+          SLAB_BOUND(a0 + len - 1 - (ibase + sl), n);
           if (fmask) fbuf_f[(a0 + ibase + sl) * 3 + comp] = sf;
           if (bmask) fbuf_b[(a0 + len - 1 - (ibase + sl)) * 3 + comp] = sb;
         }

@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
                                 st[(s0 + 2) * kSRThreads], st[(s0 + 3) * kSRThreads]);
       const int4 v1 = make_int4(st[(s0 + 4) * kSRThreads], st[(s0 + 5) * kSRThreads],
                                 st[(s0 + 6) * kSRThreads], st[(s0 + 7) * kSRThreads]);
+      SLAB_BOUND(done + 7, kcap);
       int4* dst = reinterpret_cast<int4*>(row + done);
       dst[0] = v0;
       dst[1] = v1;
@@ -310,7 +311,10 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
     }
   }
   if (cnt <= kcap)
-    for (int k = done; k < cnt; ++k) row[k] = st[(k & (kRing - 1)) * kSRThreads];
+    for (int k = done; k < cnt; ++k) {
+      SLAB_BOUND(k, kcap);
+      row[k] = st[(k & (kRing - 1)) * kSRThreads];
+    }
   nn[a - a_begin] = cnt <= kcap ? cnt : -1;  // -1: overflowed, evaluated by overflow_pairs_kernel
   if (cnt > kcap) {
     atomicOr(status, SLAB_STATUS_NBR_OVERFLOW_DEV);

@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(kTileThreads) short_tile_kernel(
           while (r) {
             const int t = __ffs(r) - 1;
             r &= r - 1u;
+            SLAB_BOUND(p, kTileQueue);
             q_w[p++] = (uint16_t)((lane << 5) | t);
           }
         }
@@ -404,6 +405,7 @@ __global__ void __launch_bounds__(kTileThreads) short_tile_kernel(
                 by = ay;
                 bz = az;
               } else {  // an interior segment: exclusive to this lane
+                SLAB_BOUND(cur, 32);
                 f0[cur] += ax;
                 f1[cur] += ay;
                 f2[cur] += az;

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_onesweep_kernel(
     __syncthreads();
     if (valid) {
       const int32_t dst = wcnt[warp][digit] + rank;
+      SLAB_BOUND(dst, n);
       kout[dst] = key;
       vout[dst] = vin[p];
     }
