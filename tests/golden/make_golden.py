@@ -270,12 +270,100 @@ def golden_ewald_ref() -> dict:
     return out
 
 
+def golden_batches() -> dict:
+    """rbse2d.py:320-363 run_many_batches, with the k-sequence drawn once from the
+    reference sampler and injected: per-batch forward-sweep energies from the
+    reference's own _rb_batch_energy_kernel, plus u_det.  N = 1e4, P = 100 and
+    41 batches: one full device pass of 40 batches and a 1-batch tail pass (the
+    plan-mismatch case of ADVICE r01)."""
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    configs = _load_pkg_module("core") and _load_pkg_module("configs")
+    wl = configs.make_workload("cfg5_1e4")
+    b = wl.box
+    box = core.BoxGeometry(b.lx, b.ly, b.lz, b.sigma_top, b.sigma_bot)
+    sysm = core.make_system(wl.system.charge, wl.system.mass, wl.system.pos, box=box)
+    params = core.make_ewald_params(wl.alpha, wl.s, box)
+    soe = rsoe.build_soe_contour(wl.m)
+    P, nb = 100, 41
+    alpha = params.alpha
+    H = rbse2d.normalization_H(alpha, box)
+    Q = float(np.sum(sysm.charge ** 2))
+    c_q = rbse2d.charge_term_sum(alpha, box, Q)
+    u_s, _ = ewald2d.short_range_energy_forces(sysm, box, alpha, params.r_c)
+    u_ps, _ = ewald2d.slab_energy_forces(sysm, box)
+    u_det = (u_s + soewald2d.zero_mode_energy_soe(sysm, box, alpha, soe)
+             - ewald2d.self_energy(sysm, alpha) + u_ps + c_q)
+    sampler = rbse2d.ModeSampler(alpha, box, seed=31)
+    rec = sampler.batch_indices(nb * P)
+    kx = 2 * np.pi * rec[:, 0] / box.lx
+    ky = 2 * np.pi * rec[:, 1] / box.ly
+    kv = np.hypot(kx, ky)
+    _, x, yv, z, q = soewald2d._sorted_view(sysm, box)
+    bvec = alpha * soe.s
+    decays = soewald2d._decay_table(z, bvec)
+    commonv = np.full(nb * P, (H / P) * rbse2d.TWO_OVER_SQRT_PI * alpha)
+    out = np.empty(nb)
+    rbse2d._rb_batch_energy_kernel(x, yv, z, q, kx, ky, kv, commonv, soe.w, bvec, box.area,
+                                   decays, P, out)
+    return dict(n=wl.n, P=P, n_batches=nb, H=H, c_q=c_q, u_det=u_det,
+                modes=np.column_stack([kx, ky, kv]), batch_u=out,
+                estimates=out + u_det, pos_sha=sha(wl.system.pos))
+
+
+def golden_formats() -> dict:
+    """Files WRITTEN by the reference (core.py:305-329 save_particles, soe.py:172-177
+    save_soe_table), their text and the reference's own load of them, for
+    cross-checking this package's readers and writers."""
+    import tempfile
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    rng = np.random.default_rng(77)
+    n = 37
+    pos = rng.uniform(-3.0, 13.0, size=(n, 3))
+    pos[:, 2] = rng.uniform(0.0, 6.0, size=n)
+    pos[0] = [0.0, -0.0, 6.0]
+    pos[1, 0] = 1e-300
+    vel = rng.normal(size=(n, 3)) * 1e3
+    q = rng.choice([-2.0, 1.0, 0.5], size=n)
+    m = rng.uniform(0.1, 40.0, size=n)
+    box = core.BoxGeometry(10.0, 12.0, 6.0)
+    sysm = core.make_system(q, m, pos, vel, box=box)
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        pp = os.path.join(td, "p.csv")
+        core.save_particles(pp, sysm)
+        out["particles_csv"] = np.array(open(pp).read())
+        back = core.load_particles(pp, box=box)
+        out["particles_q"], out["particles_m"] = back.charge, back.mass
+        out["particles_pos"], out["particles_vel"] = back.pos, back.vel
+        for mm in (8, 16):
+            tp = os.path.join(td, f"s{mm}.csv")
+            rsoe.save_soe_table(tp, rsoe.build_soe_contour(mm))
+            out[f"soe{mm}_csv"] = np.array(open(tp).read())
+            t = rsoe.load_soe_table(tp)
+            out[f"soe{mm}_w"], out[f"soe{mm}_s"] = t.w, t.s
+            out[f"soe{mm}_eps"] = t.eps_certified
+        # a hand-made table (one real term, one complex pair) as the soe tests use
+        hand = rsoe.SOEApprox(m=3, w=np.array([0.5 + 0.0j, 0.2 + 0.1j, 0.2 - 0.1j]),
+                              s=np.array([1.3 + 0.0j, 0.7 + 2.0j, 0.7 - 2.0j]),
+                              eps_certified=0.0, domain_max=20.0)
+        hp = os.path.join(td, "hand.csv")
+        rsoe.save_soe_table(hp, hand)
+        out["hand_csv"] = np.array(open(hp).read())
+        t = rsoe.load_soe_table(hp)
+        out["hand_w"], out["hand_s"], out["hand_eps"] = t.w, t.s, t.eps_certified
+    out["box"] = np.array([box.lx, box.ly, box.lz])
+    out["src_pos"], out["src_vel"], out["src_q"], out["src_m"] = sysm.pos, sysm.vel, q, m
+    return out
+
+
 def main(argv):
     names = argv or ["units", "cfg1", "cfg2", "small_600", "small_2000", "cfg5_1e4",
                      "cfg3", "cfg5_1e5", "cfg4", "cfg5_1e6"]
     for name in names:
         t0 = time.perf_counter()
         data = (golden_units() if name == "units" else
+                golden_batches() if name == "batches" else
+                golden_formats() if name == "formats" else
                 golden_md() if name == "md" else
                 golden_ewald_ref() if name == "ewald_ref" else golden_workload(name))
         path = os.path.join(HERE, f"{name}.npz")

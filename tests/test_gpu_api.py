@@ -518,3 +518,32 @@ def test_ewald2d_reference_solver_matches_reference(pk, tag, box_l, alpha, s_par
     assert bs.total == pytest.approx(bd.total, rel=1e-7)
     with pytest.raises(ValueError, match="neutral"):
         pk.ref_energy_forces(pk.make_system(np.ones(n), np.ones(n), pos, box), box, params)
+
+
+def test_batch_energies_match_reference_batches(pk):
+    """SURVEY 8(f) rank 2 pinned to the REAL reference: the per-batch energies of
+    rbse2d.py:320-363 (_rb_batch_energy_kernel, k-sequence from the reference
+    sampler injected; tests/golden/batches.npz) against slab_batch_energies --
+    N = 1e4, P = 100, 41 batches = a 40-batch device pass plus a 1-batch tail
+    pass with its own plan -- and the deterministic part u_det."""
+    import torch
+    from paper_2403_01521_b200.configs import make_workload
+    from paper_2403_01521_b200.engine import get_engine
+    from paper_2403_01521_b200.rbse2d import _rb_commonv
+    g = load_golden("batches")
+    wl = make_workload("cfg5_1e4")
+    soe = pk.build_soe_contour(wl.m)
+    params = wl.params()
+    eng = get_engine()
+    d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(eng.device)
+    P, nb = int(g["P"]), int(g["n_batches"])
+    out, status = eng.batch_energies(d(wl.system.pos), d(wl.system.charge), soe, wl.alpha,
+                                     wl.box.area, d(g["modes"]), nb, P,
+                                     _rb_commonv(float(g["H"]), P, wl.alpha))
+    assert int(status.cpu().item()) == 0
+    got = out.cpu().numpy()
+    scale = np.max(np.abs(g["batch_u"]))
+    assert np.max(np.abs(got - g["batch_u"])) <= 1e-10 * scale
+    bd, _ = pk.soe_energy_forces(wl.system, wl.box, params, soe)
+    u_det = bd.u_s + bd.u_l_0 - bd.u_self + bd.u_ps + float(g["c_q"])
+    assert u_det == pytest.approx(float(g["u_det"]), rel=1e-10)

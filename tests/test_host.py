@@ -220,3 +220,35 @@ def test_bench_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "cfg2"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_formats_cross_check_with_reference_written_files(tmp_path):
+    """SURVEY 8(f) rank 3 against files the REFERENCE wrote (tests/golden/formats.npz:
+    core.py:305-329 save_particles, soe.py:151-177 save/load_soe_table): our
+    readers load them to the reference's own arrays, our writers reproduce the
+    reference's bytes, and the recertified SOE error matches."""
+    from helpers import load_golden
+    from paper_2403_01521_b200.core import BoxGeometry, load_particles, make_system, save_particles
+    from paper_2403_01521_b200.soe import SOEApprox, load_soe_table, save_soe_table
+    g = load_golden("formats")
+    box = BoxGeometry(*[float(v) for v in g["box"]])
+    p = tmp_path / "ref_particles.csv"
+    p.write_text(str(g["particles_csv"]))
+    s = load_particles(str(p), box=box)
+    for ours, key in ((s.charge, "particles_q"), (s.mass, "particles_m"),
+                      (s.pos, "particles_pos"), (s.vel, "particles_vel")):
+        assert np.array_equal(ours, g[key]), key
+    mine = tmp_path / "ours.csv"
+    save_particles(str(mine), make_system(g["src_q"], g["src_m"], g["src_pos"], g["src_vel"],
+                                          box=box))
+    assert mine.read_text() == str(g["particles_csv"])
+    for tag in ("soe8", "soe16", "hand"):
+        f = tmp_path / f"{tag}.csv"
+        f.write_text(str(g[f"{tag}_csv"]))
+        t = load_soe_table(str(f))
+        assert np.array_equal(t.w, g[f"{tag}_w"]) and np.array_equal(t.s, g[f"{tag}_s"]), tag
+        assert t.eps_certified == pytest.approx(float(g[f"{tag}_eps"]), rel=1e-12), tag
+        out = tmp_path / f"{tag}_ours.csv"
+        save_soe_table(str(out), SOEApprox(m=len(t.w), w=t.w, s=t.s,
+                                           eps_certified=t.eps_certified, domain_max=20.0))
+        assert out.read_text() == str(g[f"{tag}_csv"]), tag

@@ -80,3 +80,24 @@ def test_oracle_large_config_perm_hashes():
         wl = make_workload(name)
         perm = O.sort_perm(wl.system.pos[:, 2], wl.box.lz)
         assert _sha(perm) == str(g["perm_sha"]), name
+
+
+def test_oracle_batch_energies_match_reference():
+    """The oracle's forward sweep (energy only) per injected batch equals the
+    reference's _rb_batch_energy_kernel (tests/golden/batches.npz)."""
+    from oracle import oracle as O
+    from paper_2403_01521_b200.configs import make_workload
+    from paper_2403_01521_b200.soe import build_soe_contour
+    g = load_golden("batches")
+    wl = make_workload("cfg5_1e4")
+    soe = build_soe_contour(wl.m)
+    perm = O.sort_perm(wl.system.pos[:, 2], wl.box.lz)
+    xs, ys, zs = (np.ascontiguousarray(wl.system.pos[perm, i]) for i in range(3))
+    qs = wl.system.charge[perm]
+    P = int(g["P"])
+    cv = O.rb_commonv(float(g["H"]), P, wl.alpha)
+    scale = np.max(np.abs(g["batch_u"]))
+    for b in (0, 17, int(g["n_batches"]) - 1):
+        u, _ = O.fourier_sweep(xs, ys, zs, qs, g["modes"][b * P:(b + 1) * P], cv, soe.w, soe.s,
+                               wl.alpha, wl.box.area, nthreads=4)
+        assert abs(u - g["batch_u"][b]) <= 1e-12 * scale, b
