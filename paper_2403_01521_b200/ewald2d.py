@@ -194,6 +194,74 @@ def zero_mode_energy_ref(system: ParticleSystem, box: BoxGeometry, alpha: float)
     return u
 
 
+class Ewald2DDevice:
+    """The O(N^2 K) Ewald2D evaluation (ewald2d.py:548-561) enqueued into caller
+    device buffers with no host synchronisation: the force field of an MD run
+    with ``solver="ewald2d"`` (reference md.py:149-150).  Per-run constants (the
+    ring table of the mode set, u_q, the k = 0 constant) are prepared once."""
+
+    def __init__(self, eng, params, box: BoxGeometry, Q: float, variant: str = "stable"):
+        from scipy.special import erfc as _erfc
+        import torch
+        from .engine import to_device
+        self.eng, self.params, self.box = eng, params, box
+        self.variant = 1 if variant == "naive" else 0
+        km = params.kmodes
+        self.nmode = km.shape[0]
+        self.u_q = float(np.sum(np.pi * Q / (km[:, 2] * box.area) *
+                                _erfc(km[:, 2] / (2 * params.alpha)))) if self.nmode else 0.0
+        self.const0 = -SQRT_PI * Q / (params.alpha * box.area)
+        if self.nmode:
+            mx, my, ring, kap = _ring_table(params, box)
+            self.mxy = torch.as_tensor(np.ascontiguousarray(np.column_stack([mx, my]))).to(
+                eng.device)
+            self.ring = torch.as_tensor(ring).to(eng.device)
+            self.kap = to_device(kap)
+            self.nring, self.mxmax, self.mymax = len(kap), int(np.max(np.abs(mx))), int(
+                np.max(np.abs(my)))
+
+    def enqueue(self, pos, q, forces, energy, status):
+        """forces (N,3) = total Ewald2D forces; energy[0:5] = (u_s, u_l_k, u_l_0,
+        u_self, u_ps), energy[5] = status bits (also OR-ed into ``status``)."""
+        import ctypes
+        import torch
+        from ._native import SlabBox, check
+        eng, box, prm = self.eng, self.box, self.params
+        n = q.numel()
+        dev = eng.device
+        p = lambda t: ctypes.c_void_p(t.data_ptr())
+        sbox = SlabBox(box.lx, box.ly, box.lz, box.sigma_top, box.sigma_bot)
+        st = eng._stream()
+        es = torch.zeros(1, dtype=torch.float64, device=dev)
+        sr_status = torch.zeros(1, dtype=torch.int32, device=dev)
+        check(eng.lib.slab_short_range(eng.ctx, p(pos), p(q), n, sbox, float(prm.alpha),
+                                       float(prm.r_c), p(forces), p(es), p(sr_status), st),
+              "slab_short_range")
+        ek = torch.zeros(8, dtype=torch.float64, device=dev)
+        if self.nmode and n >= 2:
+            fk = torch.empty((n, 3), dtype=torch.float64, device=dev)
+            check(eng.lib.slab_ewald_ref_fourier(
+                eng.ctx, p(pos), p(q), n, float(box.lx), float(box.ly), float(prm.alpha),
+                p(self.mxy), p(self.ring), self.nmode, p(self.kap), self.nring, self.mxmax,
+                self.mymax, self.variant, p(fk), p(ek), st), "slab_ewald_ref_fourier")
+            forces += fk
+        e0 = torch.zeros(8, dtype=torch.float64, device=dev)
+        if n >= 2:
+            fz = torch.empty(n, dtype=torch.float64, device=dev)
+            check(eng.lib.slab_ewald_ref_zero(eng.ctx, p(pos), p(q), n, float(prm.alpha), p(fz),
+                                              p(e0), st), "slab_ewald_ref_zero")
+            forces[:, 2] += (2.0 * np.pi / box.area) * fz
+        ec = eng.constant_terms(pos, q, box, prm.alpha)
+        forces[:, 2] += (-2.0 * np.pi * (box.sigma_top - box.sigma_bot)) * q
+        energy[0] = es[0]
+        energy[1] = ek[0] + self.u_q
+        energy[2] = -(2.0 * np.pi / box.area) * e0[0] + (self.const0 if n else 0.0)
+        energy[3] = ec[3]
+        energy[4] = ec[4]
+        energy[5] = sr_status[0].to(torch.float64)
+        status.bitwise_or_(sr_status)
+
+
 def ref_energy_forces(system: ParticleSystem, box: BoxGeometry, params,
                       variant: str = "stable"):
     """Full Ewald2D reference evaluation: EnergyBreakdown plus forces

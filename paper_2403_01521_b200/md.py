@@ -147,11 +147,10 @@ class _ForceField:
         self.c_q = None
         self._cv = None
         self._uq = 0.0
+        self._Q = float(np.sum(np.asarray(charge) ** 2))
+        self._ewald = None
         if opts.coulomb:
-            if opts.solver not in ("soewald2d", "rbse2d"):
-                if opts.solver == "ewald2d":
-                    raise NotImplementedError(
-                        "the O(N^2) Ewald2D reference solver is outside this device path")
+            if opts.solver not in ("soewald2d", "rbse2d", "ewald2d"):
                 raise ValueError(f"unknown solver {opts.solver!r}")
             alpha = opts.alpha
             if alpha is None:
@@ -160,9 +159,17 @@ class _ForceField:
                                      prefactor=0.8, s=opts.s)
             self.params = make_ewald_params(alpha, opts.s, box)
             check_short_range_cutoff(box, self.params.r_c)
-            self.soe = build_soe_contour(opts.soe_size)
-            Q = float(np.sum(np.asarray(charge) ** 2))
-            if opts.solver == "rbse2d":
+            self.soe = build_soe_contour(opts.soe_size) if opts.solver != "ewald2d" else None
+            Q = self._Q
+            if opts.solver == "ewald2d":
+                # the reference evaluates ref_energy_forces, which requires neutrality
+                from .core import validate_neutrality
+                ok, residual = validate_neutrality(
+                    ParticleSystem(np.asarray(charge), np.ones(len(charge)),
+                                   np.zeros((len(charge), 3)), np.zeros((len(charge), 3))), box)
+                if not ok:
+                    raise ValueError(f"system is not charge neutral (residual {residual:g})")
+            elif opts.solver == "rbse2d":
                 self.sampler = ModeSampler(alpha, box, seed=rb_seed)
                 self.H = normalization_H(alpha, box)
                 self.c_q = charge_term_sum(alpha, box, Q)
@@ -174,7 +181,10 @@ class _ForceField:
         if self._dev is None:
             from .engine import _SOEPack, to_device
             d = {}
-            if self.opts.coulomb:
+            if self.opts.coulomb and self.opts.solver == "ewald2d":
+                from .ewald2d import Ewald2DDevice
+                self._ewald = Ewald2DDevice(eng, self.params, self.box, self._Q)
+            elif self.opts.coulomb:
                 d["pack"] = _SOEPack(self.soe)
                 if self.opts.solver == "soewald2d":
                     km = self.params.kmodes
@@ -187,7 +197,9 @@ class _ForceField:
         import torch
         opts = self.opts
         dev = self._device_consts(eng)
-        if opts.coulomb:
+        if opts.coulomb and opts.solver == "ewald2d":
+            self._ewald.enqueue(pos, q, forces, ebuf[:8], status)
+        elif opts.coulomb:
             if opts.solver == "soewald2d":
                 modes, cv, cconst = dev["modes"], dev["cv"], self._uq
             else:

@@ -244,6 +244,21 @@ def golden_md() -> dict:
     return out
 
 
+def golden_md_ewald() -> dict:
+    """md.py with solver="ewald2d" (md.py:149-150, the O(N^2 K) reference solver as
+    the force field): a 20-step NVE trajectory of the md_system slab."""
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    from slabewald import md
+    charge, mass, pos, vel = md_system()
+    box = core.BoxGeometry(8.0, 8.0, 6.0)
+    sysm = core.ParticleSystem(charge=charge, mass=mass, pos=pos.copy(), vel=vel.copy())
+    opts = md.MDOptions(dt=0.002, n_steps=20, thermostat="none", solver="ewald2d", alpha=1.0,
+                        s=3.0, sample_every=5, seed=3)
+    res = md.run_simulation(sysm, box, opts)
+    return dict(pos0=pos, vel0=vel, pos=res.positions, unwrapped=res.unwrapped,
+                vel=res.velocities, pot=res.potential, kin=res.kinetic, cons=res.conserved)
+
+
 def golden_ewald_ref() -> dict:
     """ewald2d.py: the O(N^2 K) Ewald2D reference on two small neutral systems
     (stable and naive xi kernels, k = 0 mode, full breakdown)."""
@@ -365,6 +380,7 @@ def main(argv):
                 golden_batches() if name == "batches" else
                 golden_formats() if name == "formats" else
                 golden_md() if name == "md" else
+                golden_md_ewald() if name == "md_ewald" else
                 golden_ewald_ref() if name == "ewald_ref" else golden_workload(name))
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in data.items()})
