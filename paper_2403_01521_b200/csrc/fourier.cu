@@ -869,8 +869,13 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
     for (int l = 0; l < MH; ++l) {
       sgr += HR[l].re;
       sgi += HI[l].re;
+#if SLAB_SWEEP_NOB  // timing probe only (wrong results): the b-weighted readouts without b
+      sbr += HR[l].re - HR[l].im;
+      sbi += HI[l].re - HI[l].im;
+#else
       sbr = fma(b.re[l], HR[l].re, fma(-b.im[l], HR[l].im, sbr));
       sbi = fma(b.re[l], HI[l].re, fma(-b.im[l], HI[l].im, sbi));
+#endif
     }
     const double ps = sigma * sn;  // phase e^{+-i theta} = (cs, ps)
     const double pr = fma(kappa, gk.re, -two_k * sgr);

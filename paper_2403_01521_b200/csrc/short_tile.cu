@@ -163,7 +163,8 @@ template <bool kTabOnly>
 __device__ __forceinline__ void tile_pair(double xi, double yi, double zi, double qi, double xj,
                                           double yj, double zj, double qj, bool live, double lx,
                                           double ly, double ilx, double ily, double alpha,
-                                          double rc2, double c, double& e, double& fx, double& fy, double& fz,
+                                          double rc2, double c, const double* __restrict__ etab,
+                                          double& e, double& fx, double& fy, double& fz,
                                           int& flag) {
   double dx = xi - xj, dy = yi - yj;
   const double dz = zi - zj;
@@ -182,7 +183,11 @@ __device__ __forceinline__ void tile_pair(double xi, double yi, double zi, doubl
   const double d = d2u * inv_d;
   const double qq = use ? qi * qj : 0.0;
   double er, g;
+#if SLAB_TILE_TABLE
+  erfc_gauss<kTabOnly>(alpha * d, etab, &er, &g);  // the 48-interval erfcx table (short.cu's)
+#else
   erfc_gauss_rat<kTabOnly>(alpha * d, &er, &g);
+#endif
   const double qe = qq * er;
   e = qe * inv_d;
   const double fmag = fma(qq * c, g, qe * inv_d) * (inv_d * inv_d);
@@ -191,7 +196,13 @@ __device__ __forceinline__ void tile_pair(double xi, double yi, double zi, doubl
   fz = fmag * dz;
 }
 
+#ifndef SLAB_TILE_TABLE
+#define SLAB_TILE_TABLE 0
+#endif
 struct TileShared {
+#if SLAB_TILE_TABLE
+  double etab[kErfcxTabSize];
+#endif
   float nfx[kTileWarps][32], nfy[kTileWarps][32];  // staged candidates: -(fp32 screen image)
   float nfz[kTileWarps][32];                       //   (SoA: float2 pairs for the f32x2 screen)
   int32_t cj[kTileWarps][32];                      // staged candidates: cell-sorted index
@@ -214,6 +225,13 @@ __global__ void __launch_bounds__(kTileThreads) short_tile_kernel(
     float rc2f, float rcf, double* __restrict__ forces, double* __restrict__ eblk,
     int* __restrict__ status) {
   __shared__ TileShared sh;
+#if SLAB_TILE_TABLE
+  load_erfcx_table(sh.etab);
+  __syncthreads();
+  const double* etab = sh.etab;
+#else
+  const double* etab = nullptr;
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   const double c = kTwoOverSqrtPi * alpha, ilx = 1.0 / lx, ily = 1.0 / ly;
@@ -430,11 +448,11 @@ __global__ void __launch_bounds__(kTileThreads) short_tile_kernel(
           double pe1, fx1, fy1, fz1, pe2, fx2, fy2, fz2;
           tile_pair<kTabOnly>(sh.hx[warp][h1_], sh.hy[warp][h1_], sh.hz[warp][h1_],
                               sh.hq[warp][h1_], sh.cx[warp][k1], sh.cy[warp][k1], sh.cz[warp][k1],
-                              sh.cq[warp][k1], l1, lx, ly, ilx, ily, alpha, rc2, c, pe1, fx1, fy1,
+                              sh.cq[warp][k1], l1, lx, ly, ilx, ily, alpha, rc2, c, etab, pe1, fx1, fy1,
                               fz1, flag);
           tile_pair<kTabOnly>(sh.hx[warp][h2_], sh.hy[warp][h2_], sh.hz[warp][h2_],
                               sh.hq[warp][h2_], sh.cx[warp][k2], sh.cy[warp][k2], sh.cz[warp][k2],
-                              sh.cq[warp][k2], l2, lx, ly, ilx, ily, alpha, rc2, c, pe2, fx2, fy2,
+                              sh.cq[warp][k2], l2, lx, ly, ilx, ily, alpha, rc2, c, etab, pe2, fx2, fy2,
                               fz2, flag);
           E += pe1;
           E += pe2;
