@@ -589,6 +589,10 @@ constexpr int64_t kForkMaxN = SLAB_FORK_MAX_N;
 #define SLAB_FORK_HOST 1
 #endif
 constexpr bool kForkHost = SLAB_FORK_HOST;
+#ifndef SLAB_FORK_SORT
+#define SLAB_FORK_SORT 1
+#endif
+constexpr bool kForkSort = SLAB_FORK_SORT;
 #ifndef SLAB_PAR_ZERO
 #define SLAB_PAR_ZERO 1
 #endif
@@ -732,7 +736,13 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   // the sort / Fourier / k = 0 chain on ctx->hi (highest priority); both join
   // back into `st` before the assembly.  (A z-split phase 1 returns with the
   // short range possibly still running; phase 2 joins it.)
-  const bool fork = !a->skip_short_range && n > 0 && (n <= kForkMaxN || (host_entry && kForkHost));
+  const bool fork_all = !a->skip_short_range && n > 0 && (n <= kForkMaxN || (host_entry && kForkHost));
+  // Large systems on device buffers: only the z sort + gather run beside the
+  // short range (latency-bound passes that barely compete with it); the scan
+  // waits for the short range, so its kernels keep the GPU to themselves.
+  const bool fork_sort = kForkSort && !fork_all && !a->skip_short_range && n > 0 &&
+                         a->phase == 0;
+  const bool fork = fork_all || fork_sort;
   // the k = 0 chain (aggregate, carry, sweep: low-occupancy kernels) runs on
   // ctx->aux beside the Fourier chain once the decay table exists
   const bool par_zero = kParZero && a->phase == 0 && n >= 2 && lead;
@@ -767,6 +777,7 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
                              sl));
     }
     ctx->zs_perm = perm;
+    if (fork_sort) CK(cudaStreamWaitEvent(sl, ctx->ev_short, 0));  // scan after the short range
     if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, sl));
     if (n >= 2) {
       if (zsplit && !lead)  // rows of this rank's chunk range only (no k = 0 mode here)
