@@ -102,6 +102,11 @@ struct SOEHost {
   slab::BVec b{};
   slab::WVec w{};
   slab::ZCoef z{};
+  // lone complex terms (no conjugate partner): the swapped second pass, pairs
+  // (s_l, i w_l / 2) evaluated with inputs (u_i, -u_r) -- see prepare_soe
+  int mh2 = 0;
+  slab::BVec b2{};
+  slab::WVec w2{};
 };
 
 // The kernels run over conjugate PAIRS (s, w), (conj s, conj w): per pair two
@@ -122,6 +127,7 @@ int prepare_soe(const SlabSOE& soe, double alpha, SOEHost& out) {
   cd ps[24], pw[24];
   int mh = 0;
   out.real_terms = 0;
+  out.mh2 = 0;
   for (int l = 0; l < m; ++l) {
     if (used[l]) continue;
     used[l] = true;
@@ -139,9 +145,30 @@ int prepare_soe(const SlabSOE& soe, double alpha, SOEHost& out) {
         r = j;
         break;
       }
-    if (r < 0)
-      return fail(SLAB_ERR_UNSUPPORTED,
-                  "SOE table is not conjugate-symmetric (a complex term without its conjugate)");
+    if (r < 0) {
+      // A lone complex term F(s, w) (soewald2d.py:85-208 accepts any table).  With
+      // G(s, w) = F(s, w) + F(conj s, conj w) -- one pair of the main pass --
+      // F(s, w) = 1/2 G(s, w) - (i/2) G(s, i w): the pair (s, w/2) joins the main
+      // pass, and the pair (s, i w/2) a second pass whose real inputs are swapped
+      // (u_r, u_i) -> (u_i, -u_r), which multiplies that pass's p, zeta and g chain
+      // by -i (FourierPlan::swap).  The k = 0 mode has real inputs, so there the
+      // lone term is exactly the half-weight pair.
+      const cd s_l(soe.h_s_re[l], soe.h_s_im[l]), w_l(soe.h_w_re[l], soe.h_w_im[l]);
+      if (std::abs(s_l.imag()) < 1e-5 * s_l.real())
+        return fail(SLAB_ERR_UNSUPPORTED,
+                    "a lone complex SOE term with a near-real exponent is not supported");
+      if (out.mh2 >= 12) return fail(SLAB_ERR_UNSUPPORTED, "more than 12 lone complex SOE terms");
+      ps[mh] = s_l;
+      pw[mh] = 0.5 * w_l;
+      ++mh;
+      const cd w2 = cd(0.0, 0.5) * w_l;
+      out.b2.re[out.mh2] = alpha * s_l.real();
+      out.b2.im[out.mh2] = alpha * s_l.imag();
+      out.w2.re[out.mh2] = w2.real();
+      out.w2.im[out.mh2] = w2.imag();
+      ++out.mh2;
+      continue;
+    }
     used[r] = true;
     ps[mh] = cd(soe.h_s_re[l], soe.h_s_im[l]);
     pw[mh] = cd(soe.h_w_re[l], soe.h_w_im[l]);
@@ -170,18 +197,27 @@ int prepare_soe(const SlabSOE& soe, double alpha, SOEHost& out) {
   return SLAB_OK;
 }
 
+// plan of the lone-term pass (prepare_soe): same modes, mh2 swapped pairs
+slab::FourierPlan lone_plan(const SOEHost& sh, int64_t n, int nmode, int dirs) {
+  auto p = slab::fourier_plan(n, nmode, sh.mh2 > 0 ? sh.mh2 : 1, dirs);
+  p.swap = 1;
+  return p;
+}
+
 // workspace for the z-sorted part of an evaluation
 struct SortedWork {
   slab::SortWork sw;
   double *xs, *ys, *zs, *qs;
   double2* dtab;
+  double2* dtab2;  // decay table of the lone-term pass (mh2 columns)
+  double* elone;   // energies of the lone-term pass (one per batch / one)
   double* fwork;
   double* zwork;
   double *fsorted, *fzf, *fzb;
 };
 
 size_t sorted_bytes(int64_t n, int mh, const slab::FourierPlan& fp, const slab::ZeroPlan& zp,
-                    bool with_sort) {
+                    bool with_sort, int mh2 = 0, const slab::FourierPlan* fp2 = nullptr) {
   const size_t N = (size_t)(n > 0 ? n : 1);
   size_t b = 0;
   if (with_sort) {
@@ -189,14 +225,18 @@ size_t sorted_bytes(int64_t n, int mh, const slab::FourierPlan& fp, const slab::
     b += 4 * pad(8 * N);
   }
   b += pad(sizeof(double2) * (N + 1) * mh);
-  b += pad(8 * slab::fourier_work_doubles(fp));
+  b += pad(sizeof(double2) * (N + 1) * (size_t)mh2) + pad(8 * 4096);
+  size_t fw = slab::fourier_work_doubles(fp);
+  if (fp2 && slab::fourier_work_doubles(*fp2) > fw) fw = slab::fourier_work_doubles(*fp2);
+  b += pad(8 * fw);
   b += pad(8 * slab::zero_work_doubles(zp));
   b += pad(24 * N) + 2 * pad(8 * N);
   return b;
 }
 
 void carve_sorted(Carver& cv, int64_t n, int mh, const slab::FourierPlan& fp,
-                  const slab::ZeroPlan& zp, bool with_sort, SortedWork& w) {
+                  const slab::ZeroPlan& zp, bool with_sort, SortedWork& w, int mh2 = 0,
+                  const slab::FourierPlan* fp2 = nullptr) {
   const size_t N = (size_t)(n > 0 ? n : 1);
   if (with_sort) {
     w.sw.k0 = cv.take<uint64_t>(N);
@@ -210,7 +250,11 @@ void carve_sorted(Carver& cv, int64_t n, int mh, const slab::FourierPlan& fp,
     w.qs = cv.take<double>(N);
   }
   w.dtab = cv.take<double2>((N + 1) * mh);
-  w.fwork = cv.take<double>(slab::fourier_work_doubles(fp));
+  w.dtab2 = cv.take<double2>((N + 1) * (size_t)mh2);
+  w.elone = cv.take<double>(4096);
+  size_t fwd = slab::fourier_work_doubles(fp);
+  if (fp2 && slab::fourier_work_doubles(*fp2) > fwd) fwd = slab::fourier_work_doubles(*fp2);
+  w.fwork = cv.take<double>(fwd);
   w.zwork = cv.take<double>(slab::zero_work_doubles(zp));
   w.fsorted = cv.take<double>(3 * N);
   w.fzf = cv.take<double>(N);
@@ -303,13 +347,15 @@ int slab_fourier_sweep(SlabCtx* ctx, const double* d_x, const double* d_y, const
   int rc = prepare_soe(soe, alpha, sh);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  auto fp = slab::fourier_plan(n, (int)nmode, sh.mh, (want_forces && d_forces_sorted) ? 2 : 1);
+  const int dirs = (want_forces && d_forces_sorted) ? 2 : 1;
+  auto fp = slab::fourier_plan(n, (int)nmode, sh.mh, dirs);
+  auto fp2 = lone_plan(sh, n, (int)nmode, dirs);
   auto zp = slab::zero_plan(n, sh.mh);
-  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, false) + 4096);
+  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, false, sh.mh2, &fp2) + 4096);
   if (rc) return rc;
   Carver cv{(char*)ctx->arena};
   SortedWork w{};
-  carve_sorted(cv, n, sh.mh, fp, zp, false, w);
+  carve_sorted(cv, n, sh.mh, fp, zp, false, w, sh.mh2, &fp2);
   slab::FourierWork fw;
   slab::fourier_work_carve(fp, w.fwork, fw);
   CK(cudaMemsetAsync(d_energy, 0, sizeof(double), st));
@@ -320,6 +366,14 @@ int slab_fourier_sweep(SlabCtx* ctx, const double* d_x, const double* d_y, const
   CK(slab::fourier_run(fp, fw, d_x, d_y, d_z, d_q, w.dtab, d_modes, d_commonv, commonv_scalar,
                        area, sh.b, sh.w, want_forces && d_forces_sorted, d_energy, status,
                        d_forces_sorted, st));
+  if (sh.mh2) {  // lone complex terms: the swapped pass, added in
+    CK(slab::decay_table(d_z, n, sh.mh2, sh.b2, w.dtab2, st));
+    slab::fourier_work_carve(fp2, w.fwork, fw);
+    CK(slab::fourier_run(fp2, fw, d_x, d_y, d_z, d_q, w.dtab2, d_modes, d_commonv,
+                         commonv_scalar, area, sh.b2, sh.w2, want_forces && d_forces_sorted,
+                         w.elone, status, d_forces_sorted, st));
+    CK(slab::add_into(d_energy, w.elone, 1, st));
+  }
   return SLAB_OK;
 }
 
@@ -408,21 +462,25 @@ int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charg
   // length, chunk count, buffer counts): the arena is carved for the larger of
   // the two work areas and each pass re-carves it with its own plan
   auto fp = slab::fourier_plan(n, (int)(per * P), sh.mh, 1);
+  auto fp2 = lone_plan(sh, n, (int)(per * P), 1);
   const int64_t tail = nbatch % per;
   if (tail) {
     auto ft = slab::fourier_plan(n, (int)(tail * P), sh.mh, 1);
     if (slab::fourier_work_doubles(ft) > slab::fourier_work_doubles(fp)) fp = ft;
+    auto ft2 = lone_plan(sh, n, (int)(tail * P), 1);
+    if (slab::fourier_work_doubles(ft2) > slab::fourier_work_doubles(fp2)) fp2 = ft2;
   }
   auto zp = slab::zero_plan(n, sh.mh);
-  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, true) + 8192);
+  rc = ensure_arena(ctx, sorted_bytes(n, sh.mh, fp, zp, true, sh.mh2, &fp2) + 8192);
   if (rc) return rc;
   Carver cv{(char*)ctx->arena};
   SortedWork w{};
-  carve_sorted(cv, n, sh.mh, fp, zp, true, w);
+  carve_sorted(cv, n, sh.mh, fp, zp, true, w, sh.mh2, &fp2);
   int32_t* perm = nullptr;
   CK(slab::sort_by_z_device(d_pos + 2, 3, n, w.sw, st, &perm, d_status));
   CK(slab::gather_sorted(d_pos, d_charge, perm, n, w.xs, w.ys, w.zs, w.qs, nullptr, st));
   CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, st));
+  if (sh.mh2) CK(slab::decay_table(w.zs, n, sh.mh2, sh.b2, w.dtab2, st));
   for (int64_t b0 = 0; b0 < nbatch; b0 += per) {
     const int64_t nb = nbatch - b0 < per ? nbatch - b0 : per;
     auto fpb = slab::fourier_plan(n, (int)(nb * P), sh.mh, 1);
@@ -431,6 +489,14 @@ int slab_batch_energies(SlabCtx* ctx, const double* d_pos, const double* d_charg
     CK(slab::fourier_run(fpb, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, d_modes + 3 * b0 * P, nullptr,
                          commonv_scalar, area, sh.b, sh.w, 0, d_out + b0, d_status, nullptr, st,
                          (int)P));
+    if (sh.mh2) {  // lone complex terms: the swapped pass, per batch, added in
+      auto fpb2 = lone_plan(sh, n, (int)(nb * P), 1);
+      slab::fourier_work_carve(fpb2, w.fwork, fw);
+      CK(slab::fourier_run(fpb2, fw, w.xs, w.ys, w.zs, w.qs, w.dtab2, d_modes + 3 * b0 * P,
+                           nullptr, commonv_scalar, area, sh.b2, sh.w2, 0, w.elone, d_status,
+                           nullptr, st, (int)P));
+      CK(slab::add_into(d_out + b0, w.elone, (int)nb, st));
+    }
   }
   return SLAB_OK;
 }
@@ -593,6 +659,10 @@ constexpr bool kForkHost = SLAB_FORK_HOST;
 #define SLAB_FORK_SORT 1
 #endif
 constexpr bool kForkSort = SLAB_FORK_SORT;
+#ifndef SLAB_SPLIT_SHORT
+#define SLAB_SPLIT_SHORT 0
+#endif
+constexpr bool kSplitShort = SLAB_SPLIT_SHORT;
 #ifndef SLAB_PAR_ZERO
 #define SLAB_PAR_ZERO 1
 #endif
@@ -603,7 +673,10 @@ static int ensure_fork(SlabCtx* ctx) {
   int least = 0, greatest = 0;
   CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
   CK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
-  CK(cudaStreamCreateWithPriority(&ctx->lo, cudaStreamNonBlocking, least));
+#ifndef SLAB_SHORT_HI
+#define SLAB_SHORT_HI 0
+#endif
+  CK(cudaStreamCreateWithPriority(&ctx->lo, cudaStreamNonBlocking, SLAB_SHORT_HI ? greatest : least));
   CK(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, greatest));
   for (cudaEvent_t* e : {&ctx->ev_fork, &ctx->ev_short, &ctx->ev_long, &ctx->ev_x,
                          &ctx->ev_dtab, &ctx->ev_zero})
@@ -701,8 +774,9 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   if (a->phase != 0 && !zsplit) return fail(SLAB_ERR_ARG, "phases belong to the z-split mode");
   if (zsplit && a->phase == 0) return fail(SLAB_ERR_ARG, "z-split runs as phase 1 + phase 2");
   if (zsplit && a->nmode > 0 && !a->d_xchg) return fail(SLAB_ERR_ARG, "z-split needs d_xchg");
-  if (zsplit && sh.real_terms)  // the exchange is sized for m = 2 mh (slab_zsplit_exchange_doubles)
-    return fail(SLAB_ERR_UNSUPPORTED, "z-split needs a table of conjugate pairs (no real terms)");
+  if (zsplit && (sh.real_terms || sh.mh2))  // the exchange is sized for m = 2 mh
+    return fail(SLAB_ERR_UNSUPPORTED,
+                "z-split needs a table of conjugate pairs (no real or lone complex terms)");
   const bool forces = a->want_forces && n > 0;
   auto fp = slab::fourier_plan(n, (int)a->nmode, sh.mh, forces ? 2 : 1, zsplit ? scount : 1);
   if (zsplit) {  // this rank's contiguous chunk range of the z-sorted particles
@@ -710,10 +784,11 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     fp.c1 = (int)((int64_t)fp.nch * (srank + 1) / scount);
   }
   auto zp = slab::zero_plan(n, sh.mh);
+  auto fp2 = lone_plan(sh, n, (int)a->nmode, forces ? 2 : 1);
   auto sp = slab::short_plan(n, box.lx, box.ly, box.lz, a->r_c);
   if (sp.kcap < ctx->kcap_min) sp.kcap = ctx->kcap_min;
   const size_t N = (size_t)(n > 0 ? n : 1);
-  size_t bytes = sorted_bytes(n, sh.mh, fp, zp, true) + pad(24 * N) +
+  size_t bytes = sorted_bytes(n, sh.mh, fp, zp, true, sh.mh2, &fp2) + pad(24 * N) +
                  (a->skip_short_range ? 0 : pad(slab::short_work_bytes(sp))) + 8192;
   if (a->phase == 2 && bytes > ctx->arena_bytes)
     return fail(SLAB_ERR_ARG, "phase 2 without a matching phase 1 on this context");
@@ -721,7 +796,7 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   if (rc) return rc;
   Carver cv{(char*)ctx->arena};
   SortedWork w{};
-  carve_sorted(cv, n, sh.mh, fp, zp, true, w);
+  carve_sorted(cv, n, sh.mh, fp, zp, true, w, sh.mh2, &fp2);
   double* fshort = cv.take<double>(3 * N);
   void* swork = a->skip_short_range ? nullptr : cv.take<char>(slab::short_work_bytes(sp));
   slab::FourierWork fw;
@@ -743,6 +818,9 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   const bool fork_sort = kForkSort && !fork_all && !a->skip_short_range && n > 0 &&
                          a->phase == 0;
   const bool fork = fork_all || fork_sort;
+  // ... and with SLAB_SPLIT_SHORT the neighbour screen (no fp64 work) also runs
+  // beside the scan's first phase while the pair kernel waits for the scan's end
+  const bool split_short = kSplitShort && fork_sort;
   // the k = 0 chain (aggregate, carry, sweep: low-occupancy kernels) runs on
   // ctx->aux beside the Fourier chain once the decay table exists
   const bool par_zero = kParZero && a->phase == 0 && n >= 2 && lead;
@@ -760,7 +838,7 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
       CK(cudaStreamWaitEvent(ctx->hi, ctx->ev_fork, 0));
       CK(cudaStreamWaitEvent(ctx->lo, ctx->ev_fork, 0));
     }
-    if (!a->skip_short_range) {
+    if (!a->skip_short_range && !split_short) {
       cudaStream_t ss = fork ? ctx->lo : st;
       if (pos_ready) CK(cudaStreamWaitEvent(ss, pos_ready, 0));
       if (charge_ready) CK(cudaStreamWaitEvent(ss, charge_ready, 0));
@@ -777,7 +855,8 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
                              sl));
     }
     ctx->zs_perm = perm;
-    if (fork_sort) CK(cudaStreamWaitEvent(sl, ctx->ev_short, 0));  // scan after the short range
+    if (fork_sort && !split_short)  // scan after the short range
+      CK(cudaStreamWaitEvent(sl, ctx->ev_short, 0));
     if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, sl));
     if (n >= 2) {
       if (zsplit && !lead)  // rows of this rank's chunk range only (no k = 0 mode here)
@@ -827,6 +906,15 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
       }
       CK(slab::fourier_phase2(fp, fw, w.xs, w.ys, w.zs, w.qs, w.dtab, sh.b, forces ? 1 : 0,
                               u_sweep, w.fsorted, tin, sl));
+      if (sh.mh2) {  // lone complex terms: the swapped pass (phase 0 only, see above)
+        CK(slab::decay_table(w.zs, n, sh.mh2, sh.b2, w.dtab2, sl));
+        slab::FourierWork fw2;
+        slab::fourier_work_carve(fp2, w.fwork, fw2);
+        CK(slab::fourier_run(fp2, fw2, w.xs, w.ys, w.zs, w.qs, w.dtab2, a->d_modes,
+                             a->d_commonv, a->commonv_scalar, area, sh.b2, sh.w2,
+                             forces ? 1 : 0, w.elone, ctx->status, w.fsorted, sl));
+        CK(slab::add_into(u_sweep, w.elone, 1, sl));
+      }
     }
     if (lead && !par_zero)
       CK(slab::zero_run_b(zp, w.zwork, w.zs, w.qs, w.dtab, sh.z, sh.b, a->alpha, forces ? 1 : 0,
@@ -834,6 +922,16 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     if (par_zero) CK(cudaStreamWaitEvent(sl, ctx->ev_zero, 0));
   }
   if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, sl));
+  if (split_short) {  // enqueued after the scan chain so the pair kernel can wait on its end
+    CK(cudaEventRecord(ctx->ev_long, sl));
+    if (pos_ready) CK(cudaStreamWaitEvent(ctx->lo, pos_ready, 0));
+    if (charge_ready) CK(cudaStreamWaitEvent(ctx->lo, charge_ready, 0));
+    const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
+    CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
+                       a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, ctx->lo, 0, 0.0,
+                       0.0, 0, ctx->ev_long));
+    CK(cudaEventRecord(ctx->ev_short, ctx->lo));
+  }
   if (fork) {  // join
     CK(cudaEventRecord(ctx->ev_long, sl));
     CK(cudaStreamWaitEvent(st, ctx->ev_long, 0));

@@ -345,7 +345,7 @@ template <int MH>
 __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier_aggregate_mma_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, int64_t n, int R, const double* __restrict__ modetab, int P,
-    int tiles_per_cta, BVec b, double2* __restrict__ carry, int c0) {
+    int tiles_per_cta, BVec b, double2* __restrict__ carry, int c0, int swap) {
   constexpr int MHP = mma_mhp(MH);  // pairs padded to whole n-tiles of 4 pairs
   constexpr int NT = MHP / 2;       // n-tiles: 2 directions x MHP/4
   constexpr int NCOL = 8 * NT;      // (dir, l, re/im) columns
@@ -470,14 +470,18 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
       const double sgn = dir == 0 ? 1.0 : -1.0;  // backward I input is +q sin = -ui
       SLAB_BOUND((size_t)c * nc * nitems + (size_t)(MH + l) * nitems + item,
                  (size_t)(c + 1) * nc * nitems);
-      out[(size_t)l * nitems + item] = make_double2(acc[0][u][0], acc[0][u][1]);
-      out[(size_t)(MH + l) * nitems + item] =
-          make_double2(sgn * acc[1][u][0], sgn * acc[1][u][1]);
+      // R slot <- row 0 (q cos), I slot <- row 1 (-+ q sin); swapped pass:
+      // R slot <- the I input, I slot <- minus the R input
+      const double2 rs = make_double2(acc[0][u][0], acc[0][u][1]);
+      const double2 is = make_double2(sgn * acc[1][u][0], sgn * acc[1][u][1]);
+      out[(size_t)l * nitems + item] = swap ? is : rs;
+      out[(size_t)(MH + l) * nitems + item] = swap ? make_double2(-rs.x, -rs.y) : is;
     }
   }
-  if (kk == 0) {
-    out[(size_t)(2 * MH) * nitems + t] = make_double2(gfr, gfi);
-    out[(size_t)(2 * MH) * nitems + P + t] = make_double2(gbr, gbi);
+  if (kk == 0) {  // the g chain's input is u itself: swapped, -i u
+    out[(size_t)(2 * MH) * nitems + t] = swap ? make_double2(gfi, -gfr) : make_double2(gfr, gfi);
+    out[(size_t)(2 * MH) * nitems + P + t] =
+        swap ? make_double2(gbi, -gbr) : make_double2(gbr, gbi);
   }
 }
 
@@ -738,7 +742,7 @@ static int carry_groups(int nch, int items, int mh) {
 // smem and 3*kSB lanes row-sum them; each warp writes its own partial buffer
 // (forward and backward lanes to separate buffers), reduced in fixed order
 // afterwards: deterministic, no atomics.
-template <int MH>
+template <int MH, bool kSwap>
 __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
@@ -931,7 +935,8 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
       }
     }
     // T_a = S_a + u_a: real input scaled by C_l into the scaled state
-    const double ur = q * cs, ui = -sigma * q * sn;
+    const double ur0 = q * cs, ui0 = -sigma * q * sn;
+    const double ur = kSwap ? ui0 : ur0, ui = kSwap ? -ur0 : ui0;
 #pragma unroll
     for (int l = 0; l < MH; ++l) {
       const double2 cl = sCl[l * blockDim.x];
@@ -1171,10 +1176,11 @@ static void set_attrs() {
   const unsigned long long bit = 1ull << (dev & 63);
   if (done & bit) return;
   // largest shared-memory carveout so two CTAs of each fit per SM
-  cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sweep_smem(kMaxR, MH, 8));
-  cudaFuncSetAttribute(fourier_sweep_kernel<MH>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       100);
+  for (auto fn : {fourier_sweep_kernel<MH, false>, fourier_sweep_kernel<MH, true>}) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sweep_smem(kMaxR, MH, 8));
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
   cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)agg_mma_smem(kMaxR, MH));
   cudaFuncSetAttribute(fourier_aggregate_mma_kernel<MH>,
@@ -1213,7 +1219,7 @@ static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const d
     const int ngy = (tiles + kAggMaxWarps - 1) / kAggMaxWarps;
     const int tpc = (tiles + ngy - 1) / ngy;
     fourier_aggregate_mma_kernel<MH><<<dim3(nch_r, ngy), tpc * 32, agg_mma_smem(p.R, MH), st>>>(
-        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry, p.c0);
+        xs, ys, zs, qs, p.n, p.R, w.modetab, p.P, tpc, b, w.carry, p.c0, p.swap);
     const dim3 cg = carry_grid(p);
     const int nseg = cg.z * kCarrySegs;
     fourier_carry_compose_kernel<<<cg, 32 * kCarrySegs, 0, st>>>(
@@ -1258,9 +1264,14 @@ static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const d
         w.carry, p.nch, p.c0, p.c1, p.P, p.items, MH, nseg, w.modetab, w.dchunk,
         w.dchunk + (size_t)p.nch * MH, w.zbound, segmap);
   }
-  fourier_sweep_kernel<MH><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
-      xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
-      w.fpart, want_forces, p.c0);
+  if (p.swap)
+    fourier_sweep_kernel<MH, true><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
+        xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
+        w.fpart, want_forces, p.c0);
+  else
+    fourier_sweep_kernel<MH, false><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
+        xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
+        w.fpart, want_forces, p.c0);
   return cudaGetLastError();
 }
 
@@ -1342,6 +1353,16 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
             w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
     }
   }
+  return cudaGetLastError();
+}
+
+// dst[i] += src[i] (the lone-term pass's energies into the main pass's)
+__global__ void add_into_kernel(double* __restrict__ dst, const double* __restrict__ src, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) dst[i] += src[i];
+}
+cudaError_t add_into(double* dst, const double* src, int count, cudaStream_t st) {
+  if (count > 0) add_into_kernel<<<(count + 255) / 256, 256, 0, st>>>(dst, src, count);
   return cudaGetLastError();
 }
 

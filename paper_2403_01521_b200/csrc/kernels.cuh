@@ -55,6 +55,8 @@ struct FourierPlan {
   int items;      // active (mode, direction) items: 2P, or P for energy-only (forward)
   int c0, c1;     // chunk range this plan scans (z-split multi-GPU rank), default [0, nch)
   size_t smem_sweep;
+  int swap;       // 1: real inputs swapped (u_r, u_i) -> (u_i, -u_r), i.e. the pass's result
+                  // times -i (lone complex SOE terms, capi.cu prepare_soe)
 };
 FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2, int ranks = 1);
 // bytes of device workspace the plan needs (carry, chunk decays, mode table, partials)
@@ -80,6 +82,7 @@ cudaError_t fourier_run(const FourierPlan& p, const FourierWork& w, const double
                         double commonv_scalar, double area, const BVec& b, const WVec& wv,
                         int want_forces, double* energy_out, int* status, double* forces_sorted,
                         cudaStream_t st, int seg_len = 0);  // seg_len > 0: energy per segment
+cudaError_t add_into(double* dst, const double* src, int count, cudaStream_t st);
 // the same as two phases around a z-split exchange: phase 1 builds the chunk
 // range's aggregates (and, with `totals`, its total map per (comp, item):
 // 4 doubles each, the all-gather payload); fourier_zsplit_tin composes the
@@ -143,7 +146,8 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
                       double* energy_out, int* status, int64_t home_begin, int64_t home_end,
                       int* maxnn_out, cudaStream_t st, int kind = 0, double lj_eps = 0.0,
                       double lj_sigma = 0.0,  // kind 1: WCA core instead of erfc Coulomb
-                      int accumulate = 0);    // 1: forces += (full home range only)
+                      int accumulate = 0,     // 1: forces += (full home range only)
+                      cudaEvent_t pairs_after = nullptr);  // pair kernel waits on it
 
 // ---------------------------------------------------------------- md.cu
 int64_t md_partials(int64_t n);

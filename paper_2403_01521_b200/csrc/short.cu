@@ -898,7 +898,7 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
                       double* energy_out, int* status, int64_t h0, int64_t h1,
                       int* maxnn_out, cudaStream_t st, int kind, double lj_eps,
-                      double lj_sigma, int accumulate) {
+                      double lj_sigma, int accumulate, cudaEvent_t pairs_after) {
   const int64_t n = p.n;
   const double sig2 = lj_sigma * lj_sigma;
   if (n < 2 || h1 <= h0) {
@@ -1001,6 +1001,7 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
       nbr_build_kernel<1><<<(unsigned)nblk, kSRThreads, 0, st>>>(
           cpf, skey, start, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz, rc2f, p.kcap, nbr,
           nn, maxnn, status);
+    if (pairs_after) cudaStreamWaitEvent(st, pairs_after, 0);
     const int split = pair_split(nh);
     const int64_t pgrid = pair_grid((nh * split + kSRThreads - 1) / kSRThreads);
     // every pair has alpha d <= alpha r_c: below the table end -> branch-free form

@@ -12,8 +12,9 @@ Reference: ``pkg/src/slabewald/soe.py`` -- contour nodes ``_contour_nodes``
 The device kernels carry conjugate PAIRS of terms: a table is accepted when
 every term is real (carried as two half-weight copies) or has its bitwise
 conjugate elsewhere in the table.  Every contour built here is paired in
-mirrored order, ``s[M-1-l] == conj(s[l])`` (``is_conjugate_paired``); a table
-with a complex term lacking its conjugate raises ``NotImplementedError``.
+mirrored order, ``s[M-1-l] == conj(s[l])`` (``is_conjugate_paired``).  A complex
+term lacking its conjugate is evaluated too: as a half-weight pair plus a second,
+input-swapped device pass (``capi.cu`` prepare_soe).
 """
 
 from __future__ import annotations

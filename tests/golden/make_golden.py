@@ -259,6 +259,26 @@ def golden_md_ewald() -> dict:
                 vel=res.velocities, pot=res.potential, kin=res.kinetic, cons=res.conserved)
 
 
+def golden_lone_soe() -> dict:
+    """soe_energy_forces (soewald2d.py:398-438) with an SOE table whose complex
+    terms have no conjugate partners -- the reference sweep takes any (w, s)."""
+    core, ewald2d, rbse2d, rsoe, soewald2d = ref_modules()
+    rng = np.random.default_rng(31)
+    box = core.BoxGeometry(15.0, 15.0, 6.0)
+    n = 300
+    pos = rng.uniform([0, 0, 0.2], [15, 15, 5.8], size=(n, 3))
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    sysm = core.make_system(q, np.ones(n), pos, box=box)
+    w = np.array([0.7 - 0.2j, 0.3 + 0.9j, 1.1 + 0.1j])
+    sv = np.array([1.5 + 0.8j, 2.5 - 1.7j, 0.9 + 3.0j])
+    soe = rsoe.SOEApprox(m=3, w=w, s=sv, eps_certified=1.0, domain_max=20.0)
+    params = core.make_ewald_params(0.9, 3.0, box)
+    bd, f = soewald2d.soe_energy_forces(sysm, box, params, soe)
+    return dict(pos=sysm.pos, q=q, w=w, s=sv, alpha=0.9, s_par=3.0, box=np.array([15.0, 15.0, 6.0]),
+                u_s=bd.u_s, u_l_k=bd.u_l_k, u_l_0=bd.u_l_0, u_self=bd.u_self, u_ps=bd.u_ps,
+                forces=f)
+
+
 def golden_ewald_ref() -> dict:
     """ewald2d.py: the O(N^2 K) Ewald2D reference on two small neutral systems
     (stable and naive xi kernels, k = 0 mode, full breakdown)."""
@@ -381,6 +401,7 @@ def main(argv):
                 golden_formats() if name == "formats" else
                 golden_md() if name == "md" else
                 golden_md_ewald() if name == "md_ewald" else
+                golden_lone_soe() if name == "lone_soe" else
                 golden_ewald_ref() if name == "ewald_ref" else golden_workload(name))
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in data.items()})

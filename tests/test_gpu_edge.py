@@ -139,10 +139,62 @@ def test_real_and_unordered_soe_tables_match_oracle(pk, table):
     e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes,
                                 (H / 7) * (2 / np.sqrt(np.pi)) * alpha, 0.0)
     _check(bd, f, e_ref, f_ref)
-    bad = pk.SOEApprox(m=2, w=np.array([1.0 + 0.5j, 1.0 + 0j]),
-                       s=np.array([2.0 + 1j, 3.0 + 0j]), eps_certified=1.0, domain_max=20.0)
-    with pytest.raises(NotImplementedError, match="conjugate"):
-        pk.rb_energy_forces(s, box, params, bad, _Stub(modes), 7, H=H, c_q=0.0)
+
+
+@pytest.mark.parametrize("table", ["lone_plus_real", "contour_halves", "all_lone"])
+def test_lone_complex_soe_terms_match_oracle(pk, table):
+    """Tables with complex terms that have NO conjugate partner (the reference's
+    sweep takes any (w, s); load_soe_table reads any table): each lone term runs
+    as a half-weight pair plus a second, input-swapped pass (capi.cu
+    prepare_soe).  RB and full-mode-sum evaluations (energies, forces, k = 0
+    mode) and the batched energies against the oracle, which restates the
+    reference's per-term loops."""
+    rng = np.random.default_rng(31)
+    box = pk.BoxGeometry(15.0, 15.0, 6.0)
+    n = 700
+    s = pk.make_system(np.where(np.arange(n) % 2 == 0, 1.0, -1.0), np.ones(n),
+                       rng.uniform([0, 0, 0.2], [15, 15, 5.8], size=(n, 3)), box)
+    alpha = 0.9
+    params = pk.make_ewald_params(alpha, 3.0, box)
+    if table == "lone_plus_real":
+        w = np.array([1.0 + 0.5j, 1.0 + 0j])
+        sv = np.array([2.0 + 1j, 3.0 + 0j])
+    elif table == "contour_halves":   # a built table with two conjugates dropped
+        b8 = pk.build_soe_contour(8)
+        keep = [0, 1, 2, 3, 4, 6]           # terms 7 and 5 (partners of 0 and 2) removed
+        order = rng.permutation(len(keep))
+        w, sv = b8.w[keep][order], b8.s[keep][order]
+    else:
+        w = np.array([0.7 - 0.2j, 0.3 + 0.9j, 1.1 + 0.1j])
+        sv = np.array([1.5 + 0.8j, 2.5 - 1.7j, 0.9 + 3.0j])
+    soe = pk.SOEApprox(m=len(w), w=w, s=sv, eps_certified=1.0, domain_max=20.0)
+    modes = pk.ModeSampler(alpha, box, seed=4).batch(9)
+    H = pk.normalization_H(alpha, box)
+    cv = (H / 9) * (2 / np.sqrt(np.pi)) * alpha
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), 9, H=H, c_q=0.0)
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes, cv, 0.0)
+    _check(bd, f, e_ref, f_ref)
+    # the deterministic full mode sum through the same two passes
+    from paper_2403_01521_b200.soewald2d import full_sum_constants
+    cvf, uq = full_sum_constants(params, box, float(np.sum(s.charge ** 2)))
+    bdf, ff = pk.soe_energy_forces(s, box, params, soe)
+    e_reff, f_reff = _oracle_eval(pk, s, box, params, soe, params.kmodes, cvf, uq)
+    _check(bdf, ff, e_reff, f_reff)
+    # batched energies: every batch's forward sweep (one device pass + the lone pass)
+    import torch
+    from oracle import oracle as O
+    from paper_2403_01521_b200.engine import get_engine
+    eng = get_engine()
+    allm = pk.ModeSampler(alpha, box, seed=5).batch(5 * 9)
+    d = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(eng.device)
+    out, status = eng.batch_energies(d(s.pos), d(s.charge), soe, alpha, box.area, d(allm), 5, 9, cv)
+    got = out.cpu().numpy()
+    perm = O.sort_perm(s.pos[:, 2], box.lz)
+    xs, ys, zs = (np.ascontiguousarray(s.pos[perm, i]) for i in range(3))
+    for b in range(5):
+        u, _ = O.fourier_sweep(xs, ys, zs, s.charge[perm], allm[b * 9:(b + 1) * 9],
+                               np.full(9, cv), soe.w, soe.s, alpha, box.area)
+        assert abs(got[b] - u) <= E_TOL * max(abs(u), 1e-300), b
 
 
 @pytest.mark.parametrize("table", ["real_m1", "pairs_plus_real"])
@@ -351,3 +403,17 @@ def test_neighbour_overflow_mid_run_matches_oracle(pk, squeeze):
     e = e.cpu().numpy()
     bd = pk.EnergyBreakdown(*[float(x) for x in e[:5]])
     _check(bd, f.cpu().numpy(), e_ref, f_ref)
+
+
+def test_lone_complex_soe_table_matches_reference(pk):
+    """soe_energy_forces with lone complex SOE terms against the REAL reference's
+    output (tests/golden/lone_soe.npz)."""
+    from helpers import load_golden
+    g = load_golden("lone_soe")
+    box = pk.BoxGeometry(*[float(v) for v in g["box"]])
+    s = pk.make_system(g["q"], np.ones(len(g["q"])), g["pos"], box)
+    params = pk.make_ewald_params(float(g["alpha"]), float(g["s_par"]), box)
+    soe = pk.SOEApprox(m=3, w=g["w"], s=g["s"], eps_certified=1.0, domain_max=20.0)
+    bd, f = pk.soe_energy_forces(s, box, params, soe)
+    _check(bd, f, [float(g[k]) for k in ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps")],
+           g["forces"])

@@ -101,3 +101,20 @@ def test_oracle_batch_energies_match_reference():
         u, _ = O.fourier_sweep(xs, ys, zs, qs, g["modes"][b * P:(b + 1) * P], cv, soe.w, soe.s,
                                wl.alpha, wl.box.area, nthreads=4)
         assert abs(u - g["batch_u"][b]) <= 1e-12 * scale, b
+
+
+def test_oracle_lone_complex_soe_table_matches_reference():
+    """A table with lone complex terms (no conjugate partners) through the oracle's
+    full mode sum equals the reference's soe_energy_forces (golden lone_soe)."""
+    from paper_2403_01521_b200.core import BoxGeometry, make_ewald_params, make_system
+    from paper_2403_01521_b200.soewald2d import full_sum_constants
+    g = load_golden("lone_soe")
+    box = BoxGeometry(*[float(v) for v in g["box"]])
+    s = make_system(g["q"], np.ones(len(g["q"])), g["pos"], box=box)
+    params = make_ewald_params(float(g["alpha"]), float(g["s_par"]), box)
+    cv, uq = full_sum_constants(params, box, float(np.sum(s.charge ** 2)))
+    e, f, flag = O.energy_forces(s.pos, s.charge, box, params.alpha, params.r_c, params.kmodes,
+                                 cv, uq, g["w"], g["s"])
+    for val, key in zip(e, ("u_s", "u_l_k", "u_l_0", "u_self", "u_ps")):
+        assert val == pytest.approx(float(g[key]), rel=1e-13, abs=1e-13), key
+    assert np.max(np.abs(f - g["forces"])) <= 1e-13 * np.max(np.abs(g["forces"]))

@@ -13,7 +13,7 @@ from collections import Counter
 ROUND = sys.argv[1] if len(sys.argv) > 1 else "r02"
 OBJ = "paper_2403_01521_b200/_lib/obj"
 KERNELS = [
-    ("fourier.o", "fourier_sweep_kernelILi8E", "fourier_sweep_kernel<8>"),
+    ("fourier.o", "fourier_sweep_kernelILi8ELb0E", "fourier_sweep_kernel<8>"),
     ("fourier.o", "fourier_aggregate_mma_kernelILi8E", "fourier_aggregate_mma_kernel<8>"),
     ("fourier.o", "fourier_carry_compose_kernel", "fourier_carry_compose_kernel"),
     ("zero.o", "zero_sweep_kernelILi8E", "zero_sweep_kernel<8>"),
