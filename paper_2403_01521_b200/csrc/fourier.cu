@@ -40,6 +40,17 @@ namespace slab {
 #ifndef SLAB_SWEEP_CB
 #define SLAB_SWEEP_CB 0
 #endif
+#ifndef SLAB_SWEEP_GDECAY
+#define SLAB_SWEEP_GDECAY 0
+#endif
+#ifndef SLAB_SWEEP_REM
+#define SLAB_SWEEP_REM 1
+#endif
+constexpr bool kSweepRem = SLAB_SWEEP_REM;
+#ifndef SLAB_SWEEP_REM_MAX
+#define SLAB_SWEEP_REM_MAX 8  // cfg3 (16 left over of 400) ran 2.21 -> 2.37 ms with it
+#endif
+constexpr int kSweepRemMax = SLAB_SWEEP_REM_MAX;
 #ifndef SLAB_SWEEP_PIPE
 #define SLAB_SWEEP_PIPE 0  // 1: next particle's sincos/exp issued one iteration ahead (measured 2.5% slower since exp_neg went branch-free)
 #endif
@@ -781,7 +792,9 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
     sz[0] = zs[a0 > 0 ? a0 - 1 : 0];
     sz[len + 1] = zs[a1 < n ? a1 : a1 - 1];
   }
+#if !SLAB_SWEEP_GDECAY
   for (int e = threadIdx.x; e < (len + 1) * MH; e += blockDim.x) sd[e] = dtab[a0 * MH + e];
+#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nitems = 2 * P;
@@ -862,7 +875,11 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
     // S_a = T_{a-1} * d_a  (forward) / T'_{a+1} * d_{a+1} (backward)
 #pragma unroll
     for (int l = 0; l < MH; ++l) {
+#if SLAB_SWEEP_GDECAY  // experiment: decays straight from global memory (L1), not staged
+      const double2 d = __ldg(dtab + (a0 + id) * MH + l);
+#else
       const double2 d = sd[id * MH + l];
+#endif
       HR[l] = cmul(HR[l], C2{d.x, d.y});
       HI[l] = cmul(HI[l], C2{d.x, d.y});
     }
@@ -953,6 +970,172 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
     dk = dk_n;
     q = q_n;
 #endif
+  }
+  if (active && fwd) epart[(size_t)c * P + t] = E;
+}
+
+// ---------------------------------------------------------------------------
+// the remainder sweep: the last (items mod 32) items of every chunk
+// ---------------------------------------------------------------------------
+// A partial warp costs the fp64 pipe as much as a full one (measured at cfg4:
+// P = 100 -> 200 items = 6 full warps + 8 lanes took 4.18 ms, P = 112 -> 7 full
+// warps 4.16 ms, P = 96 -> 6 warps 3.63 ms).  So the main sweep runs the full
+// warps only and this kernel packs the leftover L <= 16 items of G = 32 / L
+// consecutive chunks into one warp: lane group g (L lanes) walks chunk
+// c0 + G w + g.  The groups walk different particles, so nothing is staged in
+// shared memory: particle data and decay rows come straight from global memory
+// (read once per group; small next to the main sweep).  Same recurrence and
+// epilogue as fourier_sweep_kernel; a group's force contributions are summed
+// in fixed order over its L lanes into the remainder's own partial buffer
+// (each particle has one remainder group): deterministic.
+constexpr int kRemWarps = 4;
+constexpr int kRemSB = 4;  // steps per force flush
+template <int MH, bool kSwap>
+__global__ void __launch_bounds__(32 * kRemWarps) fourier_sweep_rem_kernel(
+    const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
+    const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
+    const double* __restrict__ modetab, int P, int item0, int L, int G, BVec b,
+    const double2* __restrict__ carry, double* __restrict__ epart, double* __restrict__ frem,
+    int want_forces, int c0, int c1) {
+  __shared__ double stg[kRemWarps][kRemSB * 32 * 3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wg = blockIdx.x * kRemWarps + warp;
+  const int grp = lane / L;
+  const int c = c0 + wg * G + grp;
+  const bool active = lane < G * L && c < c1;
+  const int item = item0 + (lane % L);
+  const bool fwd = item < P;
+  const int t = fwd ? item : item - P;
+  const int nitems = 2 * P;
+  const int64_t a0 = active ? (int64_t)c * R : 0;
+  const int len = active ? (int)(a0 + R < n ? R : n - a0) : 0;
+  const double* mt = modetab + (size_t)t * mode_stride(MH);
+  const double kx = mt[0], ky = mt[1], k = mt[2];
+  const double sigma = fwd ? 1.0 : -1.0;
+  const double fxy_c = active ? sigma * mt[3] : 0.0;
+  const double fz_c = active ? -sigma * mt[4] : 0.0;
+  const double kappa = mt[5];
+  const double two_k = 2.0 * k;
+  const int nc = ncomp_of(MH);
+  C2 HR[MH], HI[MH], CL[MH];
+  C2 gk{0.0, 0.0};
+  {
+    const double2* cin = carry + (size_t)(active ? c : c0) * nc * nitems + item;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      CL[l] = C2{mt[8 + 2 * l], mt[9 + 2 * l]};
+      const double2 r = cin[(size_t)l * nitems], im = cin[(size_t)(MH + l) * nitems];
+      HR[l] = cmul(CL[l], C2{r.x, r.y});
+      HI[l] = cmul(CL[l], C2{im.x, im.y});
+    }
+    const double2 gg = cin[(size_t)(2 * MH) * nitems];
+    gk = C2{gg.x, gg.y};
+  }
+  double E = 0.0;
+  // The next step's particle data and decay row are loaded one step ahead and
+  // its transcendentals computed one step ahead (nothing waits for them;
+  // registers are plentiful at this occupancy).  Forces are staged for kRemSB
+  // steps and summed per group in one pass.
+  double nx = 0.0, ny = 0.0, nq = 0.0, ndz = 0.0;
+  double2 nd[MH];
+  auto fetch = [&](int i) {
+    const bool live = i < len;
+    const int ia = fwd ? i : len - 1 - i;
+    const int64_t ag = live ? a0 + ia : 0;
+    nx = live ? __ldg(xs + ag) : 0.0;
+    ny = live ? __ldg(ys + ag) : 0.0;
+    nq = live ? __ldg(qs + ag) : 0.0;
+    ndz = 0.0;
+    if (live) {
+      if (fwd) ndz = ag > 0 ? __ldg(zs + ag) - __ldg(zs + ag - 1) : 0.0;  // (chunk start: carry)
+      else ndz = ag + 1 < n ? __ldg(zs + ag + 1) - __ldg(zs + ag) : 0.0;
+    }
+    const int64_t drow = live ? (fwd ? ag : ag + 1) : 0;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) nd[l] = __ldg(dtab + drow * MH + l);
+  };
+  double ncs, nsn, ndk;
+  auto trans = [&]() {  // transcendentals of the fetched step
+    ndk = exp_neg(k * ndz);
+    sincos_fast(__dadd_rn(__dmul_rn(kx, nx), __dmul_rn(ky, ny)), &nsn, &ncs);
+  };
+  fetch(0);
+  trans();
+  double* st = stg[warp];
+  for (int i = 0; i < R; ++i) {
+    const bool live = i < len;
+    const int ia = fwd ? i : len - 1 - i;
+    const int64_t ag = live ? a0 + ia : 0;
+    const double q = nq, cs = ncs, sn = nsn, dk = ndk;
+    double2 dd[MH];
+#pragma unroll
+    for (int l = 0; l < MH; ++l) dd[l] = nd[l];
+    if (i + 1 < R) {
+      fetch(i + 1);
+      trans();
+    }
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      HR[l] = cmul(HR[l], C2{dd[l].x, dd[l].y});
+      HI[l] = cmul(HI[l], C2{dd[l].x, dd[l].y});
+    }
+    gk.re *= dk;
+    gk.im *= dk;
+    double sgr = 0.0, sgi = 0.0, sbr = 0.0, sbi = 0.0;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      sgr += HR[l].re;
+      sgi += HI[l].re;
+      sbr = fma(b.re[l], HR[l].re, fma(-b.im[l], HR[l].im, sbr));
+      sbi = fma(b.re[l], HI[l].re, fma(-b.im[l], HI[l].im, sbi));
+    }
+    const double ps = sigma * sn;
+    const double pr = fma(kappa, gk.re, -two_k * sgr);
+    const double pi = fma(kappa, gk.im, -two_k * sgi);
+    const double er = fma(cs, pr, -ps * pi);
+    const double ei = fma(cs, pi, ps * pr);
+    E = fma(q, er, E);
+    if (want_forces) {
+      const double ztr = fma(2.0, sbr, -kappa * gk.re);
+      const double zti = fma(2.0, sbi, -kappa * gk.im);
+      const double fxy = fxy_c * q * ei;
+      const int slot = i % kRemSB;
+      double* row = st + slot * 32 * 3;
+      row[lane * 3 + 0] = live ? fxy * kx : 0.0;
+      row[lane * 3 + 1] = live ? fxy * ky : 0.0;
+      row[lane * 3 + 2] = live ? fz_c * q * fma(cs, ztr, -ps * zti) : 0.0;
+      if (slot == kRemSB - 1 || i == R - 1) {
+        __syncwarp();
+        // (slot, group, comp) sums in fixed order over the group's L lanes
+        const int ibase = i - slot;
+        for (int e = lane; e < (slot + 1) * G * 3; e += 32) {
+          const int sl = e / (3 * G), rem = e - sl * 3 * G, gg = rem / 3, comp = rem - 3 * gg;
+          const int cg = c0 + wg * G + gg;
+          const int64_t a0g = (int64_t)cg * R;
+          const int leng = cg < c1 ? (int)(a0g + R < n ? R : n - a0g) : 0;
+          const int ii = ibase + sl;
+          if (ii < leng) {
+            const double* rs = st + sl * 32 * 3;
+            double sum = 0.0;
+            for (int j = 0; j < L; ++j) sum += rs[(gg * L + j) * 3 + comp];
+            frem[(a0g + (fwd ? ii : leng - 1 - ii)) * 3 + comp] = sum;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    const double ur0 = q * cs, ui0 = -sigma * q * sn;
+    const double ur = kSwap ? ui0 : ur0, ui = kSwap ? -ur0 : ui0;
+#pragma unroll
+    for (int l = 0; l < MH; ++l) {
+      HR[l].re = fma(CL[l].re, ur, HR[l].re);
+      HR[l].im = fma(CL[l].im, ur, HR[l].im);
+      HI[l].re = fma(CL[l].re, ui, HI[l].re);
+      HI[l].im = fma(CL[l].im, ui, HI[l].im);
+    }
+    gk.re += ur;
+    gk.im += ui;
+    (void)ag;
   }
   if (active && fwd) epart[(size_t)c * P + t] = E;
 }
@@ -1067,10 +1250,27 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   // is the forward sum, soewald2d.py:138-170; the backward sweep only adds the
   // j-side forces, 172-202): active items = dirs * P, carry layout stays 2P
   p.items = (dirs == 1 ? 1 : 2) * P;
-  const int nitems = p.items;
+  // leftover items (items mod 32, <= 16) go to the remainder sweep, several
+  // chunks per warp; the main sweep then runs whole warps only
+  p.rem = 0;
+  p.rem_g = 0;
+  {
+    const int left = p.items % 32;
+    if (kSweepRem && p.items >= 32 && left > 0 && left <= kSweepRemMax) {
+      p.rem = left;
+      p.rem_g = 32 / left;
+      if (const char* env = getenv("SLAB_REM_G")) {  // tuning knob
+        const int gg = atoi(env);
+        if (gg >= 1 && gg <= 32 / left) p.rem_g = gg;
+      }
+    }
+  }
+  p.items_main = p.items - p.rem;
+  const int nitems = p.items_main;
   p.ngroups = (nitems + kSweepMaxThreads - 1) / kSweepMaxThreads;
   if (p.ngroups < 1) p.ngroups = 1;
   p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
+  if (p.rem) p.ipg = (p.ipg + 31) / 32 * 32;  // groups of whole warps
   if (p.ipg < 1) p.ipg = 1;
   p.warps = (p.ipg + 31) / 32;
   if (p.warps < 1) p.warps = 1;
@@ -1118,6 +1318,8 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   const int g_of_p = P / p.ipg;  // group containing item P (first backward item)
   const bool mixed = P < nitems && ((P - g_of_p * p.ipg) % 32) != 0;
   p.nbuf = p.ngroups * p.warps + (mixed ? 1 : 0);
+  p.rem_buf = p.nbuf;
+  if (p.rem) p.nbuf += 1;
   return p;
 }
 
@@ -1242,6 +1444,30 @@ static cudaError_t phase1_mh(const FourierPlan& p, const FourierWork& w, const d
 }
 
 // phase 2: carried-in states (optionally entering the range with tin), the sweep
+// The remainder sweep runs on a side stream beside the main sweep (it is a
+// handful of latency-bound warps: alone after the main sweep it cost the whole
+// of its serial walk; beside it, it fills the SMs the main sweep leaves idle).
+// One high-priority stream and a fork / join event pair per device, created on
+// first use (before any graph capture: the evaluators warm up first).
+struct RemSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static RemSide& rem_side() {
+  static RemSide sides[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  RemSide& r = sides[dev & 63];
+  if (!r.s) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&r.s, cudaStreamNonBlocking, greatest);
+    cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+  }
+  return r;
+}
+
 template <int MH>
 static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
                              const double* ys, const double* zs, const double* qs,
@@ -1264,14 +1490,36 @@ static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const d
         w.carry, p.nch, p.c0, p.c1, p.P, p.items, MH, nseg, w.modetab, w.dchunk,
         w.dchunk + (size_t)p.nch * MH, w.zbound, segmap);
   }
-  if (p.swap)
-    fourier_sweep_kernel<MH, true><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
-        xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
-        w.fpart, want_forces, p.c0);
-  else
-    fourier_sweep_kernel<MH, false><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
-        xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items, p.ipg, b, w.carry, w.epart,
-        w.fpart, want_forces, p.c0);
+  if (p.rem) {  // the remainder sweep, forked beside the main one
+    RemSide& rs = rem_side();
+    cudaEventRecord(rs.fork, st);
+    cudaStreamWaitEvent(rs.s, rs.fork, 0);
+    const int rwarps = (nch_r + p.rem_g - 1) / p.rem_g;
+    const int rblocks = (rwarps + kRemWarps - 1) / kRemWarps;
+    double* frem = w.fpart + (size_t)p.rem_buf * p.n * 3;
+    if (p.swap)
+      fourier_sweep_rem_kernel<MH, true><<<rblocks, 32 * kRemWarps, 0, rs.s>>>(
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.rem, p.rem_g, b,
+          w.carry, w.epart, frem, want_forces, p.c0, p.c1);
+    else
+      fourier_sweep_rem_kernel<MH, false><<<rblocks, 32 * kRemWarps, 0, rs.s>>>(
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.rem, p.rem_g, b,
+          w.carry, w.epart, frem, want_forces, p.c0, p.c1);
+    cudaEventRecord(rs.join, rs.s);
+  }
+  if (p.items_main > 0) {
+    if (p.swap)
+      fourier_sweep_kernel<MH, true><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.ipg, b, w.carry,
+          w.epart, w.fpart, want_forces, p.c0);
+    else
+      fourier_sweep_kernel<MH, false><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.ipg, b, w.carry,
+          w.epart, w.fpart, want_forces, p.c0);
+  }
+  if (p.rem) {
+    cudaStreamWaitEvent(st, rem_side().join, 0);
+  }
   return cudaGetLastError();
 }
 
@@ -1347,10 +1595,10 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
     if (e1 > e0) {
       if ((e1 - e0) < (int64_t)148 * 2048 && p.nbuf >= 16)
         fourier_force_reduce_kernel<8><<<(unsigned)((8 * (e1 - e0) + 255) / 256), 256, 0, st>>>(
-            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
+            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items_main, n3, forces_sorted, e0, e1);
       else
         fourier_force_reduce_kernel<1><<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
-            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items, n3, forces_sorted, e0, e1);
+            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items_main, n3, forces_sorted, e0, e1);
     }
   }
   return cudaGetLastError();

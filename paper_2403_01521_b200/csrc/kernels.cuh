@@ -57,6 +57,10 @@ struct FourierPlan {
   size_t smem_sweep;
   int swap;       // 1: real inputs swapped (u_r, u_i) -> (u_i, -u_r), i.e. the pass's result
                   // times -i (lone complex SOE terms, capi.cu prepare_soe)
+  int items_main; // items of the main sweep (whole warps when rem > 0)
+  int rem;        // leftover items per chunk run by the remainder sweep (0: none)
+  int rem_g;      // chunks per remainder warp (32 / rem)
+  int rem_buf;    // the remainder's partial force buffer
 };
 FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2, int ranks = 1);
 // bytes of device workspace the plan needs (carry, chunk decays, mode table, partials)
