@@ -990,8 +990,11 @@ __global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourie
 // (each particle has one remainder group): deterministic.
 constexpr int kRemWarps = 4;
 constexpr int kRemSB = 4;  // steps per force flush
+#ifndef SLAB_REM_MINB
+#define SLAB_REM_MINB 1
+#endif
 template <int MH, bool kSwap>
-__global__ void __launch_bounds__(32 * kRemWarps) fourier_sweep_rem_kernel(
+__global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_rem_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
     const double* __restrict__ modetab, int P, int item0, int L, int G, BVec b,

@@ -268,11 +268,23 @@ def test_sampler_statistics(pk):
     exp = np.append(expected[keep], n_draw - expected[keep].sum())
     _, p = chisquare(obs, exp * obs.sum() / exp.sum())
     assert p > 1e-3
-    # the reference chain's own draws follow the same law (different RNG stream)
+    # the reference chain's own draws (different RNG stream, same law): a
+    # two-sample chi-square test on the joint (mx, my) histogram -- pooled bins
+    # with >= 10 expected draws per sample, the rest merged into one bin -- and
+    # the same acceptance rate
+    from scipy.stats import chi2_contingency
     g = load_golden("units")
     ref = g["sampler_idx_a03_L100_seed11"]
-    for arr in (rec, ref):
-        assert abs(np.mean(np.abs(arr[:, 0])) - np.mean(np.abs(ref[:, 0]))) < 0.25
+    keys = lambda a: (a[:, 0].astype(np.int64) + 1000) * 4000 + (a[:, 1].astype(np.int64) + 1000)
+    ka, kb = keys(rec), keys(ref)
+    cells, pooled = np.unique(np.concatenate([ka, kb]), return_counts=True)
+    big = cells[pooled >= 20]
+    ca = np.array([np.sum(ka == c) for c in big] + [np.sum(~np.isin(ka, big))])
+    cb = np.array([np.sum(kb == c) for c in big] + [np.sum(~np.isin(kb, big))])
+    _, p2, _, _ = chi2_contingency(np.vstack([ca, cb]))
+    assert p2 > 1e-3, p2
+    assert len(big) > 50
+    assert abs(smp.acceptance_rate - float(g["sampler_acc_a03_L100_seed11"])) < 0.02
 
 
 def test_sampler_determinism_and_scaling(pk):
