@@ -136,6 +136,10 @@ size_t tile_work_bytes(int64_t n, int ncx, int ncy, int ncz);
 int tile_grid(int64_t nhomes);
 cudaError_t tile_homes(const int32_t* start, const uint32_t* skey, int64_t n, int ncx, int ncy,
                        int ncz, void* work, int32_t** hperm_out, cudaStream_t st);
+cudaError_t nbr_tile(const float4* cpf, const int32_t* start, const int32_t* hperm, int64_t h0,
+                     int64_t h1, int ncx, int ncy, int ncz, double lx, double ly, double lz,
+                     float rc2f, int kcap, int32_t* nbr, int32_t* nn, int* maxnn, int* status,
+                     cudaStream_t st);
 cudaError_t tile_pairs(const double4* cp, const float4* cpf, const int32_t* start,
                        const int32_t* hperm, const int32_t* order, int64_t h0, int64_t h1,
                        int ncx, int ncy, int ncz, double lx, double ly, double lz, double alpha,

@@ -811,6 +811,10 @@ constexpr int kShortSpan = SLAB_SHORT_SPAN_DEFAULT;
 #define SLAB_TILE_MIN_N 40000
 #endif
 constexpr int64_t kTileMinN = SLAB_TILE_MIN_N;
+#ifndef SLAB_NBR_TILE
+#define SLAB_NBR_TILE 0  // cfg4: warp-window screen 1.46 ms (2.7x the candidates) vs nbr_build 1.10 ms
+#endif
+constexpr bool kNbrTile = SLAB_NBR_TILE;
 #ifndef SLAB_TILE_DEFAULT
 #define SLAB_TILE_DEFAULT 0  // cfg4: tile 4.5 ms vs neighbour rows 3.2 ms (DESIGN 4.3)
 #endif
@@ -885,9 +889,8 @@ size_t short_work_bytes(const ShortPlan& p) {
     b += align256(sizeof(int32_t) * radix_hist_entries(p.n));
     b += align256(sizeof(int32_t) * (p.ncell + 1));
     b += align256(sizeof(double4) * n) + align256(sizeof(float4) * n);
-    if (p.tile)
-      b += tile_work_bytes(p.n, p.ncx, p.ncy, p.ncz);
-    else
+    b += tile_work_bytes(p.n, p.ncx, p.ncy, p.ncz);  // home order (tile kernels)
+    if (!p.tile)
       b += align256(sizeof(int32_t) * n * (size_t)p.kcap) + align256(sizeof(int32_t) * n);
     b += align256(sizeof(int));
   }
@@ -959,10 +962,12 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
                                                                              start);
     cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, lx,
                                                                     ly, cp, cpf);
+    void* twork = w;  // home-order work (tile_work_bytes)
+    w += tile_work_bytes(p.n, p.ncx, p.ncy, p.ncz);
     if (p.tile) {  // fused screen + pair kernel: no neighbour rows
       if (accumulate) return cudaErrorInvalidValue;  // Coulomb callers overwrite
       int32_t* hperm = nullptr;
-      e = tile_homes(start, skey, n, p.ncx, p.ncy, p.ncz, w, &hperm, st);
+      e = tile_homes(start, skey, n, p.ncx, p.ncy, p.ncz, twork, &hperm, st);
       if (e != cudaSuccess) return e;
       const int grid = tile_grid(nh) < p.nblk ? tile_grid(nh) : (int)p.nblk;
       e = tile_pairs(cp, cpf, start, hperm, order, h0, h1, p.ncx, p.ncy, p.ncz, lx, ly, lz,
@@ -981,7 +986,19 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     const int64_t nblk = (nh + kSRThreads - 1) / kSRThreads;
     const int64_t cblk = (p.ncell + kSRThreads / 32 - 1) / (kSRThreads / 32);
     const bool cells = nh <= kNbrCellsMaxHomes;
-    if (cells && p.span == 3)
+    // the warp-cooperative screen (short_tile.cu) for large full home ranges; its
+    // rows follow the cell order like nbr_build's (a shard's home range is a
+    // cell-order range, which the brick home order does not tile)
+    const bool tile_screen = kNbrTile && !cells && h0 == 0 && h1 == n && p.span >= 2 &&
+                             p.ncx >= 2 * p.span + 6 && p.ncy >= 2 * p.span + 6;
+    if (tile_screen) {
+      int32_t* hperm = nullptr;
+      e = tile_homes(start, skey, n, p.ncx, p.ncy, p.ncz, twork, &hperm, st);
+      if (e != cudaSuccess) return e;
+      e = nbr_tile(cpf, start, hperm, 0, n, p.ncx, p.ncy, p.ncz, lx, ly, lz, rc2f, p.kcap, nbr, nn,
+                   maxnn, status, st);
+      if (e != cudaSuccess) return e;
+    } else if (cells && p.span == 3)
       nbr_cells_kernel<3><<<(unsigned)cblk, kSRThreads, 0, st>>>(
           cpf, start, p.ncell, h0, h1, p.ncx, p.ncy, p.ncz, (float)lx, (float)ly, (float)lz,
           rc2f, p.kcap, nbr, nn, maxnn, status);

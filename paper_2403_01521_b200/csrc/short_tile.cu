@@ -517,6 +517,202 @@ __global__ void __launch_bounds__(kTileThreads) short_tile_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// the same warp-cooperative screen, writing neighbour rows for pair_list_kernel
+// ---------------------------------------------------------------------------
+// Replaces nbr_build_kernel's per-lane candidate streams (each lane loading its
+// own candidates: L1-throughput bound, lanes idling on uneven column lengths)
+// with the tile kernel's screen: a warp's 32 homes (a compact brick of the home
+// order) test every candidate of their r_c window, staged 32 at a time in shared
+// memory and compared two at a time in paired fp32; each lane appends its hits to
+// its home's row (cell-sorted index a -> row a, as nbr_build writes them).  A row
+// that would exceed kcap is marked nn = -1 (overflow_pairs_kernel evaluates it).
+constexpr int kNbrTileWarps = 4;
+__global__ void __launch_bounds__(32 * kNbrTileWarps) nbr_tile_kernel(
+    const float4* __restrict__ cpf, const int32_t* __restrict__ start,
+    const int32_t* __restrict__ hperm, int64_t h0, int64_t h1, int ncx, int ncy, int ncz,
+    float lxf, float lyf, float lzf, float rc2f, float rcf, int kcap,
+    int32_t* __restrict__ nbr, int32_t* __restrict__ nn, int* __restrict__ maxnn,
+    int* __restrict__ status) {
+  __shared__ float s_nx[kNbrTileWarps][32], s_ny[kNbrTileWarps][32], s_nz[kNbrTileWarps][32];
+  __shared__ int32_t s_j[kNbrTileWarps][32];
+  // per-lane ring of pending row entries (slot-major: conflict-free), written to
+  // the row as whole 32-byte sectors, as nbr_build does
+  constexpr int kTRing = 16;
+  __shared__ int32_t s_ring[kNbrTileWarps][kTRing][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const float ex = lxf / ncx, ey = lyf / ncy, izc = ncz / lzf;
+  const float ilxf = 1.0f / lxf, ilyf = 1.0f / lyf;
+  float* snx = s_nx[warp];
+  float* sny = s_ny[warp];
+  float* snz = s_nz[warp];
+  int32_t* sj = s_j[warp];
+  const int64_t ngroups = (h1 - h0 + 31) / 32;
+  for (int64_t grp = blockIdx.x * (int64_t)kNbrTileWarps + warp; grp < ngroups;
+       grp += (int64_t)gridDim.x * kNbrTileWarps) {
+    const int64_t hidx = h0 + grp * 32 + lane;
+    const bool hact = hidx < h1;
+    const int a = hact ? hperm[hidx] : -1;
+    const float4 pf = hact ? cpf[a] : make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t* row = nbr + (hact ? (int64_t)a : 0) * kcap;  // rows indexed by cell order
+    int cnt = 0, done = 0;  // hits found / hits already written to the row
+    int32_t* ring = &s_ring[warp][0][lane];
+    auto flush8 = [&]() {
+      if (done + 8 <= kcap) {
+        const int s0 = done & (kTRing - 1);
+        const int4 v0 = make_int4(ring[(s0 + 0) * 32], ring[(s0 + 1) * 32], ring[(s0 + 2) * 32],
+                                  ring[(s0 + 3) * 32]);
+        const int4 v1 = make_int4(ring[(s0 + 4) * 32], ring[(s0 + 5) * 32], ring[(s0 + 6) * 32],
+                                  ring[(s0 + 7) * 32]);
+        int4* dst = reinterpret_cast<int4*>(row + done);
+        dst[0] = v0;
+        dst[1] = v1;
+      }
+      done += 8;
+    };
+    float x0 = hact ? pf.x : 3e30f, x1 = hact ? pf.x : -3e30f;
+    float y0 = hact ? pf.y : 3e30f, y1 = hact ? pf.y : -3e30f;
+    float z0 = hact ? pf.z : 3e30f, z1 = hact ? pf.z : -3e30f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      x0 = fminf(x0, __shfl_xor_sync(full, x0, o));
+      x1 = fmaxf(x1, __shfl_xor_sync(full, x1, o));
+      y0 = fminf(y0, __shfl_xor_sync(full, y0, o));
+      y1 = fmaxf(y1, __shfl_xor_sync(full, y1, o));
+      z0 = fminf(z0, __shfl_xor_sync(full, z0, o));
+      z1 = fmaxf(z1, __shfl_xor_sync(full, z1, o));
+    }
+    const int ix0 = (int)floorf((x0 - rcf) / ex), ix1 = (int)floorf((x1 + rcf) / ex);
+    const int iy0 = (int)floorf((y0 - rcf) / ey), iy1 = (int)floorf((y1 + rcf) / ey);
+    const bool wrap_x = ix1 - ix0 + 1 > ncx, wrap_y = iy1 - iy0 + 1 > ncy;
+    const bool minimg = wrap_x || wrap_y;
+    const int nX = wrap_x ? ncx : ix1 - ix0 + 1;
+    const int nY = wrap_y ? ncy : iy1 - iy0 + 1;
+    const int ncol = nX * nY;
+#pragma unroll 1
+    for (int q0 = 0; q0 < ncol; q0 += 32) {
+      const int qc = q0 + lane;
+      int j0 = 0, len = 0;
+      float shx = 0.f, shy = 0.f;
+      if (qc < ncol) {
+        const int ux = ix0 + qc / nY, uy = iy0 + qc % nY;
+        const int mx = ux >= 0 ? ux / ncx : -((-ux + ncx - 1) / ncx);
+        const int my = uy >= 0 ? uy / ncy : -((-uy + ncy - 1) / ncy);
+        const int wx = ux - mx * ncx, wy = uy - my * ncy;
+        shx = (float)mx * lxf;
+        shy = (float)my * lyf;
+        const float dxr = wrap_x ? 0.0f : fmaxf(0.0f, fmaxf(ux * ex - x1, x0 - (ux + 1) * ex));
+        const float dyr = wrap_y ? 0.0f : fmaxf(0.0f, fmaxf(uy * ey - y1, y0 - (uy + 1) * ey));
+        const float dxy2 = fmaf(dxr, dxr, dyr * dyr);
+        if (dxy2 <= rc2f) {
+          const float h = sqrtf(rc2f - dxy2);
+          int zlo = (int)floorf((z0 - h) * izc - 1e-3f);
+          int zhi = (int)floorf((z1 + h) * izc + 1e-3f);
+          zlo = zlo < 0 ? 0 : (zlo >= ncz ? ncz - 1 : zlo);
+          zhi = zhi < 0 ? 0 : (zhi >= ncz ? ncz - 1 : zhi);
+          const int64_t col = ((int64_t)wx * ncy + wy) * ncz;
+          j0 = start[col + zlo];
+          len = start[col + zhi + 1] - j0;
+        }
+      }
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(full, incl, 31);
+      const int excl = incl - len;
+#pragma unroll 1
+      for (int fb = 0; fb < total; fb += 32) {
+        const int f = fb + lane;
+        int k = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int v = __shfl_sync(full, incl, k + step - 1);
+          if (v <= f) k += step;
+        }
+        const int jk = __shfl_sync(full, j0, k & 31);
+        const int ek = __shfl_sync(full, excl, k & 31);
+        const float sx = __shfl_sync(full, shx, k & 31);
+        const float sy = __shfl_sync(full, shy, k & 31);
+        const bool valid = f < total;
+        const int j = jk + (f - ek);
+        const float4 cfj = valid ? cpf[j] : make_float4(3e30f, 3e30f, 3e30f, 0.f);
+        snx[lane] = -(cfj.x + sx);
+        sny[lane] = -(cfj.y + sy);
+        snz[lane] = -cfj.z;
+        sj[lane] = valid ? j : -2;
+        __syncwarp();
+        unsigned hits = 0u;
+        if (!minimg) {
+          const float2 px = make_float2(pf.x, pf.x), py = make_float2(pf.y, pf.y);
+          const float2 pz = make_float2(pf.z, pf.z), nrc = make_float2(-rc2f, -rc2f);
+#pragma unroll
+          for (int t = 0; t < 32; t += 2) {
+            const float2 dx = __fadd2_rn(px, *reinterpret_cast<const float2*>(snx + t));
+            const float2 dy = __fadd2_rn(py, *reinterpret_cast<const float2*>(sny + t));
+            const float2 dz = __fadd2_rn(pz, *reinterpret_cast<const float2*>(snz + t));
+            float2 d = __ffma2_rn(dz, dz, nrc);
+            d = __ffma2_rn(dy, dy, d);
+            d = __ffma2_rn(dx, dx, d);
+            hits = __funnelshift_l(__float_as_uint(d.x), hits, 1);
+            hits = __funnelshift_l(__float_as_uint(d.y), hits, 1);
+          }
+          hits = __brev(hits);
+        } else {
+#pragma unroll 4
+          for (int t = 0; t < 32; ++t) {
+            float dx = pf.x + snx[t], dy = pf.y + sny[t];
+            const float dz = pf.z + snz[t];
+            dx = fmaf(-lxf, rintf(dx * ilxf), dx);
+            dy = fmaf(-lyf, rintf(dy * ilyf), dy);
+            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (d2 <= rc2f && sj[t] >= 0) hits |= 1u << t;
+          }
+        }
+        if (!hact) hits = 0u;
+        // append the hits (the home itself is screened in: skip it by index)
+        while (hits) {
+          const int t = __ffs(hits) - 1;
+          hits &= hits - 1u;
+          const int jj = sj[t];
+          if (jj != a) {
+            ring[(cnt & (kTRing - 1)) * 32] = jj;
+            ++cnt;
+            if (cnt - done >= 8) flush8();
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (hact && cnt <= kcap)
+      for (int e = done; e < cnt; ++e) row[e] = ring[(e & (kTRing - 1)) * 32];
+    if (hact) {
+      nn[a] = cnt <= kcap ? cnt : -1;  // -1: overflowed, evaluated by overflow_pairs_kernel
+      if (cnt > kcap) {
+        atomicOr(status, SLAB_STATUS_NBR_OVERFLOW_DEV);
+        atomicMax(maxnn, cnt);
+      }
+    }
+  }
+}
+
+cudaError_t nbr_tile(const float4* cpf, const int32_t* start, const int32_t* hperm, int64_t h0,
+                     int64_t h1, int ncx, int ncy, int ncz, double lx, double ly, double lz,
+                     float rc2f, int kcap, int32_t* nbr, int32_t* nn, int* maxnn, int* status,
+                     cudaStream_t st) {
+  const int64_t groups = (h1 - h0 + 31) / 32;
+  int64_t ctas = (groups + kNbrTileWarps - 1) / kNbrTileWarps;
+  const int64_t cap = 148 * 12;
+  ctas = ctas < cap ? (ctas > 0 ? ctas : 1) : cap;
+  nbr_tile_kernel<<<(unsigned)ctas, 32 * kNbrTileWarps, 0, st>>>(
+      cpf, start, hperm, h0, h1, ncx, ncy, ncz, (float)lx, (float)ly, (float)lz, rc2f,
+      sqrtf(rc2f), kcap, nbr, nn, maxnn, status);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 int64_t tile_home_slots(int ncx, int ncy, int ncz) {
