@@ -60,6 +60,15 @@ constexpr int kSB = SLAB_SWEEP_SB;
 #endif
 // sweep CTA size cap: 2 CTAs/SM at 65536 / (2 * cap) registers per thread
 constexpr int kSweepMaxThreads = SLAB_SWEEP_MAXT;  // force staging batch (particles)
+#ifndef SLAB_SWEEP_MAXT_2CTA
+#define SLAB_SWEEP_MAXT_2CTA 192
+#endif
+// CTA size cap of the two-CTAs-per-SM sweep: 192 threads (6 warps) lets the
+// allocator use 168 registers (2 x 6 warps x 32 x 168 <= 64K; 3 warps per SM
+// sub-partition) instead of 128 -- no spills, cfg4 sweep 3.77 -> 3.57 ms.  With
+// the remainder sweep a P = 100 chunk's main items are exactly 192.  The
+// one-CTA form (12 pairs) keeps 256-thread groups (cfg3: 192 -> 3 groups per
+// chunk restaging the chunk, 2.20 -> 2.79 ms).
 constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
 // CTAs per SM the sweep is compiled for: 2 (128 registers) up to SLAB_SWEEP_BIG_MH
 // pairs; 1 above it, where 128 registers spill hundreds of bytes per lane
@@ -67,6 +76,9 @@ constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
 #define SLAB_SWEEP_BIG_MH 10  // cfg3 (M = 24, 12 pairs): sweep 1.90 -> 1.31 ms; 8 pairs stay at 2 CTAs (4.14 vs 4.86 ms)
 #endif
 __host__ __device__ constexpr int sweep_min_blocks(int mh) { return mh >= SLAB_SWEEP_BIG_MH ? 1 : 2; }
+__host__ __device__ constexpr int sweep_max_threads(int mh) {
+  return mh >= SLAB_SWEEP_BIG_MH ? SLAB_SWEEP_MAXT : SLAB_SWEEP_MAXT_2CTA;
+}
 constexpr int kMaxR = 256;
 constexpr size_t kSmemPerSM = 227 * 1024;  // usable shared memory per SM (B200)
 constexpr int kAggRegs = 72;               // fourier_aggregate_mma_kernel (ptxas)
@@ -754,7 +766,7 @@ static int carry_groups(int nch, int items, int mh) {
 // (forward and backward lanes to separate buffers), reduced in fixed order
 // afterwards: deterministic, no atomics.
 template <int MH, bool kSwap>
-__global__ void __launch_bounds__(kSweepMaxThreads, sweep_min_blocks(MH)) fourier_sweep_kernel(
+__global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
     const double* __restrict__ modetab, int P, int items, int ipg, BVec b,
@@ -1270,7 +1282,8 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   }
   p.items_main = p.items - p.rem;
   const int nitems = p.items_main;
-  p.ngroups = (nitems + kSweepMaxThreads - 1) / kSweepMaxThreads;
+  const int maxt = sweep_max_threads(mh);
+  p.ngroups = (nitems + maxt - 1) / maxt;
   if (p.ngroups < 1) p.ngroups = 1;
   p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
   if (p.rem) p.ipg = (p.ipg + 31) / 32 * 32;  // groups of whole warps
@@ -1296,7 +1309,7 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
       const int by_regs = 65536 / (regs * threads);
       return by_smem < by_regs ? (by_smem < 32 ? by_smem : 32) : (by_regs < 32 ? by_regs : 32);
     };
-    const int sw_regs = sweep_min_blocks(mh) == 1 ? 255 : 128;
+    const int sw_regs = sweep_min_blocks(mh) == 1 ? 255 : 65536 / (2 * maxt) / 8 * 8;
     const int sw_full = 65536 / (sw_regs * 32 * p.warps) > 0 ? 65536 / (sw_regs * 32 * p.warps) : 1;
     const int ag_full = 65536 / (kAggRegs * 32 * tpc);
     // ... but not below 64 particles: shorter chunks multiply the chunk count and
