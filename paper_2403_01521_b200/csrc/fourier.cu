@@ -34,9 +34,6 @@
 
 namespace slab {
 
-#ifndef SLAB_SWEEP_SB
-#define SLAB_SWEEP_SB 4
-#endif
 #ifndef SLAB_SWEEP_CB
 #define SLAB_SWEEP_CB 0
 #endif
@@ -57,7 +54,6 @@ constexpr int kSweepRemMax = SLAB_SWEEP_REM_MAX;
 #ifndef SLAB_SWEEP_PIPE
 #define SLAB_SWEEP_PIPE 1  // next particle's sincos/exp one iteration ahead: 3.57 -> 3.52 ms at 168 registers (2.5% slower at 128)
 #endif
-constexpr int kSB = SLAB_SWEEP_SB;
 #ifndef SLAB_SWEEP_MAXT
 #define SLAB_SWEEP_MAXT 256
 #endif
@@ -72,7 +68,11 @@ constexpr int kSweepMaxThreads = SLAB_SWEEP_MAXT;  // force staging batch (parti
 // the remainder sweep a P = 100 chunk's main items are exactly 192.  The
 // one-CTA form (12 pairs) keeps 256-thread groups (cfg3: 192 -> 3 groups per
 // chunk restaging the chunk, 2.20 -> 2.79 ms).
-constexpr int kStageStride = 33;  // padded row (32 lanes + 1)
+// force staging rows: 32 lanes, the backward half-warp shifted one column so
+// that the row-summing lanes (8 rows x 2 halves per 16-lane phase) hit distinct
+// banks; two buffers per warp (one batch staged while the previous one is summed)
+constexpr int kStageStride = 34;
+constexpr int kStageBuf = 3 * 4 * kStageStride;  // 4 particles x 3 components
 // CTAs per SM the sweep is compiled for: 2 (128 registers) up to SLAB_SWEEP_BIG_MH
 // pairs; 1 above it, where 128 registers spill hundreds of bytes per lane
 #ifndef SLAB_SWEEP_BIG_MH
@@ -764,15 +764,22 @@ static int carry_groups(int nch, int items, int mh) {
 // and the real input enters as H += C_l u.  C_l lives in shared memory
 // (per-lane column), which keeps the kernel at <= 128 registers: 2 CTAs / 16
 // warps per SM to hide the fp64 dependency latency.
-// Forces: per batch of kSB particles, lanes stage (Fx, Fy, Fz) transposed in
-// smem and 3*kSB lanes row-sum them; each warp writes its own partial buffer
-// (forward and backward lanes to separate buffers), reduced in fixed order
-// afterwards: deterministic, no atomics.
+// Lanes (force plans, `paired`): a warp holds 16 modes, forward in lanes 0-15
+// and backward in 16-31, so every warp has the same shape.  Energy-only plans
+// (forward items only) keep consecutive items per lane.
+// Forces: lanes stage (Fx, Fy, Fz) of each particle transposed in shared memory
+// (one row per component, one column per lane); a batch of 4 particles is 12
+// rows, and while the next batch is computed 24 lanes sum the previous batch's
+// rows, one (row, half-warp) each and 4 columns per particle step, so the
+// transposed reduction is spread through the recurrence instead of stalling the
+// warp every 4 particles (measured: the batched flush cost 12% of the sweep).
+// Each warp writes its forward and backward sums to two partial buffers of its
+// own, reduced in fixed order afterwards: deterministic, no atomics.
 template <int MH, bool kSwap>
 __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) fourier_sweep_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
-    const double* __restrict__ modetab, int P, int items, int ipg, BVec b,
+    const double* __restrict__ modetab, int P, int units, int upg, int paired, BVec b,
     const double2* __restrict__ carry, double* __restrict__ epart, double* __restrict__ fpart,
     int want_forces, int c0) {
   extern __shared__ double4 smem4[];
@@ -783,7 +790,7 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
   double* sy = sx + R;
   double* sq = sy + R;
   double* sz = sq + R;                                     // R + 2 (halo below / above)
-  double* stage = sz + R + 2;                              // nwarps * kSB*3 * 33
+  double* stage = sz + R + 2;                              // nwarps * 2 * kStageBuf
 #if SLAB_SWEEP_CB == 2
   // transcendental coefficients, broadcast from shared memory (one LDS.128 per
   // two constants instead of two UMOVs per constant)
@@ -807,16 +814,26 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
     sz[0] = zs[a0 > 0 ? a0 - 1 : 0];
     sz[len + 1] = zs[a1 < n ? a1 : a1 - 1];
   }
+  for (int e = threadIdx.x; e < nwarps * 2 * kStageBuf; e += blockDim.x) stage[e] = 0.0;
 #if !SLAB_SWEEP_GDECAY
   for (int e = threadIdx.x; e < (len + 1) * MH; e += blockDim.x) sd[e] = dtab[a0 * MH + e];
 #endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nitems = 2 * P;
-  const int item = g * ipg + threadIdx.x;
-  const int gend = min(items, (g + 1) * ipg);
-  const bool active = item < gend;
-  const bool fwd = item < P;
+  const int gend = min(units, (g + 1) * upg);  // units: modes (paired) or items
+  int item;
+  bool active, fwd;
+  if (paired) {
+    const int tm = g * upg + 16 * warp + (lane & 15);
+    fwd = lane < 16;
+    active = tm < gend;
+    item = fwd ? tm : P + tm;
+  } else {
+    item = g * upg + threadIdx.x;
+    active = item < gend;
+    fwd = item < P;
+  }
   const int t = active ? (fwd ? item : item - P) : 0;
   const unsigned fmask = __ballot_sync(0xffffffffu, active && fwd);
   const unsigned bmask = __ballot_sync(0xffffffffu, active && !fwd);
@@ -854,13 +871,22 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
   __syncthreads();
   if ((fmask | bmask) == 0u) return;  // no items in this warp (its buffer is skipped)
 
-  // partial force buffers: one per (group, warp); the single warp that holds
-  // both directions sends its backward lanes to the extra buffer G*W
+  // partial force buffers: two per (group, warp), forward and backward half
   const int gw = g * nwarps + warp;
-  double* fbuf_f = fpart + (size_t)gw * n * 3;
-  double* fbuf_b = fpart + (size_t)(fmask ? gridDim.y * nwarps : gw) * n * 3;
   const double2* sCl = sC + threadIdx.x;
-  double* st = stage + warp * kSB * 3 * kStageStride;
+  double* st = stage + warp * 2 * kStageBuf;
+  const int scol = lane + (lane >> 4);  // staging column of this lane
+  // the summing role of this lane: row r (slot r / 3, component r % 3) of half h
+  const int rr = lane < 16 ? (lane & 7) : 8 + (lane & 3);
+  const int rh = lane < 16 ? (lane >> 3) : ((lane - 16) >> 2) & 1;
+  const bool rsum = lane < 24;
+  const int rslot = rr / 3;
+  const int roff = rr * kStageStride + 17 * rh;
+  // destination of the row sum for chunk particle p: forward p, backward len-1-p
+  double* const rdst = fpart + (size_t)(2 * gw + rh) * n * 3 +
+                       (rh ? (a0 + len - 1) * 3 : a0 * 3) + (rr - 3 * rslot);
+  const int rstep = rh ? -3 : 3;
+  double facc = 0.0;
   double E = 0.0;
   // Software pipeline: the k-dependent transcendentals of the NEXT particle
   // (sincos of theta, e^{-k dz}) are issued in the same basic block as this
@@ -930,47 +956,24 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
       const double ztr = fma(2.0, sbr, -kappa * gk.re);
       const double zti = fma(2.0, sbi, -kappa * gk.im);
       const double fxy = fxy_c * q * ei;
-      const int slot = i % kSB;
-      st[(slot * 3 + 0) * kStageStride + lane] = fxy * kx;
-      st[(slot * 3 + 1) * kStageStride + lane] = fxy * ky;
-      st[(slot * 3 + 2) * kStageStride + lane] = fz_c * q * fma(cs, ztr, -ps * zti);
-      if (slot == kSB - 1 || i == len - 1) {
-        __syncwarp();
-        const int nslot = slot + 1, ibase = i - slot;
-        const int nrow = 3 * nslot;
-        // two lanes per (particle, component) row, 16 columns each, then one shuffle
-        const int r = lane % (3 * kSB), half = lane / (3 * kSB);
-        double sf = 0.0, sb = 0.0;
-        if (r < nrow && half < 2) {
-          const double* row = st + r * kStageStride + 16 * half;
-          if (bmask == 0u || fmask == 0u) {  // single-direction warp (all but one)
-            double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-            for (int j = 0; j < 16; j += 2) {
-              acc0 += row[j];
-              acc1 += row[j + 1];
-            }
-            (bmask == 0u ? sf : sb) = acc0 + acc1;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const double v = row[j];
-              const int col = 16 * half + j;
-              if ((fmask >> col) & 1u) sf += v;
-              if ((bmask >> col) & 1u) sb += v;
-            }
-          }
+      const int slot = i & 3;
+      double* cur = st + ((i >> 2) & 1) * kStageBuf;
+      const double* prv = st + (((i >> 2) & 1) ^ 1) * kStageBuf + roff + 4 * slot;
+      __syncwarp();  // orders the previous batch's rows before their sums (and
+                     // those sums' reads before this buffer's reuse)
+      facc += prv[0];
+      facc += prv[1];
+      facc += prv[2];
+      facc += prv[3];
+      cur[(slot * 3 + 0) * kStageStride + scol] = fxy * kx;
+      cur[(slot * 3 + 1) * kStageStride + scol] = fxy * ky;
+      cur[(slot * 3 + 2) * kStageStride + scol] = fz_c * q * fma(cs, ztr, -ps * zti);
+      if (slot == 3) {  // the previous batch (particles i - 7 .. i - 4) is summed
+        if (rsum && i >= 7) {
+          SLAB_BOUND(a0 + i - 7 + rslot, n);
+          rdst[rstep * (i - 7 + rslot)] = facc;
         }
-        sf += __shfl_down_sync(0xffffffffu, sf, 3 * kSB);
-        sb += __shfl_down_sync(0xffffffffu, sb, 3 * kSB);
-        if (lane < nrow) {
-          const int sl = lane / 3, comp = lane - 3 * sl;
-          SLAB_BOUND(a0 + ibase + sl, n);
-          SLAB_BOUND(a0 + len - 1 - (ibase + sl), n);
-          if (fmask) fbuf_f[(a0 + ibase + sl) * 3 + comp] = sf;
-          if (bmask) fbuf_b[(a0 + len - 1 - (ibase + sl)) * 3 + comp] = sb;
-        }
-        __syncwarp();
+        facc = 0.0;
       }
     }
     // T_a = S_a + u_a: real input scaled by C_l into the scaled state
@@ -997,6 +1000,25 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
     q = q_n;
 #endif
   }
+  if (want_forces && len > 0) {
+    // the batch before the last one (unless the last, full batch summed it) and
+    // the last batch (ns particles) -- columns in the same order as in the loop
+    const int bl = (len - 1) >> 2, ns = len - 4 * bl;
+    if (ns < 4 && bl >= 1) {
+      const double* prv = st + ((bl & 1) ^ 1) * kStageBuf + roff;
+      for (int j = 4 * ns; j < 16; ++j) facc += prv[j];
+      if (rsum) rdst[rstep * (4 * (bl - 1) + rslot)] = facc;
+    }
+    __syncwarp();
+    const double* lst = st + (bl & 1) * kStageBuf + roff;
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a += lst[j];
+    if (rsum && rslot < ns) {
+      SLAB_BOUND(a0 + 4 * bl + rslot, n);
+      rdst[rstep * (4 * bl + rslot)] = a;
+    }
+  }
   if (active && fwd) epart[(size_t)c * P + t] = E;
 }
 
@@ -1012,8 +1034,9 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
 // shared memory: particle data and decay rows come straight from global memory
 // (read once per group; small next to the main sweep).  Same recurrence and
 // epilogue as fourier_sweep_kernel; a group's force contributions are summed
-// in fixed order over its L lanes into the remainder's own partial buffer
-// (each particle has one remainder group): deterministic.
+// in fixed order over its lanes of each direction into the remainder's own
+// forward / backward partial buffers (each particle has one remainder group):
+// deterministic.
 constexpr int kRemWarps = 4;
 constexpr int kRemSB = 4;  // steps per force flush
 #ifndef SLAB_REM_MINB
@@ -1023,7 +1046,7 @@ template <int MH, bool kSwap>
 __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_rem_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
-    const double* __restrict__ modetab, int P, int item0, int L, int G, BVec b,
+    const double* __restrict__ modetab, int P, int unit0, int L, int paired, int G, BVec b,
     const double2* __restrict__ carry, double* __restrict__ epart, double* __restrict__ frem,
     int want_forces, int c0, int c1) {
   __shared__ double stg[kRemWarps][kRemSB * 32 * 3];
@@ -1032,7 +1055,11 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
   const int grp = lane / L;
   const int c = c0 + wg * G + grp;
   const bool active = lane < G * L && c < c1;
-  const int item = item0 + (lane % L);
+  // paired: the group's first L/2 lanes are modes unit0.. forward, the rest
+  // the same modes backward; otherwise L consecutive (forward) items
+  const int Ld = paired ? L / 2 : L;
+  const int jl = lane % L;
+  const int item = jl < Ld ? unit0 + jl : P + unit0 + (jl - Ld);
   const bool fwd = item < P;
   const int t = fwd ? item : item - P;
   const int nitems = 2 * P;
@@ -1135,10 +1162,14 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
       row[lane * 3 + 2] = live ? fz_c * q * fma(cs, ztr, -ps * zti) : 0.0;
       if (slot == kRemSB - 1 || i == R - 1) {
         __syncwarp();
-        // (slot, group, comp) sums in fixed order over the group's L lanes
+        // (slot, group, direction, comp) sums in fixed order over the group's
+        // lanes of that direction, forward / backward into frem's two buffers
         const int ibase = i - slot;
-        for (int e = lane; e < (slot + 1) * G * 3; e += 32) {
-          const int sl = e / (3 * G), rem = e - sl * 3 * G, gg = rem / 3, comp = rem - 3 * gg;
+        const int nd = paired ? 2 : 1;
+        for (int e = lane; e < (slot + 1) * G * nd * 3; e += 32) {
+          const int sl = e / (3 * nd * G), rem = e - sl * 3 * nd * G, gd = rem / 3,
+                    comp = rem - 3 * gd;
+          const int gg = gd / nd, d = gd - nd * gg;
           const int cg = c0 + wg * G + gg;
           const int64_t a0g = (int64_t)cg * R;
           const int leng = cg < c1 ? (int)(a0g + R < n ? R : n - a0g) : 0;
@@ -1146,8 +1177,9 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
           if (ii < leng) {
             const double* rs = st + sl * 32 * 3;
             double sum = 0.0;
-            for (int j = 0; j < L; ++j) sum += rs[(gg * L + j) * 3 + comp];
-            frem[(a0g + (fwd ? ii : leng - 1 - ii)) * 3 + comp] = sum;
+            for (int j = 0; j < Ld; ++j) sum += rs[(gg * L + d * Ld + j) * 3 + comp];
+            const bool dfwd = paired ? d == 0 : true;
+            frem[(size_t)d * n * 3 + (a0g + (dfwd ? ii : leng - 1 - ii)) * 3 + comp] = sum;
           }
         }
         __syncwarp();
@@ -1231,15 +1263,15 @@ __global__ void __launch_bounds__(kKahanThreads) kahan_modes_kernel(
 }
 
 // forces_sorted += sum of the per-warp partial buffers (fixed order)
-// Buffer b < ngroups * nwarps belongs to warp b % nwarps of item group
-// b / nwarps and is written only if that warp holds items; buffer
-// ngroups * nwarps (when nbuf exceeds the grid) is the mixed warp's backward one.
+// Buffers b < 2 * ngroups * nwarps: (forward, backward) of warp (b / 2) % nwarps
+// of group b / (2 nwarps), written only if that warp holds modes; the rest are
+// the remainder sweep's.
 // NS > 1 (few particles, many buffers: small systems with full mode sums): NS
 // lanes per element take the buffers round robin and combine by a fixed
 // xor-shuffle tree (deterministic).
 template <int NS>
 __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int nbuf,
-                                            int ngroups, int nwarps, int ipg, int nitems,
+                                            int ngroups, int nwarps, int upg, int units,
                                             int64_t n3, double* __restrict__ out, int64_t e0,
                                             int64_t e1) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1249,10 +1281,10 @@ __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, in
   double v = 0.0;
   if (live)
     for (int b = sub; b < nbuf; b += NS) {
-      if (b < ngroups * nwarps) {
-        const int g = b / nwarps, w = b - g * nwarps;
-        const int cnt = min(nitems, (g + 1) * ipg) - g * ipg;
-        if (32 * w >= cnt) continue;
+      if (b < 2 * ngroups * nwarps) {
+        const int g = b / (2 * nwarps), w = (b >> 1) - g * nwarps;
+        const int cnt = min(units, (g + 1) * upg) - g * upg;
+        if (16 * w >= cnt) continue;
       }
       v += fpart[(size_t)b * n3 + e];
     }
@@ -1267,7 +1299,7 @@ __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, in
 static size_t sweep_smem(int R, int mh, int warps) {
   return sizeof(double2) * (size_t)mh * warps * 32 + sizeof(double2) * (size_t)(R + 1) * mh +
          sizeof(double) * (3 * (size_t)R + R + 2) +
-         sizeof(double) * (size_t)warps * kSB * 3 * kStageStride;
+         sizeof(double) * (size_t)warps * 2 * kStageBuf;
 }
 
 FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
@@ -1279,30 +1311,36 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   // is the forward sum, soewald2d.py:138-170; the backward sweep only adds the
   // j-side forces, 172-202): active items = dirs * P, carry layout stays 2P
   p.items = (dirs == 1 ? 1 : 2) * P;
-  // leftover items (items mod 32, <= 16) go to the remainder sweep, several
-  // chunks per warp; the main sweep then runs whole warps only
+  // force plans pair the directions: a warp = 16 modes x (forward, backward);
+  // energy-only plans: a warp = 32 consecutive forward items
+  p.paired = dirs == 1 ? 0 : 1;
+  const int upw = p.paired ? 16 : 32;          // units (modes / items) per warp
+  const int units = p.paired ? P : p.items;
+  // leftover units (units mod upw, <= 8 items) go to the remainder sweep,
+  // several chunks per warp; the main sweep then runs whole warps only
   p.rem = 0;
   p.rem_g = 0;
   {
-    const int left = p.items % 32;
-    if (kSweepRem && p.items >= 32 && left > 0 && left <= kSweepRemMax) {
-      p.rem = left;
-      p.rem_g = 32 / left;
+    const int left = units % upw;
+    const int left_items = left * (p.paired ? 2 : 1);
+    if (kSweepRem && units >= upw && left > 0 && left_items <= kSweepRemMax) {
+      p.rem = left_items;
+      p.rem_g = 32 / left_items;
       if (const char* env = getenv("SLAB_REM_G")) {  // tuning knob
         const int gg = atoi(env);
-        if (gg >= 1 && gg <= 32 / left) p.rem_g = gg;
+        if (gg >= 1 && gg <= 32 / left_items) p.rem_g = gg;
       }
     }
   }
-  p.items_main = p.items - p.rem;
-  const int nitems = p.items_main;
+  p.units_main = units - (p.rem ? units % upw : 0);
+  p.items_main = p.units_main * (p.paired ? 2 : 1);
   const int maxt = sweep_max_threads(mh);
-  p.ngroups = (nitems + maxt - 1) / maxt;
+  p.ngroups = (p.items_main + maxt - 1) / maxt;
   if (p.ngroups < 1) p.ngroups = 1;
-  p.ipg = (nitems + p.ngroups - 1) / p.ngroups;
-  if (p.rem) p.ipg = (p.ipg + 31) / 32 * 32;  // groups of whole warps
-  if (p.ipg < 1) p.ipg = 1;
-  p.warps = (p.ipg + 31) / 32;
+  p.upg = (p.units_main + p.ngroups - 1) / p.ngroups;
+  if (p.rem || p.paired) p.upg = (p.upg + upw - 1) / upw * upw;  // groups of whole warps
+  if (p.upg < 1) p.upg = 1;
+  p.warps = (p.upg + upw - 1) / upw;
   if (p.warps < 1) p.warps = 1;
   // >= 4 CTAs per SM of chunks in each rank's range (a z-split rank scans 1/ranks
   // of the chunks: shorter chunks keep its sweep grid from ending on a partial wave)
@@ -1343,13 +1381,11 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   p.c0 = 0;
   p.c1 = p.nch;
   p.smem_sweep = sweep_smem(R, mh, p.warps);
-  // one partial force buffer per (group, warp) + one for the backward lanes of
-  // the (at most one) warp that holds both directions
-  const int g_of_p = P / p.ipg;  // group containing item P (first backward item)
-  const bool mixed = P < nitems && ((P - g_of_p * p.ipg) % 32) != 0;
-  p.nbuf = p.ngroups * p.warps + (mixed ? 1 : 0);
+  // partial force buffers: forward and backward per (group, warp), then the
+  // remainder's forward and backward ones
+  p.nbuf = 2 * p.ngroups * p.warps;
   p.rem_buf = p.nbuf;
-  if (p.rem) p.nbuf += 1;
+  if (p.rem) p.nbuf += 2;
   return p;
 }
 
@@ -1529,23 +1565,23 @@ static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const d
     double* frem = w.fpart + (size_t)p.rem_buf * p.n * 3;
     if (p.swap)
       fourier_sweep_rem_kernel<MH, true><<<rblocks, 32 * kRemWarps, 0, rs.s>>>(
-          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.rem, p.rem_g, b,
-          w.carry, w.epart, frem, want_forces, p.c0, p.c1);
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.units_main, p.rem, p.paired, p.rem_g,
+          b, w.carry, w.epart, frem, want_forces, p.c0, p.c1);
     else
       fourier_sweep_rem_kernel<MH, false><<<rblocks, 32 * kRemWarps, 0, rs.s>>>(
-          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.rem, p.rem_g, b,
-          w.carry, w.epart, frem, want_forces, p.c0, p.c1);
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.units_main, p.rem, p.paired, p.rem_g,
+          b, w.carry, w.epart, frem, want_forces, p.c0, p.c1);
     cudaEventRecord(rs.join, rs.s);
   }
   if (p.items_main > 0) {
     if (p.swap)
       fourier_sweep_kernel<MH, true><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
-          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.ipg, b, w.carry,
-          w.epart, w.fpart, want_forces, p.c0);
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.units_main, p.upg, p.paired, b,
+          w.carry, w.epart, w.fpart, want_forces, p.c0);
     else
       fourier_sweep_kernel<MH, false><<<dim3(nch_r, p.ngroups), p.warps * 32, p.smem_sweep, st>>>(
-          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.items_main, p.ipg, b, w.carry,
-          w.epart, w.fpart, want_forces, p.c0);
+          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.units_main, p.upg, p.paired, b,
+          w.carry, w.epart, w.fpart, want_forces, p.c0);
   }
   if (p.rem) {
     cudaStreamWaitEvent(st, rem_side().join, 0);
@@ -1625,10 +1661,10 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
     if (e1 > e0) {
       if ((e1 - e0) < (int64_t)148 * 2048 && p.nbuf >= 16)
         fourier_force_reduce_kernel<8><<<(unsigned)((8 * (e1 - e0) + 255) / 256), 256, 0, st>>>(
-            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items_main, n3, forces_sorted, e0, e1);
+            w.fpart, p.nbuf, p.ngroups, p.warps, p.upg, p.units_main, n3, forces_sorted, e0, e1);
       else
         fourier_force_reduce_kernel<1><<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
-            w.fpart, p.nbuf, p.ngroups, p.warps, p.ipg, p.items_main, n3, forces_sorted, e0, e1);
+            w.fpart, p.nbuf, p.ngroups, p.warps, p.upg, p.units_main, n3, forces_sorted, e0, e1);
     }
   }
   return cudaGetLastError();

@@ -49,15 +49,17 @@ struct FourierPlan {
   int R;          // particles per chunk
   int nch;        // chunks
   int ngroups;    // item groups per chunk
-  int ipg;        // items per group
+  int upg;        // units per group: modes (paired) or items
   int warps;      // warps per CTA
-  int nbuf;       // partial force buffers (per group x warp, + 1 if a warp mixes directions)
+  int nbuf;       // partial force buffers (2 per group x warp, + 2 for the remainder)
   int items;      // active (mode, direction) items: 2P, or P for energy-only (forward)
   int c0, c1;     // chunk range this plan scans (z-split multi-GPU rank), default [0, nch)
   size_t smem_sweep;
   int swap;       // 1: real inputs swapped (u_r, u_i) -> (u_i, -u_r), i.e. the pass's result
                   // times -i (lone complex SOE terms, capi.cu prepare_soe)
-  int items_main; // items of the main sweep (whole warps when rem > 0)
+  int paired;     // 1: a warp = 16 modes x 2 directions (force plans); 0: 32 forward items
+  int units_main; // modes (paired) / items of the main sweep (whole warps when rem > 0)
+  int items_main; // items of the main sweep
   int rem;        // leftover items per chunk run by the remainder sweep (0: none)
   int rem_g;      // chunks per remainder warp (32 / rem)
   int rem_buf;    // the remainder's partial force buffer
