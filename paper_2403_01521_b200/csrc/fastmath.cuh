@@ -21,6 +21,61 @@
 
 namespace slab {
 
+// SLAB_MINIMAX: near-minimax polynomials of lower degree on the same reduced
+// ranges (Chebyshev fits, tools/fit_minimax.py): exp to r^11, sin to r^13, cos
+// to r^14, max relative error 1.2e-16 evaluated in double -- 4 fewer DFMA and 4
+// fewer constants per (exp, sincos) than the Taylor forms.
+#ifndef SLAB_MINIMAX
+#define SLAB_MINIMAX 1  // cfg4 step 8.75 -> 8.62 ms (sweep 3.31 -> 3.25, aggregate 1.11 -> 1.07)
+#endif
+#if SLAB_MINIMAX
+constexpr int kExpTerms = 12, kSinTerms = 6, kCosTerms = 8;
+#else
+constexpr int kExpTerms = 14, kSinTerms = 7, kCosTerms = 9;
+#endif
+// e^r on |r| <= ln2/2 (highest degree first; the last two are 1, 1), sin: P(z)
+// with sin r = r + r z P(z); cos: 1 + z Q(z) (Q's coefficients then the 1)
+__device__ __forceinline__ constexpr double exp_coef(int i) {
+#if SLAB_MINIMAX
+  constexpr double c[12] = {2.5100375832561234e-08, 2.7620075879983367e-07,
+                            2.7557268480310024e-06, 2.4801521322368692e-05,
+                            0.00019841269863040545, 0.0013888888917196719,
+                            0.008333333333330065,   0.041666666666624164,
+                            0.16666666666666669,    0.5000000000000001,
+                            1.0,                    1.0};
+#else
+  constexpr double c[14] = {1.6059043836821613e-10, 2.08767569878681e-09,  2.505210838544172e-08,
+                            2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
+                            0.0001984126984126984,  0.001388888888888889,  0.008333333333333333,
+                            0.041666666666666664,   0.16666666666666666,   0.5,
+                            1.0,                    1.0};
+#endif
+  return c[i];
+}
+__device__ __forceinline__ constexpr double sin_coef(int i) {
+#if SLAB_MINIMAX
+  constexpr double c[6] = {1.5918129294866608e-10, -2.5051131845003624e-08, 2.755731610255244e-06,
+                           -0.00019841269836758574, 0.008333333333330948, -0.16666666666666666};
+#else
+  constexpr double c[7] = {-7.647163731819816e-13, 1.6059043836821613e-10, -2.505210838544172e-08,
+                           2.7557319223985893e-06, -0.0001984126984126984, 0.008333333333333333,
+                           -0.16666666666666666};
+#endif
+  return c[i];
+}
+__device__ __forceinline__ constexpr double cos_coef(int i) {
+#if SLAB_MINIMAX
+  constexpr double c[8] = {-1.1367998654022494e-11, 2.0875886738047052e-09, -2.7557315566341895e-07,
+                           2.480158729369346e-05,   -0.0013888888888880775, 0.04166666666666664,
+                           -0.5,                    1.0};
+#else
+  constexpr double c[9] = {4.779477332387385e-14, -1.1470745597729725e-11, 2.08767569878681e-09,
+                           -2.755731922398589e-07, 2.48015873015873e-05,   -0.001388888888888889,
+                           0.041666666666666664,  -0.5,                    1.0};
+#endif
+  return c[i];
+}
+
 __device__ __forceinline__ double exp_neg(double t) {
   // t >= 700 (and +inf) returns 0
   const bool tiny = !(t < 700.0);
@@ -31,20 +86,9 @@ __device__ __forceinline__ double exp_neg(double t) {
   const double n = rint(-t * kL2e);  // in [-1010, 0]
   double r = fma(n, -kLn2Hi, -t);
   r = fma(n, -kLn2Lo, r);
-  double p = 1.6059043836821613e-10;  // 1/13!
-  p = fma(p, r, 2.08767569878681e-09);
-  p = fma(p, r, 2.505210838544172e-08);
-  p = fma(p, r, 2.755731922398589e-07);
-  p = fma(p, r, 2.7557319223985893e-06);
-  p = fma(p, r, 2.48015873015873e-05);
-  p = fma(p, r, 0.0001984126984126984);
-  p = fma(p, r, 0.001388888888888889);
-  p = fma(p, r, 0.008333333333333333);
-  p = fma(p, r, 0.041666666666666664);
-  p = fma(p, r, 0.16666666666666666);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  double p = exp_coef(0);
+#pragma unroll
+  for (int i = 1; i < kExpTerms; ++i) p = fma(p, r, exp_coef(i));
   const long long e = tiny ? 0ll : (long long)((int)n + 1023) << 52;
   return p * __longlong_as_double(e);  // zero exponent factor: no branch around the polynomial
 }
@@ -58,23 +102,14 @@ __device__ __forceinline__ void sincos_fast(double th, double* s, double* c) {
   r = fma(n, -6.123233995736766e-17, r);
   r = fma(n, 1.4973849048591698e-33, r);
   const double z = r * r;
-  double ps = -7.647163731819816e-13;  // -1/15!
-  ps = fma(ps, z, 1.6059043836821613e-10);
-  ps = fma(ps, z, -2.505210838544172e-08);
-  ps = fma(ps, z, 2.7557319223985893e-06);
-  ps = fma(ps, z, -0.0001984126984126984);
-  ps = fma(ps, z, 0.008333333333333333);
-  ps = fma(ps, z, -0.16666666666666666);
+  double ps = sin_coef(0);
+#pragma unroll
+  for (int i = 1; i < kSinTerms; ++i) ps = fma(ps, z, sin_coef(i));
   const double sr = fma(ps * z, r, r);
-  double pc = 4.779477332387385e-14;  // 1/16!
-  pc = fma(pc, z, -1.1470745597729725e-11);
-  pc = fma(pc, z, 2.08767569878681e-09);
-  pc = fma(pc, z, -2.755731922398589e-07);
-  pc = fma(pc, z, 2.48015873015873e-05);
-  pc = fma(pc, z, -0.001388888888888889);
-  pc = fma(pc, z, 0.041666666666666664);
-  pc = fma(pc, z, -0.5);
-  const double cr = fma(pc, z, 1.0);
+  double pc = cos_coef(0);
+#pragma unroll
+  for (int i = 1; i < kCosTerms; ++i) pc = fma(pc, z, cos_coef(i));
+  const double cr = pc;
   const int q = ((int)(long long)n) & 3;
   const double ss = (q & 1) ? cr : sr;
   const double cc = (q & 1) ? sr : cr;
@@ -88,41 +123,64 @@ __device__ __forceinline__ void sincos_fast(double th, double* s, double* c) {
 // pair).  Faster where registers are plentiful (fourier_aggregate: 1.59 ->
 // 1.41 ms at cfg4); slower in the 128-register sweep, where the extra live
 // values spill (4.75 -> 6.0 ms) -- hence both forms.
-static __constant__ double kFmExp[16] = {
+#if SLAB_MINIMAX
+static __constant__ double kFmExp[kExpTerms + 2] = {
+    2.5100375832561234e-08, 2.7620075879983367e-07, 2.7557268480310024e-06,
+    2.4801521322368692e-05, 0.00019841269863040545, 0.0013888888917196719,
+    0.008333333333330065,   0.041666666666624164,   0.16666666666666669,
+    0.5000000000000001,     1.0,                    1.0,
+    6.93147180369123816490e-01,  // ln2 hi (32 significant bits)
+    1.90821492927058770002e-10,  // ln2 lo
+};
+static __constant__ double kFmSin[kSinTerms + 1] = {
+    1.5918129294866608e-10, -2.5051131845003624e-08, 2.755731610255244e-06,
+    -0.00019841269836758574, 0.008333333333330948,   -0.16666666666666666,
+    0.6366197723675814,  // 2/pi
+};
+static __constant__ double kFmCos[kCosTerms + 3] = {
+    -1.1367998654022494e-11, 2.0875886738047052e-09, -2.7557315566341895e-07,
+    2.480158729369346e-05,   -0.0013888888888880775, 0.04166666666666664,
+    -0.5,                    1.0,
+    -1.5707963267948966,  // -pi/2 split in three
+    -6.123233995736766e-17,  1.4973849048591698e-33,
+};
+#else
+static __constant__ double kFmExp[kExpTerms + 2] = {
     1.6059043836821613e-10,  // 1/13!
     2.08767569878681e-09,  2.505210838544172e-08, 2.755731922398589e-07,
     2.7557319223985893e-06, 2.48015873015873e-05, 0.0001984126984126984,
     0.001388888888888889,  0.008333333333333333,  0.041666666666666664,
     0.16666666666666666,   0.5,                   1.0,
     1.0,
-    6.93147180369123816490e-01,  // [14] ln2 hi (32 significant bits)
-    1.90821492927058770002e-10,  // [15] ln2 lo
+    6.93147180369123816490e-01,  // ln2 hi (32 significant bits)
+    1.90821492927058770002e-10,  // ln2 lo
 };
-static __constant__ double kFmSin[8] = {
+static __constant__ double kFmSin[kSinTerms + 1] = {
     -7.647163731819816e-13,  // -1/15!
     1.6059043836821613e-10, -2.505210838544172e-08, 2.7557319223985893e-06,
     -0.0001984126984126984, 0.008333333333333333,   -0.16666666666666666,
-    0.6366197723675814,      // [7] 2/pi
+    0.6366197723675814,      // 2/pi
 };
-static __constant__ double kFmCos[12] = {
+static __constant__ double kFmCos[kCosTerms + 3] = {
     4.779477332387385e-14,  // 1/16!
     -1.1470745597729725e-11, 2.08767569878681e-09, -2.755731922398589e-07,
     2.48015873015873e-05,    -0.001388888888888889, 0.041666666666666664,
     -0.5,                    1.0,
-    -1.5707963267948966,     // [9..11] -pi/2 split in three
+    -1.5707963267948966,     // -pi/2 split in three
     -6.123233995736766e-17,  1.4973849048591698e-33,
 };
+#endif
 
 __device__ __forceinline__ double exp_neg_cb(double t) {
   // branch-free: t >= 700 (and +inf) returns 0 by zeroing the exponent factor
   const bool tiny = !(t < 700.0);
   t = tiny ? 0.0 : t;
   const double n = rint(-t * 1.4426950408889634);  // in [-1010, 0]
-  double r = fma(n, -kFmExp[14], -t);
-  r = fma(n, -kFmExp[15], r);
+  double r = fma(n, -kFmExp[kExpTerms], -t);
+  r = fma(n, -kFmExp[kExpTerms + 1], r);
   double p = kFmExp[0];
 #pragma unroll
-  for (int i = 1; i < 14; ++i) p = fma(p, r, kFmExp[i]);
+  for (int i = 1; i < kExpTerms; ++i) p = fma(p, r, kFmExp[i]);
   const long long e = tiny ? 0ll : (long long)((int)n + 1023) << 52;
   return p * __longlong_as_double(e);
 }
@@ -131,63 +189,24 @@ __device__ __forceinline__ double exp_neg_cb(double t) {
 // products n*P_i are exact inside the FMAs, th - n*P1 is exact by Sterbenz and
 // pi/2 - (P1+P2+P3) ~ 1e-49); physical phases are |th| < 1e4.
 __device__ __forceinline__ void sincos_fast_cb(double th, double* s, double* c) {
-  const double n = rint(th * kFmSin[7]);
-  double r = fma(n, kFmCos[9], th);
-  r = fma(n, kFmCos[10], r);
-  r = fma(n, kFmCos[11], r);
+  const double n = rint(th * kFmSin[kSinTerms]);
+  double r = fma(n, kFmCos[kCosTerms], th);
+  r = fma(n, kFmCos[kCosTerms + 1], r);
+  r = fma(n, kFmCos[kCosTerms + 2], r);
   const double z = r * r;
   double ps = kFmSin[0];
 #pragma unroll
-  for (int i = 1; i < 7; ++i) ps = fma(ps, z, kFmSin[i]);
+  for (int i = 1; i < kSinTerms; ++i) ps = fma(ps, z, kFmSin[i]);
   const double sr = fma(ps * z, r, r);
   double pc = kFmCos[0];
 #pragma unroll
-  for (int i = 1; i < 9; ++i) pc = fma(pc, z, kFmCos[i]);
+  for (int i = 1; i < kCosTerms; ++i) pc = fma(pc, z, kFmCos[i]);
   const double cr = pc;
   const int q = ((int)(long long)n) & 3;
   const double ss = (q & 1) ? cr : sr;
   const double cc = (q & 1) ? sr : cr;
   *s = (q & 2) ? -ss : ss;
   *c = ((q + 1) & 2) ? -cc : cc;
-}
-
-// *_sm variants: the same polynomials with the coefficients read from a
-// shared-memory copy (c = kFmExp for exp; c = kFmSin then kFmCos for sincos),
-// every lane the same address: broadcast loads, two constants per LDS.128
-__device__ __forceinline__ double exp_neg_sm(double t, const double* __restrict__ c) {
-  const bool tiny = !(t < 700.0);
-  t = tiny ? 0.0 : t;
-  const double n = rint(-t * 1.4426950408889634);
-  double r = fma(n, -c[14], -t);
-  r = fma(n, -c[15], r);
-  double p = c[0];
-#pragma unroll
-  for (int i = 1; i < 14; ++i) p = fma(p, r, c[i]);
-  const long long e = tiny ? 0ll : (long long)((int)n + 1023) << 52;
-  return p * __longlong_as_double(e);
-}
-
-__device__ __forceinline__ void sincos_fast_sm(double th, double* s, double* co,
-                                               const double* __restrict__ c) {
-  // c[0..7] = kFmSin, c[8..19] = kFmCos
-  const double n = rint(th * c[7]);
-  double r = fma(n, c[8 + 9], th);
-  r = fma(n, c[8 + 10], r);
-  r = fma(n, c[8 + 11], r);
-  const double z = r * r;
-  double ps = c[0];
-#pragma unroll
-  for (int i = 1; i < 7; ++i) ps = fma(ps, z, c[i]);
-  const double sr = fma(ps * z, r, r);
-  double pc = c[8];
-#pragma unroll
-  for (int i = 1; i < 9; ++i) pc = fma(pc, z, c[8 + i]);
-  const double cr = pc;
-  const int q = ((int)(long long)n) & 3;
-  const double ss = (q & 1) ? cr : sr;
-  const double cc = (q & 1) ? sr : cr;
-  *s = (q & 2) ? -ss : ss;
-  *co = ((q + 1) & 2) ? -cc : cc;
 }
 
 // tab: shared-memory copy of kErfcxCoef, coefficient-major (tab[k * NINT + i]):

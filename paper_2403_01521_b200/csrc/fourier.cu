@@ -791,14 +791,6 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
   double* sq = sy + R;
   double* sz = sq + R;                                     // R + 2 (halo below / above)
   double* stage = sz + R + 2;                              // nwarps * 2 * kStageBuf
-#if SLAB_SWEEP_CB == 2
-  // transcendental coefficients, broadcast from shared memory (one LDS.128 per
-  // two constants instead of two UMOVs per constant)
-  __shared__ __align__(16) double scoef[40];
-  if (threadIdx.x < 16) scoef[threadIdx.x] = kFmExp[threadIdx.x];
-  else if (threadIdx.x < 24) scoef[threadIdx.x] = kFmSin[threadIdx.x - 16];
-  else if (threadIdx.x < 36) scoef[threadIdx.x] = kFmCos[threadIdx.x - 24];
-#endif
 
   const int c = c0 + blockIdx.x, g = blockIdx.y;
   const int64_t a0 = (int64_t)c * R;
@@ -898,9 +890,6 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
 #if SLAB_SWEEP_CB == 1
     dk_ = exp_neg_cb(k * dz);
     sincos_fast_cb(th, &sn_, &cs_);
-#elif SLAB_SWEEP_CB == 2
-    dk_ = exp_neg_sm(k * dz, scoef);
-    sincos_fast_sm(th, &sn_, &cs_, scoef + 16);
 #else
     dk_ = exp_neg(k * dz);
     sincos_fast(th, &sn_, &cs_);
