@@ -11,8 +11,8 @@
 //                   degree-15/16 Taylor on |r| <= pi/4.
 //   erfc_gauss(x)   erfc(x) and e^{-x^2} for x >= 0 sharing one exp: e^{-x^2}
 //                   with the exact x^2 = hi + lo split, erfc = erfcx * e^{-x^2}
-//                   with erfcx from a piecewise degree-9 table on [0, 6)
-//                   (erfcx_table.cuh, 48 rows, rel. err 2e-16), libdevice beyond.
+//                   with erfcx from a piecewise degree-10 table on [0, 6)
+//                   (erfcx_table.cuh, 24 rows, rel. err 3.4e-16), libdevice beyond.
 // Parity is still checked end to end against the reference (1e-10 / 1e-9).
 #pragma once
 #include <cuda_runtime.h>
@@ -212,7 +212,8 @@ __device__ __forceinline__ void sincos_fast_cb(double th, double* s, double* c) 
 // tab: shared-memory copy of kErfcxCoef, coefficient-major (tab[k * NINT + i]):
 // the lanes of a warp evaluate different intervals i, and with consecutive
 // intervals in consecutive 8-byte words only rows 16 apart share a bank (pair
-// distances put x = alpha r in ~20 adjacent rows).  Interval-major rows read as
+// distances put x = alpha r in ~14 adjacent rows of width 1/4, so most loads
+// see no such collision).  Interval-major rows read as
 // 16-byte pairs measured 5% slower on the pair kernel (8 lanes per LDS.128
 // phase over 8 bank groups collide).
 #ifndef SLAB_ERFC_CB
