@@ -216,6 +216,12 @@ __global__ void cell_gather_kernel(const double* __restrict__ pos, const double*
 }
 
 constexpr int kSRThreads = 128;
+#ifndef SLAB_NBR_WIDE
+#define SLAB_NBR_WIDE 1
+#endif
+struct __align__(32) F8 {
+  float v[8];
+};
 constexpr int kRing = 16;  // staged neighbour indices per thread (two 32-byte sectors)
 
 // Pass 1: neighbour rows.  One thread per home particle in cell order.  Cells
@@ -296,6 +302,23 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
       int jj = start[col + zlo];
       // (scanning the warp-union of the lanes' ranges instead -- broadcast
       // loads, no idle lanes -- measured 1.51 ms against 1.13 ms per lane)
+#if SLAB_NBR_WIDE
+      // two candidates per 256-bit load (32-byte aligned pairs): half the L1
+      // requests of this L1-throughput-bound screen
+      if ((jj & 1) && jj < b1) {
+        test(jj, cpf[jj], px, py);
+        ++jj;
+      }
+      for (; jj + 4 <= b1; jj += 4) {
+        const F8 q0 = *reinterpret_cast<const F8*>(cpf + jj);
+        const F8 q1 = *reinterpret_cast<const F8*>(cpf + jj + 2);
+        test(jj, make_float4(q0.v[0], q0.v[1], q0.v[2], q0.v[3]), px, py);
+        test(jj + 1, make_float4(q0.v[4], q0.v[5], q0.v[6], q0.v[7]), px, py);
+        test(jj + 2, make_float4(q1.v[0], q1.v[1], q1.v[2], q1.v[3]), px, py);
+        test(jj + 3, make_float4(q1.v[4], q1.v[5], q1.v[6], q1.v[7]), px, py);
+        if (cnt - done >= 8) flush8();  // pending <= 7 + 4 < kRing
+      }
+#else
       for (; jj + 4 <= b1; jj += 4) {
         const float4 p0 = cpf[jj], p1 = cpf[jj + 1], p2 = cpf[jj + 2], p3 = cpf[jj + 3];
         test(jj, p0, px, py);
@@ -304,6 +327,7 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
         test(jj + 3, p3, px, py);
         if (cnt - done >= 8) flush8();  // pending <= 7 + 4 < kRing
       }
+#endif
       for (; jj < b1; ++jj) {
         test(jj, cpf[jj], px, py);
         if (cnt - done >= 8) flush8();
