@@ -514,8 +514,15 @@ __device__ __forceinline__ double4 ld_rec(const double4* p) {  // one 256-bit lo
 // SPLIT consecutive lanes share a home, taking its row's 4-entry blocks round
 // robin, and combine their partial forces with a fixed xor-shuffle tree
 // (deterministic).
+#ifndef SLAB_PAIR_CTAS
+// resident CTAs per SM the pair kernel is compiled and gridded for (cfg4, 24-row
+// erfcx table: 5 -> 1.95 ms; 6 / 7 / 8 cap the registers at 80 / 72 / 64 and
+// spill: 2.08 / 1.99 / 2.19 ms)
+#define SLAB_PAIR_CTAS 5
+#endif
+constexpr int kPairCtas = SLAB_PAIR_CTAS;
 template <int KIND, int SPLIT>
-__global__ void __launch_bounds__(kSRThreads) pair_list_kernel(
+__global__ void __launch_bounds__(kSRThreads, kPairCtas) pair_list_kernel(
     const double4* __restrict__ cp, const int32_t* __restrict__ order,
     const int32_t* __restrict__ nbr, const int32_t* __restrict__ nn, int64_t a_begin,
     int64_t a_end, int kcap, double lx, double ly, double alpha, double rc2, double eps,
@@ -783,13 +790,15 @@ __global__ void __launch_bounds__(1024) half_sum_kernel(const double* __restrict
   if (threadIdx.x == 0) out[0] = 0.5 * red[0];
 }
 
-// pair_list_kernel grid: one resident wave (5 CTAs per SM at 90 registers), grid-striding
-static int64_t pair_grid(int64_t blocks) { return blocks < 148 * 5 ? blocks : 148 * 5; }
-// lanes per home: fill one resident wave (148 SMs x 5 CTAs x 128 threads) when
-// there are fewer homes than that (cfg2, N = 1e4: 8 lanes per home)
+// pair_list_kernel grid: one resident wave (kPairCtas CTAs per SM), grid-striding
+static int64_t pair_grid(int64_t blocks) {
+  return blocks < 148 * kPairCtas ? blocks : 148 * kPairCtas;
+}
+// lanes per home: fill one resident wave (148 SMs x kPairCtas CTAs x 128 threads)
+// when there are fewer homes than that (cfg2, N = 1e4: 8 lanes per home)
 static int pair_split(int64_t nh) {
   int s = 1;
-  while (s < 8 && nh * s < (int64_t)148 * 5 * kSRThreads) s *= 2;
+  while (s < 8 && nh * s < (int64_t)148 * kPairCtas * kSRThreads) s *= 2;
   return s;
 }
 
