@@ -67,6 +67,35 @@ def test_ragged_sizes_match_oracle(pk, n):
     _check(bd, f, e_ref, f_ref)
 
 
+@pytest.mark.parametrize("P", [15, 16, 17, 20, 24, 36, 100])
+@pytest.mark.parametrize("M", [16, 24])
+def test_mode_counts_and_warp_layouts_match_oracle(pk, P, M):
+    """Sweep layouts by mode count: a force plan's warp holds 16 modes x 2
+    directions, so P = 15 / 24 leave a partial warp, 16 is exact, and 17 / 20 /
+    36 / 100 send their leftover modes (P mod 16 <= 4) to the remainder sweep;
+    M = 24 (12 pairs) takes the one-CTA-per-SM form.  n = 3000 spans several
+    chunks of both sweeps."""
+    rng = np.random.default_rng(P * 100 + M)
+    box = pk.BoxGeometry(20.0, 20.0, 10.0, sigma_top=0.002, sigma_bot=-0.001)
+    n = 3000
+    pos = rng.uniform([0, 0, 0.1], [20.0, 20.0, 9.9], size=(n, 3))
+    q = rng.choice([-1.0, 1.0, 2.0], size=n)
+    s = pk.make_system(q, np.ones(n), pos, box)
+    params = pk.make_ewald_params(0.8, 3.6, box)
+    soe = pk.build_soe_contour(M)
+    modes = pk.ModeSampler(0.8, box, seed=P).batch(P)
+    H = pk.normalization_H(0.8, box)
+    cq = pk.charge_term_sum(0.8, box, float(np.sum(q ** 2)))
+    bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), P, H=H, c_q=cq)
+    cv = (H / P) * (2 / np.sqrt(np.pi)) * 0.8
+    e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes, cv, cq)
+    _check(bd, f, e_ref, f_ref)
+    # energy-only plans (forward items only, 32 consecutive items per warp)
+    from paper_2403_01521_b200 import rbse2d
+    u = rbse2d.rb_energy_estimate(s, box, 0.8, soe, modes, H, c_q=cq)
+    assert abs(u - e_ref[1]) <= E_TOL * abs(e_ref[1])
+
+
 def test_single_mode_and_full_sum_small(pk):
     """P = 1 (one item pair per chunk) and a full deterministic mode sum."""
     rng = np.random.default_rng(7)
