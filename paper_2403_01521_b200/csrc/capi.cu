@@ -675,6 +675,12 @@ static int ensure_fork(SlabCtx* ctx) {
   if (ctx->hi) return SLAB_OK;
   int least = 0, greatest = 0;
   CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  // (the scan chain one notch below the greatest priority, so that the remainder
+  // sweep and the k = 0 chain take SM slots as soon as sweep CTAs retire rather
+  // than after its last wave, stretched the main sweep by more than the tail it
+  // saved: cfg4 8.49 -> 8.60 ms; the k = 0 chain and decay table enqueued before
+  // the scan's wait for the short range, to run beside the pair kernel, delayed
+  // the pair kernel instead: 8.48 -> 8.74 ms)
   CK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
 #ifndef SLAB_SHORT_HI
 #define SLAB_SHORT_HI 0
