@@ -680,7 +680,8 @@ static int ensure_fork(SlabCtx* ctx) {
   // than after its last wave, stretched the main sweep by more than the tail it
   // saved: cfg4 8.49 -> 8.60 ms; the k = 0 chain and decay table enqueued before
   // the scan's wait for the short range, to run beside the pair kernel, delayed
-  // the pair kernel instead: 8.48 -> 8.74 ms)
+  // the pair kernel instead: 8.48 -> 8.74 ms; the k = 0 chain alone above the
+  // scan's priority ran inside the aggregate and stretched it: 8.48 -> 8.63 ms)
   CK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
 #ifndef SLAB_SHORT_HI
 #define SLAB_SHORT_HI 0
