@@ -413,7 +413,10 @@ def run_ours(args, rank, world, local):
     c_q = charge_term_sum(wl.alpha, wl.box, float(np.sum(wl.system.charge ** 2)))
     ev = DeviceEvaluator(wl.system, wl.box, params, soe, P=wl.P, H=H, c_q=c_q, seed=wl.seed,
                          rank=rank, world=world, group=group, shard_mode=args.shard_mode)
-    use_graph = world == 1 and wl.n < 200_000
+    # one GPU: the step replayed as a CUDA graph (all sizes since round 2: at cfg4
+    # the ~470 launches' gaps cost 0.14 ms of 8.5 ms eagerly); the scan span is
+    # then timed on eager steps with the same events (below)
+    use_graph = world == 1
     ev.warmup()  # workspace + short-range neighbour capacity (may rerun once)
     for _ in range(args.warmup):
         ev.step()
