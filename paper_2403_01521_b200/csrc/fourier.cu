@@ -996,7 +996,10 @@ __global__ void __launch_bounds__(sweep_max_threads(MH), sweep_min_blocks(MH)) f
     if (ns < 4 && bl >= 1) {
       const double* prv = st + ((bl & 1) ^ 1) * kStageBuf + roff;
       for (int j = 4 * ns; j < 16; ++j) facc += prv[j];
-      if (rsum) rdst[rstep * (4 * (bl - 1) + rslot)] = facc;
+      if (rsum) {
+        SLAB_BOUND(a0 + 4 * (bl - 1) + rslot, n);
+        rdst[rstep * (4 * (bl - 1) + rslot)] = facc;
+      }
     }
     __syncwarp();
     const double* lst = st + (bl & 1) * kStageBuf + roff;
@@ -1168,6 +1171,7 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
             double sum = 0.0;
             for (int j = 0; j < Ld; ++j) sum += rs[(gg * L + d * Ld + j) * 3 + comp];
             const bool dfwd = paired ? d == 0 : true;
+            SLAB_BOUND(a0g + (dfwd ? ii : leng - 1 - ii), n);
             frem[(size_t)d * n * 3 + (a0g + (dfwd ? ii : leng - 1 - ii)) * 3 + comp] = sum;
           }
         }
