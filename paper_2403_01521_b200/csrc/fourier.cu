@@ -1376,9 +1376,9 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
                       ctas(agg_mma_smem(R, mh), 32 * tpc, kAggRegs) < ag_full))
       R /= 2;
   }
-  if (const char* env = getenv("SLAB_CHUNK_R")) {  // tuning knob (power of two, 16..256)
+  if (const char* env = getenv("SLAB_CHUNK_R")) {  // tuning knob (multiple of 4, 16..256)
     const int r = atoi(env);
-    if (r >= 16 && r <= kMaxR && (r & (r - 1)) == 0) R = r;
+    if (r >= 16 && r <= kMaxR && r % 4 == 0) R = r;
   }
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
@@ -1545,6 +1545,8 @@ static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const d
                              const double2* tin, cudaStream_t st) {
   const int nch_r = p.c1 - p.c0;
   if (nch_r <= 0) return cudaGetLastError();
+  // forces need both directions in the paired lane layout (plans with dirs = 2)
+  if (want_forces && !p.paired) return cudaErrorInvalidValue;
   if (p.nch > 1) {
     const dim3 cg = carry_grid(p);
     const int nseg = cg.z * kCarrySegs;
