@@ -12,9 +12,10 @@
 //  * Conjugate pairing.  s_{M-1-l} = conj(s_l) bitwise, so per pair one keeps two
 //    complex recurrences with REAL inputs (R: q cos theta, I: -+ q sin theta) and
 //    c_l G_l + conj = 2Re(c_l R_l) + 2i Re(c_l I_l).  kappa is real.
-//  * Lanes = (mode, direction) work items, particles in sequence.  Every lane of a
-//    warp walks the same z-sorted particle (forward lanes from the chunk start,
-//    backward lanes from its end), so the k-independent per-particle decays
+//  * Lanes = (mode, direction) work items, particles in sequence (a force plan's
+//    warp: 16 modes forward in lanes 0-15, the same modes backward in 16-31).
+//    Forward lanes walk the chunk from its start and backward lanes from its
+//    end, each half-warp one particle per step, so the k-independent decays
 //    e^{-b_l dz} are BROADCAST from shared memory: they are computed once per
 //    step (decay_table_kernel) and reused by all 2P items -- the kernel is FP64
 //    bound, not HBM bound.
@@ -23,9 +24,10 @@
 //    k-independent weights staged in smem, (2) a carry scan over chunks,
 //    (3) the exact recurrence from the carried-in state with the fused
 //    sincos/exp/energy/force epilogue.  All exponents stay <= 0 (stable in Lz).
-//  * Forces: per particle the 32 lanes' contributions are staged transposed in
-//    smem and row-summed (forward and backward lanes separately), accumulated
-//    per warp, then summed over warps in fixed order: deterministic, no atomics.
+//  * Forces: per particle the lanes' contributions are staged transposed in smem
+//    and row-summed (forward and backward halves separately, spread through the
+//    next particles' steps) into per-warp partial buffers, then summed over
+//    warps in fixed order: deterministic, no atomics.
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -73,8 +75,9 @@ constexpr int kSweepMaxThreads = SLAB_SWEEP_MAXT;  // force staging batch (parti
 // banks; two buffers per warp (one batch staged while the previous one is summed)
 constexpr int kStageStride = 34;
 constexpr int kStageBuf = 3 * 4 * kStageStride;  // 4 particles x 3 components
-// CTAs per SM the sweep is compiled for: 2 (128 registers) up to SLAB_SWEEP_BIG_MH
-// pairs; 1 above it, where 128 registers spill hundreds of bytes per lane
+// CTAs per SM the sweep is compiled for: 2 (<= 168 registers at 192 threads) up to
+// SLAB_SWEEP_BIG_MH pairs; 1 above it, where two CTAs' budget spills hundreds of
+// bytes per lane
 #ifndef SLAB_SWEEP_BIG_MH
 #define SLAB_SWEEP_BIG_MH 10  // cfg3 (M = 24, 12 pairs): sweep 1.90 -> 1.31 ms; 8 pairs stay at 2 CTAs (4.14 vs 4.86 ms)
 #endif
@@ -762,8 +765,8 @@ static int carry_groups(int nch, int items, int mh) {
 //   sum_l 2Re(c_l R_l) = sum_l Re(H^R_l)               (no C in the loop body)
 //   sum_l 2Re(c_l b_l R_l) = sum_l Re(b_l H^R_l)        (b_l k-independent: kernel param)
 // and the real input enters as H += C_l u.  C_l lives in shared memory
-// (per-lane column), which keeps the kernel at <= 128 registers: 2 CTAs / 16
-// warps per SM to hide the fp64 dependency latency.
+// (per-lane column), which keeps the 8-pair kernel at <= 168 registers: two
+// 6-warp CTAs per SM (3 warps per sub-partition) without spills.
 // Lanes (force plans, `paired`): a warp holds 16 modes, forward in lanes 0-15
 // and backward in 16-31, so every warp has the same shape.  Energy-only plans
 // (forward items only) keep consecutive items per lane.
