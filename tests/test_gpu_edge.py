@@ -96,6 +96,29 @@ def test_mode_counts_and_warp_layouts_match_oracle(pk, P, M):
     assert abs(u - e_ref[1]) <= E_TOL * abs(e_ref[1])
 
 
+@pytest.mark.parametrize("M", [4, 6, 10, 12, 14, 18, 20, 22])
+def test_every_soe_term_count_matches_oracle(pk, M):
+    """Each sweep / aggregate / k = 0 instantiation (2 .. 11 conjugate pairs; 8
+    and 12 are covered above): energies and forces against the oracle, P = 20
+    (remainder groups) and P = 9 (a partial warp), n spanning several chunks."""
+    rng = np.random.default_rng(M)
+    box = pk.BoxGeometry(18.0, 16.0, 9.0, sigma_top=-0.003, sigma_bot=0.002)
+    n = 1500
+    pos = rng.uniform([0, 0, 0.05], [18.0, 16.0, 8.95], size=(n, 3))
+    q = rng.choice([-1.0, 1.0, 2.0], size=n)
+    s = pk.make_system(q, np.ones(n), pos, box)
+    params = pk.make_ewald_params(0.8, 3.6, box)
+    soe = pk.build_soe_contour(M)
+    H = pk.normalization_H(0.8, box)
+    cq = pk.charge_term_sum(0.8, box, float(np.sum(q ** 2)))
+    for P in (20, 9):
+        modes = pk.ModeSampler(0.8, box, seed=M + P).batch(P)
+        bd, f = pk.rb_energy_forces(s, box, params, soe, _Stub(modes), P, H=H, c_q=cq)
+        cv = (H / P) * (2 / np.sqrt(np.pi)) * 0.8
+        e_ref, f_ref = _oracle_eval(pk, s, box, params, soe, modes, cv, cq)
+        _check(bd, f, e_ref, f_ref)
+
+
 def test_single_mode_and_full_sum_small(pk):
     """P = 1 (one item pair per chunk) and a full deterministic mode sum."""
     rng = np.random.default_rng(7)
