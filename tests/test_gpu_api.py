@@ -438,7 +438,13 @@ def test_run_many_batches_matches_per_batch_estimates(pk):
     s = _slab_system(pk, 25, box, 63)
     params = pk.make_ewald_params(0.8, 4.0, box)
     soe8 = pk.build_soe_contour(8)
-    P, nb = 16, 600  # 9600 modes: three 4096-mode passes
+    _batches_vs_estimates(pk, s, box, params, soe8, 16, 600)  # three 4096-mode passes
+    # P = 12: passes of 341 batches (4092 items: a partial warp) and a 59-batch
+    # tail (708 items = 22 warps + 4 items in the remainder sweep)
+    _batches_vs_estimates(pk, s, box, params, soe8, 12, 400)
+
+
+def _batches_vs_estimates(pk, s, box, params, soe8, P, nb):
     est = pk.run_many_batches(s, box, params, soe8, n_batches=nb, P=P, seed=21)
     H = pk.normalization_H(0.8, box)
     c_q = pk.charge_term_sum(0.8, box, float(np.sum(s.charge ** 2)))
