@@ -825,8 +825,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   // Large systems on device buffers: only the z sort + gather run beside the
   // short range (latency-bound passes that barely compete with it); the scan
   // waits for the short range, so its kernels keep the GPU to themselves.
-  const bool fork_sort = kForkSort && !fork_all && !a->skip_short_range && n > 0 &&
-                         a->phase == 0;
+  // (Also for the two z-split phases: phase 1 forks, phase 2 joins; round 1
+  // ran a z-split rank's sort after its short range, 0.26 ms of a 1.8 ms rank
+  // step at W = 8.)
+  const bool fork_sort = kForkSort && !fork_all && !a->skip_short_range && n > 0;
   const bool fork = fork_all || fork_sort;
   // ... and with SLAB_SPLIT_SHORT the neighbour screen (no fp64 work) also runs
   // beside the scan's first phase while the pair kernel waits for the scan's end

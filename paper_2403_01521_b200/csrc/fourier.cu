@@ -1037,21 +1037,35 @@ constexpr int kRemSB = 4;  // steps per force flush
 #ifndef SLAB_REM_MINB
 #define SLAB_REM_MINB 1
 #endif
-template <int MH, bool kSwap>
-__global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_rem_kernel(
+#ifndef SLAB_REM_MINB2
+#define SLAB_REM_MINB2 3  // (3 x 4 warps x 168 registers fill the register file)
+#endif
+constexpr int kRemMinB2 = SLAB_REM_MINB2;
+// SPL = 2 (opt-in, SLAB_REM_SPL=2, from 4 pairs): an item's pairs are split
+// over two lanes (half h carries pairs [h MS, h MS + MS)); their readout sums
+// are combined with one shuffle per sum, the transcendentals and the g chain
+// run on both lanes, and half 0 alone stages forces and writes the energy.
+// Twice the warps and half the state per lane -- measured slower (section
+// 4.1 of DESIGN.md), kept as the experiment's switch.
+template <int MH, bool kSwap, int SPL>
+__global__ void __launch_bounds__(32 * kRemWarps, SPL == 2 ? (MH <= 8 ? kRemMinB2 : 2) : SLAB_REM_MINB) fourier_sweep_rem_kernel(
     const double* __restrict__ xs, const double* __restrict__ ys, const double* __restrict__ zs,
     const double* __restrict__ qs, const double2* __restrict__ dtab, int64_t n, int R,
     const double* __restrict__ modetab, int P, int unit0, int L, int paired, int G, BVec b,
     const double2* __restrict__ carry, double* __restrict__ epart, double* __restrict__ frem,
     int want_forces, int c0, int c1) {
+  constexpr int MS = (MH + SPL - 1) / SPL;  // pairs per lane
   __shared__ double stg[kRemWarps][kRemSB * 32 * 3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wg = blockIdx.x * kRemWarps + warp;
-  const int grp = lane / L;
+  const int LS = L * SPL;  // lanes per chunk group
+  const int grp = lane / LS;
+  const int hs = (lane % LS) / L;  // pair half of this lane
   const int c = c0 + wg * G + grp;
-  const bool active = lane < G * L && c < c1;
-  // paired: the group's first L/2 lanes are modes unit0.. forward, the rest
-  // the same modes backward; otherwise L consecutive (forward) items
+  const bool active = lane < G * LS && c < c1;
+  // paired: the group's first L/2 lanes (of each half) are modes unit0..
+  // forward, the rest the same modes backward; otherwise L consecutive
+  // (forward) items
   const int Ld = paired ? L / 2 : L;
   const int jl = lane % L;
   const int item = jl < Ld ? unit0 + jl : P + unit0 + (jl - Ld);
@@ -1063,82 +1077,130 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
   const double* mt = modetab + (size_t)t * mode_stride(MH);
   const double kx = mt[0], ky = mt[1], k = mt[2];
   const double sigma = fwd ? 1.0 : -1.0;
-  const double fxy_c = active ? sigma * mt[3] : 0.0;
-  const double fz_c = active ? -sigma * mt[4] : 0.0;
+  const bool owner = active && hs == 0;  // stages forces, writes the energy
+  const double fxy_c = owner ? sigma * mt[3] : 0.0;
+  const double fz_c = owner ? -sigma * mt[4] : 0.0;
   const double kappa = mt[5];
   const double two_k = 2.0 * k;
   const int nc = ncomp_of(MH);
-  C2 HR[MH], HI[MH], CL[MH];
+  const int lb = hs * MS;  // first pair of this lane
+  C2 HR[MS], HI[MS], CL[MS];
+  double bre[MS], bim[MS];
   C2 gk{0.0, 0.0};
   {
     const double2* cin = carry + (size_t)(active ? c : c0) * nc * nitems + item;
 #pragma unroll
-    for (int l = 0; l < MH; ++l) {
-      CL[l] = C2{mt[8 + 2 * l], mt[9 + 2 * l]};
+    for (int ll = 0; ll < MS; ++ll) {
+      const bool on = lb + ll < MH;  // (odd MH: the last half is one pair short)
+      const int l = on ? lb + ll : 0;
+      CL[ll] = on ? C2{mt[8 + 2 * l], mt[9 + 2 * l]} : C2{0.0, 0.0};
+      bre[ll] = 0.0;
+      bim[ll] = 0.0;
+#pragma unroll
+      for (int h = 0; h < SPL; ++h)
+        if (h * MS + ll < MH && hs == h) {
+          bre[ll] = b.re[h * MS + ll];
+          bim[ll] = b.im[h * MS + ll];
+        }
       const double2 r = cin[(size_t)l * nitems], im = cin[(size_t)(MH + l) * nitems];
-      HR[l] = cmul(CL[l], C2{r.x, r.y});
-      HI[l] = cmul(CL[l], C2{im.x, im.y});
+      HR[ll] = cmul(CL[ll], C2{r.x, r.y});
+      HI[ll] = cmul(CL[ll], C2{im.x, im.y});
     }
     const double2 gg = cin[(size_t)(2 * MH) * nitems];
     gk = C2{gg.x, gg.y};
   }
   double E = 0.0;
-  // The next step's particle data and decay row are loaded one step ahead and
-  // its transcendentals computed one step ahead (nothing waits for them;
-  // registers are plentiful at this occupancy).  Forces are staged for kRemSB
-  // steps and summed per group in one pass.
-  double nx = 0.0, ny = 0.0, nq = 0.0, ndz = 0.0;
-  double2 nd[MH];
-  auto fetch = [&](int i) {
+  // Positions, charge and the two z values of the step's dz are loaded TWO
+  // steps ahead and only combined (dz, sincos, e^{-k dz}) one step ahead: a
+  // warp stalls at the first use of a pending load, and this kernel has only
+  // a few warps per SM to hide it (round 1 formed dz and the transcendentals
+  // right after the loads: a quarter of its stall samples waited there).
+  // Decay rows one step ahead.  Forces are staged for kRemSB steps and summed
+  // per group in one pass.
+  double px = 0.0, py = 0.0, pq = 0.0, pz1 = 0.0, pz0 = 0.0;  // step i + 2 (in flight)
+  double2 nd[MS];                                              // step i + 1
+  auto fetch_xyz = [&](int i) {
     const bool live = i < len;
     const int ia = fwd ? i : len - 1 - i;
     const int64_t ag = live ? a0 + ia : 0;
-    nx = live ? __ldg(xs + ag) : 0.0;
-    ny = live ? __ldg(ys + ag) : 0.0;
-    nq = live ? __ldg(qs + ag) : 0.0;
-    ndz = 0.0;
-    if (live) {
-      if (fwd) ndz = ag > 0 ? __ldg(zs + ag) - __ldg(zs + ag - 1) : 0.0;  // (chunk start: carry)
-      else ndz = ag + 1 < n ? __ldg(zs + ag + 1) - __ldg(zs + ag) : 0.0;
-    }
+    // dz = z[hi] - z[lo]: forward (a - 1, a), backward (a, a + 1); 0 at the
+    // ends (the forward chunk start is the carry's, the global end has none)
+    const int64_t hi = fwd ? ag : (ag + 1 < n ? ag + 1 : ag);
+    const int64_t lo = fwd ? (ag > 0 ? ag - 1 : ag) : ag;
+    px = __ldg(xs + ag);
+    py = __ldg(ys + ag);
+    pq = live ? __ldg(qs + ag) : 0.0;
+    pz1 = __ldg(zs + hi);
+    pz0 = __ldg(zs + lo);
+  };
+  auto fetch_d = [&](int i) {
+    const bool live = i < len;
+    const int ia = fwd ? i : len - 1 - i;
+    const int64_t ag = live ? a0 + ia : 0;
     const int64_t drow = live ? (fwd ? ag : ag + 1) : 0;
 #pragma unroll
-    for (int l = 0; l < MH; ++l) nd[l] = __ldg(dtab + drow * MH + l);
+    for (int ll = 0; ll < MS; ++ll)
+      nd[ll] = lb + ll < MH ? __ldg(dtab + drow * MH + lb + ll) : make_double2(0.0, 0.0);
   };
-  double ncs, nsn, ndk;
-  auto trans = [&]() {  // transcendentals of the fetched step
-    ndk = exp_neg(k * ndz);
-    sincos_fast(__dadd_rn(__dmul_rn(kx, nx), __dmul_rn(ky, ny)), &nsn, &ncs);
+  double ncs, nsn, ndk, nq;
+  auto trans = [&]() {  // transcendentals of the step whose data is in p*
+    ndk = exp_neg(k * (pz1 - pz0));
+    sincos_fast(__dadd_rn(__dmul_rn(kx, px), __dmul_rn(ky, py)), &nsn, &ncs);
+    nq = pq;
   };
-  fetch(0);
+  fetch_xyz(0);
+  fetch_d(0);
   trans();
+  fetch_xyz(1);
   double* st = stg[warp];
   for (int i = 0; i < R; ++i) {
     const bool live = i < len;
-    const int ia = fwd ? i : len - 1 - i;
-    const int64_t ag = live ? a0 + ia : 0;
     const double q = nq, cs = ncs, sn = nsn, dk = ndk;
-    double2 dd[MH];
+    double2 dd[MS];
 #pragma unroll
-    for (int l = 0; l < MH; ++l) dd[l] = nd[l];
+    for (int ll = 0; ll < MS; ++ll) dd[ll] = nd[ll];
     if (i + 1 < R) {
-      fetch(i + 1);
+      fetch_d(i + 1);
       trans();
+      fetch_xyz(i + 2);
     }
 #pragma unroll
-    for (int l = 0; l < MH; ++l) {
-      HR[l] = cmul(HR[l], C2{dd[l].x, dd[l].y});
-      HI[l] = cmul(HI[l], C2{dd[l].x, dd[l].y});
+    for (int ll = 0; ll < MS; ++ll) {
+      HR[ll] = cmul(HR[ll], C2{dd[ll].x, dd[ll].y});
+      HI[ll] = cmul(HI[ll], C2{dd[ll].x, dd[ll].y});
     }
     gk.re *= dk;
     gk.im *= dk;
+    // readout sums as two interleaved chains each (dependent-latency bound)
     double sgr = 0.0, sgi = 0.0, sbr = 0.0, sbi = 0.0;
+    double sgr1 = 0.0, sgi1 = 0.0, sbr1 = 0.0, sbi1 = 0.0;
 #pragma unroll
-    for (int l = 0; l < MH; ++l) {
-      sgr += HR[l].re;
-      sgi += HI[l].re;
-      sbr = fma(b.re[l], HR[l].re, fma(-b.im[l], HR[l].im, sbr));
-      sbi = fma(b.re[l], HI[l].re, fma(-b.im[l], HI[l].im, sbi));
+    for (int ll = 0; ll < MS; ll += 2) {
+      sgr += HR[ll].re;
+      sgi += HI[ll].re;
+      sbr = fma(bre[ll], HR[ll].re, fma(-bim[ll], HR[ll].im, sbr));
+      sbi = fma(bre[ll], HI[ll].re, fma(-bim[ll], HI[ll].im, sbi));
+      if (ll + 1 < MS) {
+        sgr1 += HR[ll + 1].re;
+        sgi1 += HI[ll + 1].re;
+        sbr1 = fma(bre[ll + 1], HR[ll + 1].re, fma(-bim[ll + 1], HR[ll + 1].im, sbr1));
+        sbi1 = fma(bre[ll + 1], HI[ll + 1].re, fma(-bim[ll + 1], HI[ll + 1].im, sbi1));
+      }
+    }
+    sgr += sgr1;
+    sgi += sgi1;
+    sbr += sbr1;
+    sbi += sbi1;
+    if constexpr (SPL == 2) {  // the item's other half (lane -+ L), fixed order
+      const int pl = hs ? lane - L : lane + L;
+      const double o0 = __shfl_sync(0xffffffffu, sgr, pl);
+      const double o1 = __shfl_sync(0xffffffffu, sgi, pl);
+      const double o2 = __shfl_sync(0xffffffffu, sbr, pl);
+      const double o3 = __shfl_sync(0xffffffffu, sbi, pl);
+      sgr = hs ? o0 + sgr : sgr + o0;
+      sgi = hs ? o1 + sgi : sgi + o1;
+      sbr = hs ? o2 + sbr : sbr + o2;
+      sbi = hs ? o3 + sbi : sbi + o3;
     }
     const double ps = sigma * sn;
     const double pr = fma(kappa, gk.re, -two_k * sgr);
@@ -1158,7 +1220,7 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
       if (slot == kRemSB - 1 || i == R - 1) {
         __syncwarp();
         // (slot, group, direction, comp) sums in fixed order over the group's
-        // lanes of that direction, forward / backward into frem's two buffers
+        // half-0 lanes of that direction, forward / backward into frem's two buffers
         const int ibase = i - slot;
         const int nd = paired ? 2 : 1;
         for (int e = lane; e < (slot + 1) * G * nd * 3; e += 32) {
@@ -1172,7 +1234,7 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
           if (ii < leng) {
             const double* rs = st + sl * 32 * 3;
             double sum = 0.0;
-            for (int j = 0; j < Ld; ++j) sum += rs[(gg * L + d * Ld + j) * 3 + comp];
+            for (int j = 0; j < Ld; ++j) sum += rs[(gg * LS + d * Ld + j) * 3 + comp];
             const bool dfwd = paired ? d == 0 : true;
             SLAB_BOUND(a0g + (dfwd ? ii : leng - 1 - ii), n);
             frem[(size_t)d * n * 3 + (a0g + (dfwd ? ii : leng - 1 - ii)) * 3 + comp] = sum;
@@ -1184,17 +1246,16 @@ __global__ void __launch_bounds__(32 * kRemWarps, SLAB_REM_MINB) fourier_sweep_r
     const double ur0 = q * cs, ui0 = -sigma * q * sn;
     const double ur = kSwap ? ui0 : ur0, ui = kSwap ? -ur0 : ui0;
 #pragma unroll
-    for (int l = 0; l < MH; ++l) {
-      HR[l].re = fma(CL[l].re, ur, HR[l].re);
-      HR[l].im = fma(CL[l].im, ur, HR[l].im);
-      HI[l].re = fma(CL[l].re, ui, HI[l].re);
-      HI[l].im = fma(CL[l].im, ui, HI[l].im);
+    for (int ll = 0; ll < MS; ++ll) {
+      HR[ll].re = fma(CL[ll].re, ur, HR[ll].re);
+      HR[ll].im = fma(CL[ll].im, ur, HR[ll].im);
+      HI[ll].re = fma(CL[ll].re, ui, HI[ll].re);
+      HI[ll].im = fma(CL[ll].im, ui, HI[ll].im);
     }
     gk.re += ur;
     gk.im += ui;
-    (void)ag;
   }
-  if (active && fwd) epart[(size_t)c * P + t] = E;
+  if (owner && fwd) epart[(size_t)c * P + t] = E;
 }
 
 // per-mode sums over chunks (one block per mode, fixed-order tree), then Kahan
@@ -1266,10 +1327,10 @@ __global__ void __launch_bounds__(kKahanThreads) kahan_modes_kernel(
 // lanes per element take the buffers round robin and combine by a fixed
 // xor-shuffle tree (deterministic).
 template <int NS>
-__global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int nbuf,
-                                            int ngroups, int nwarps, int upg, int units,
-                                            int64_t n3, double* __restrict__ out, int64_t e0,
-                                            int64_t e1) {
+__global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, int b_lo,
+                                            int nbuf, int ngroups, int nwarps, int upg,
+                                            int units, int64_t n3, double* __restrict__ out,
+                                            int64_t e0, int64_t e1) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int sub = (int)(t % NS);
   const int64_t e = e0 + t / NS;
@@ -1283,7 +1344,7 @@ __global__ void fourier_force_reduce_kernel(const double* __restrict__ fpart, in
   // latency-bound at ~45% of HBM bandwidth); the adds keep buffer order
   double v = 0.0;
   if (live) {
-    int b = sub;
+    int b = b_lo + sub;
     for (; b + 3 * NS < nbuf; b += 4 * NS) {
       double x[4];
 #pragma unroll
@@ -1327,15 +1388,22 @@ FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs, int ranks) {
   // several chunks per warp; the main sweep then runs whole warps only
   p.rem = 0;
   p.rem_g = 0;
+  p.rem_spl = 1;
   {
     const int left = units % upw;
     const int left_items = left * (p.paired ? 2 : 1);
     if (kSweepRem && units >= upw && left > 0 && left_items <= kSweepRemMax) {
       p.rem = left_items;
-      p.rem_g = 32 / left_items;
+      // one lane per item; SLAB_REM_SPL=2 splits an item's pairs over two lanes
+      // (from 4 pairs up): twice the warps, but measured slower at cfg4 (the
+      // remainder 0.46 -> 0.65 ms in the tail, step 8.31 -> 8.42 ms)
+      p.rem_spl = 1;
+      if (const char* env = getenv("SLAB_REM_SPL"))
+        p.rem_spl = (atoi(env) == 2 && mh >= 4 && 2 * left_items <= 32) ? 2 : 1;
+      p.rem_g = 32 / (p.rem_spl * left_items);
       if (const char* env = getenv("SLAB_REM_G")) {  // tuning knob
         const int gg = atoi(env);
-        if (gg >= 1 && gg <= 32 / left_items) p.rem_g = gg;
+        if (gg >= 1 && gg <= 32 / (p.rem_spl * left_items)) p.rem_g = gg;
       }
     }
   }
@@ -1541,11 +1609,28 @@ static RemSide& rem_side() {
   return r;
 }
 
+// out[e] += sum of the partial force buffers [b_lo, b_hi) of the plan's chunk
+// range, in buffer order
+static void force_reduce(const FourierPlan& p, const FourierWork& w, int b_hi, int b_lo,
+                         double* out, cudaStream_t st) {
+  const int64_t n3 = p.n * 3;
+  const int64_t e0 = (int64_t)p.c0 * p.R * 3;
+  int64_t e1 = (int64_t)p.c1 * p.R * 3;
+  e1 = e1 < n3 ? e1 : n3;
+  if (e1 <= e0 || b_hi <= b_lo) return;
+  if ((e1 - e0) < (int64_t)148 * 2048 && b_hi - b_lo >= 16)
+    fourier_force_reduce_kernel<8><<<(unsigned)((8 * (e1 - e0) + 255) / 256), 256, 0, st>>>(
+        w.fpart, b_lo, b_hi, p.ngroups, p.warps, p.upg, p.units_main, n3, out, e0, e1);
+  else
+    fourier_force_reduce_kernel<1><<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
+        w.fpart, b_lo, b_hi, p.ngroups, p.warps, p.upg, p.units_main, n3, out, e0, e1);
+}
+
 template <int MH>
 static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const double* xs,
                              const double* ys, const double* zs, const double* qs,
                              const double2* dtab, const BVec& b, int want_forces,
-                             const double2* tin, cudaStream_t st) {
+                             const double2* tin, double* forces_sorted, cudaStream_t st) {
   const int nch_r = p.c1 - p.c0;
   if (nch_r <= 0) return cudaGetLastError();
   // forces need both directions in the paired lane layout (plans with dirs = 2)
@@ -1572,14 +1657,14 @@ static cudaError_t phase2_mh(const FourierPlan& p, const FourierWork& w, const d
     const int rwarps = (nch_r + p.rem_g - 1) / p.rem_g;
     const int rblocks = (rwarps + kRemWarps - 1) / kRemWarps;
     double* frem = w.fpart + (size_t)p.rem_buf * p.n * 3;
-    if (p.swap)
-      fourier_sweep_rem_kernel<MH, true><<<rblocks, 32 * kRemWarps, 0, rs.s>>>(
-          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.units_main, p.rem, p.paired, p.rem_g,
-          b, w.carry, w.epart, frem, want_forces, p.c0, p.c1);
-    else
-      fourier_sweep_rem_kernel<MH, false><<<rblocks, 32 * kRemWarps, 0, rs.s>>>(
-          xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P, p.units_main, p.rem, p.paired, p.rem_g,
-          b, w.carry, w.epart, frem, want_forces, p.c0, p.c1);
+    constexpr int kSpl = MH >= 4 ? 2 : 1;
+    auto fn = p.rem_spl == 2 ? (p.swap ? fourier_sweep_rem_kernel<MH, true, kSpl>
+                                       : fourier_sweep_rem_kernel<MH, false, kSpl>)
+                             : (p.swap ? fourier_sweep_rem_kernel<MH, true, 1>
+                                       : fourier_sweep_rem_kernel<MH, false, 1>);
+    fn<<<rblocks, 32 * kRemWarps, 0, rs.s>>>(xs, ys, zs, qs, dtab, p.n, p.R, w.modetab, p.P,
+                                             p.units_main, p.rem, p.paired, p.rem_g, b, w.carry,
+                                             w.epart, frem, want_forces, p.c0, p.c1);
     cudaEventRecord(rs.join, rs.s);
   }
   if (p.items_main > 0) {
@@ -1640,7 +1725,7 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
   cudaError_t e = cudaErrorInvalidValue;
   switch (p.mh) {
 #define FCASE(K) \
-  case K: e = phase2_mh<K>(p, w, xs, ys, zs, qs, dtab, b, want_forces, tin2, st); break;
+  case K: e = phase2_mh<K>(p, w, xs, ys, zs, qs, dtab, b, want_forces, tin2, forces_sorted, st); break;
     FCASE(1) FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) FCASE(7) FCASE(8) FCASE(9) FCASE(10) FCASE(11)
     FCASE(12)
 #undef FCASE
@@ -1662,20 +1747,9 @@ cudaError_t fourier_phase2(const FourierPlan& p, const FourierWork& w, const dou
                                                   sing ? esing : nullptr, se);
   const int nseg = p.P / seg_len;
   if (nseg > 0) kahan_modes_kernel<<<nseg, kKahanThreads, 0, st>>>(se, nseg, seg_len, energy_out);
-  if (want_forces) {
-    const int64_t n3 = p.n * 3;
-    const int64_t e0 = (int64_t)p.c0 * p.R * 3;
-    int64_t e1 = (int64_t)p.c1 * p.R * 3;
-    e1 = e1 < n3 ? e1 : n3;
-    if (e1 > e0) {
-      if ((e1 - e0) < (int64_t)148 * 2048 && p.nbuf >= 16)
-        fourier_force_reduce_kernel<8><<<(unsigned)((8 * (e1 - e0) + 255) / 256), 256, 0, st>>>(
-            w.fpart, p.nbuf, p.ngroups, p.warps, p.upg, p.units_main, n3, forces_sorted, e0, e1);
-      else
-        fourier_force_reduce_kernel<1><<<(unsigned)((e1 - e0 + 255) / 256), 256, 0, st>>>(
-            w.fpart, p.nbuf, p.ngroups, p.warps, p.upg, p.units_main, n3, forces_sorted, e0, e1);
-    }
-  }
+  // (summing the main sweep's buffers before the remainder's join, beside it in
+  // the scan's tail, measured slower: cfg4 8.31 -> 8.33 ms)
+  if (want_forces) force_reduce(p, w, p.nbuf, 0, forces_sorted, st);
   return cudaGetLastError();
 }
 

@@ -61,7 +61,8 @@ struct FourierPlan {
   int units_main; // modes (paired) / items of the main sweep (whole warps when rem > 0)
   int items_main; // items of the main sweep
   int rem;        // leftover items per chunk run by the remainder sweep (0: none)
-  int rem_g;      // chunks per remainder warp (32 / rem)
+  int rem_g;      // chunks per remainder warp (32 / (rem_spl rem))
+  int rem_spl;    // lanes per remainder item (2: its pairs split over two lanes)
   int rem_buf;    // the remainder's partial force buffer
 };
 FourierPlan fourier_plan(int64_t n, int P, int mh, int dirs = 2, int ranks = 1);

@@ -201,12 +201,28 @@ __global__ void zero_sweep_kernel(const double* __restrict__ zs, const double* _
   }
   double S0 = cin[2 * MH].x, S1 = cin[2 * MH].y;
   double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-  for (int64_t s = 0; s < a1 - a0; ++s) {
-    const int64_t a = dir == 0 ? a0 + s : a1 - 1 - s;
+  // the next step's charge and z values are loaded one step ahead (this kernel
+  // runs a few warps per SM, mostly in the scan's tail; the decay rows stay
+  // in-step: prefetching them too spills)
+  const int64_t len = a1 - a0;
+  double nq, nz, nz1, nz0;
+  auto fetch = [&](int64_t s) {
+    const int64_t ss = s < len ? s : len - 1;
+    const int64_t a = dir == 0 ? a0 + ss : a1 - 1 - ss;
     const int64_t ad = dir == 0 ? a : a + 1;  // decay row d_a (fwd) / d_{a+1} (bwd)
-    const double q = qs[a], z = zs[a];
+    const int64_t adc = ad > 0 && ad < n ? ad : 1;
+    nq = qs[a];
+    nz = zs[a];
+    nz1 = zs[adc];
+    nz0 = zs[adc - 1];
+  };
+  fetch(0);
+  for (int64_t s = 0; s < len; ++s) {
+    const int64_t a = dir == 0 ? a0 + s : a1 - 1 - s;
+    const int64_t ad = dir == 0 ? a : a + 1;
+    const double q = nq, z = nz, dz = nz1 - nz0;
+    fetch(s + 1);
     if (ad > 0 && ad < n) {
-      const double dz = zs[ad] - zs[ad - 1];
 #pragma unroll
       for (int l = 0; l < MH; ++l) {
         const double2 d = dtab[ad * MH + l];
@@ -325,8 +341,11 @@ ZeroPlan zero_plan(int64_t n, int mh) {
   ZeroPlan p{};
   p.n = n;
   p.mh = mh;
+#ifndef SLAB_ZERO_RMAX
+#define SLAB_ZERO_RMAX 128
+#endif
   int R = 32;
-  while (R * 2 <= 128 && (int64_t)R * 2 * 8192 <= n) R *= 2;
+  while (R * 2 <= SLAB_ZERO_RMAX && (int64_t)R * 2 * 8192 <= n) R *= 2;
   p.R = R;
   p.nch = (int)((n + R - 1) / R);
   return p;

@@ -2,7 +2,10 @@
 start / end of every kernel relative to the step's first kernel, its stream,
 and the idle gaps on the union of streams -- what sits on the critical path.
 
-    python tools/timeline.py [config]
+    python tools/timeline.py [config] [W rank]
+
+With W and rank: that rank's share of a W-way sharded evaluation
+(SHARD_MODE=modes|zsplit, the collectives skipped -- one GPU).
 """
 import json
 import os
@@ -17,10 +20,18 @@ from paper_2403_01521_b200.configs import make_workload  # noqa: E402
 from paper_2403_01521_b200.engine import DeviceEvaluator  # noqa: E402
 
 
-def main(name="cfg4"):
+def main(name="cfg4", W=1, rank=0):
     wl = make_workload(name)
     soe = pk.build_soe_contour(wl.m)
-    ev = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, P=wl.P, seed=wl.seed)
+    if W > 1:
+        ev = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, P=wl.P, seed=wl.seed,
+                             rank=rank, world=W,
+                             shard_mode=os.environ.get("SHARD_MODE", "modes"))
+        ev.reduce = False
+        ev.exchange = lambda local, gathered: None
+        ev.warmup()
+    else:
+        ev = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, P=wl.P, seed=wl.seed)
     for _ in range(3):
         ev.step()
     torch.cuda.synchronize()
@@ -53,4 +64,5 @@ def main(name="cfg4"):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["cfg4"]))
+    a = sys.argv[1:]
+    main(a[0] if a else "cfg4", int(a[1]) if len(a) > 1 else 1, int(a[2]) if len(a) > 2 else 0)
