@@ -671,6 +671,19 @@ constexpr bool kSplitShort = SLAB_SPLIT_SHORT;
 #endif
 constexpr bool kParZero = SLAB_PAR_ZERO;
 
+// A caller's timing event: inside a stream capture it must be an EXTERNAL
+// record node (a plain record there only orders captured work), so that a
+// replayed graph stamps it -- the scan span is then timed inside the same
+// graph the bench replays.
+static cudaError_t record_timing_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs == cudaStreamCaptureStatusActive)
+    return cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  return cudaEventRecord(ev, s);
+}
+
 static int ensure_fork(SlabCtx* ctx) {
   if (ctx->hi) return SLAB_OK;
   int least = 0, greatest = 0;
@@ -869,7 +882,7 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     ctx->zs_perm = perm;
     if (fork_sort && !split_short)  // scan after the short range
       CK(cudaStreamWaitEvent(sl, ctx->ev_short, 0));
-    if (a->ev_scan_begin) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_begin, sl));
+    if (a->ev_scan_begin) CK(record_timing_event((cudaEvent_t)a->ev_scan_begin, sl));
     if (n >= 2) {
       if (zsplit && !lead)  // rows of this rank's chunk range only (no k = 0 mode here)
         CK(slab::decay_table(w.zs, n, sh.mh, sh.b, w.dtab, sl, (int64_t)fp.c0 * fp.R,
@@ -933,7 +946,7 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
                           w.fzf, w.fzb, u_pair, sl));
     if (par_zero) CK(cudaStreamWaitEvent(sl, ctx->ev_zero, 0));
   }
-  if (a->ev_scan_end) CK(cudaEventRecord((cudaEvent_t)a->ev_scan_end, sl));
+  if (a->ev_scan_end) CK(record_timing_event((cudaEvent_t)a->ev_scan_end, sl));
   if (split_short) {  // enqueued after the scan chain so the pair kernel can wait on its end
     CK(cudaEventRecord(ctx->ev_long, sl));
     if (pos_ready) CK(cudaStreamWaitEvent(ctx->lo, pos_ready, 0));

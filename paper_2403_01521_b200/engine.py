@@ -498,8 +498,11 @@ class DeviceEvaluator:
             if not self.eng.handle_overflow(self.status()):
                 return
 
-    def capture(self):
-        """Record one step as a CUDA graph (single GPU; small systems are launch bound)."""
+    def capture(self, scan_events=None):
+        """Record one step as a CUDA graph (single GPU; small systems are launch bound).
+        With ``scan_events`` (a pair of timing events) the graph stamps them around
+        the SOE scan on every replay and is returned without replacing the step's
+        own graph (bench.py times the scan span inside the replayed step)."""
         torch = _torch()
         if self.world > 1:
             raise RuntimeError("graph capture is single-GPU only")
@@ -511,8 +514,9 @@ class DeviceEvaluator:
         torch.cuda.synchronize(self.eng.device)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self._enqueue()
-        self.graph = g
+            self._enqueue(scan_events)
+        if scan_events is None:
+            self.graph = g
         return g
 
     def step(self, scan_events=None):
