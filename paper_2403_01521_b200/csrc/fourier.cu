@@ -336,7 +336,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 __host__ __device__ constexpr int mma_mhp(int mh) { return (mh + 3) / 4 * 4; }
 static size_t agg_mma_smem(int R, int mh) {
   return sizeof(double) * ((size_t)4 * mma_mhp(mh) * (R + 4) + 4 * (size_t)R +
-                           3 * 32 * (size_t)SLAB_AGG_MMA_MAXW);
+                           4 * 32 * (size_t)SLAB_AGG_MMA_MAXW);
 }
 
 #ifndef SLAB_AGG_RCP
@@ -436,13 +436,19 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
   double gfr = 0.0, gfi = 0.0, gbr = 0.0, gbi = 0.0;
   const double* wk = wt + nn * RP + kk;
   const double span = z_end - z_start;
-  const bool span_ok = k * span < 600.0;
-  const double ekspan = exp_neg(k * span);
+  // e^{-k span} per lane in shared memory too (0 when k span >= 600: the
+  // reciprocal form's guard); re-read at each use, registers being the limit
+  sk[3 * blockDim.x + threadIdx.x] = k * span < 600.0 ? exp_neg(k * span) : 0.0;
+  __syncwarp();
   const double* skl = sk + threadIdx.x;
+  // (the lane's particle bound folded with the mode's validity into one
+  // loop-invariant: the round-1 form spilled j and reloaded it from local
+  // memory at every iteration)
+  const int jend = tv ? len : 0;
   for (int k0 = 0; k0 < len; k0 += 4) {
     const int j = k0 + kk;
     double ur = 0.0, ui = 0.0;
-    if (tv && j < len) {
+    if (j < jend) {
       const double th = __dadd_rn(__dmul_rn(lds_volatile(skl), sx[j]),
                                   __dmul_rn(lds_volatile(skl + blockDim.x), sy[j]));
       double sn, cs;
@@ -456,6 +462,8 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
       // (Newton reciprocal vs IEEE division: register allocation decides --
       // measured 1.18 -> 1.10 ms for 8 pairs, 0.36 -> 0.39 ms for 12)
       double wb;
+      const double ekspan = lds_volatile(skl + 3 * blockDim.x);
+      const bool span_ok = ekspan != 0.0;
       if constexpr (kAggRcp && MH <= 8)
         wb = span_ok ? ekspan * rcp_normal(wf) : exp_neg_cb(kj * (span - ze));
       else

@@ -514,11 +514,16 @@ __device__ __forceinline__ double4 ld_rec(const double4* p) {  // one 256-bit lo
 // SPLIT consecutive lanes share a home, taking its row's 4-entry blocks round
 // robin, and combine their partial forces with a fixed xor-shuffle tree
 // (deterministic).
+#ifndef SLAB_PAIR_PFIDX
+#define SLAB_PAIR_PFIDX 1
+#endif
 #ifndef SLAB_PAIR_CTAS
 // resident CTAs per SM the pair kernel is compiled and gridded for (cfg4, 24-row
 // erfcx table: 5 -> 1.95 ms; 6 / 7 / 8 cap the registers at 80 / 72 / 64 and
-// spill: 2.08 / 1.99 / 2.19 ms)
-#define SLAB_PAIR_CTAS 5
+// spill: 2.08 / 1.99 / 2.19 ms).  Round 2, with the row entries loaded one block
+// ahead (SLAB_PAIR_PFIDX): 4 -> 1.91 ms (5: 2.00, 3: 2.02; without the
+// prefetch 4: 1.95; all 8 records loaded before the first term: 2.02 / 2.04)
+#define SLAB_PAIR_CTAS 4
 #endif
 constexpr int kPairCtas = SLAB_PAIR_CTAS;
 template <int KIND, int SPLIT>
@@ -566,8 +571,20 @@ __global__ void __launch_bounds__(kSRThreads, kPairCtas) pair_list_kernel(
     // multiple of 8) and one 256-bit load per neighbour record: half the L1
     // requests of 128-bit loads on this L1-bound kernel
     int k = 8 * sub;
+#if SLAB_PAIR_PFIDX
+    // the next block's 8 row entries are loaded one block ahead: the record
+    // addresses no longer wait on the row load (round 2: 10% of this kernel's
+    // stall samples sat on that dependency)
+    Idx8 jn{};
+    if (k + 8 <= cnt) jn = *reinterpret_cast<const Idx8*>(row + k);
+#endif
     for (; k + 8 <= cnt; k += 8 * SPLIT) {
+#if SLAB_PAIR_PFIDX
+      const Idx8 j8 = jn;
+      if (k + 8 * SPLIT + 8 <= cnt) jn = *reinterpret_cast<const Idx8*>(row + k + 8 * SPLIT);
+#else
       const Idx8 j8 = *reinterpret_cast<const Idx8*>(row + k);
+#endif
       {
         const double4 p0 = ld_rec(cp + j8.a0), p1 = ld_rec(cp + j8.a1), p2 = ld_rec(cp + j8.a2),
                       p3 = ld_rec(cp + j8.a3);
