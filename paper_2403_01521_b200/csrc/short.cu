@@ -301,7 +301,9 @@ __global__ void __launch_bounds__(kSRThreads) nbr_build_kernel(
       const int b1 = start[col + zhi + 1];
       int jj = start[col + zlo];
       // (scanning the warp-union of the lanes' ranges instead -- broadcast
-      // loads, no idle lanes -- measured 1.51 ms against 1.13 ms per lane)
+      // loads, no idle lanes -- measured 1.51 ms against 1.13 ms per lane;
+      // round 2: loading the next 4 candidates before testing the current 4,
+      // 1.08 -> 1.15 ms -- this loop is issue-bound, not latency-bound)
 #if SLAB_NBR_WIDE
       // two candidates per 256-bit load (32-byte aligned pairs): half the L1
       // requests of this L1-throughput-bound screen
