@@ -866,10 +866,11 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
     if (!a->skip_short_range && !split_short) {
       cudaStream_t ss = fork ? ctx->lo : st;
       if (pos_ready) CK(cudaStreamWaitEvent(ss, pos_ready, 0));
-      if (charge_ready) CK(cudaStreamWaitEvent(ss, charge_ready, 0));
+      // (charges: waited for inside, before the first kernel that reads them)
       const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
       CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
-                         a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, ss));
+                         a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, ss, 0, 0.0, 0.0,
+                         0, nullptr, charge_ready));
       if (fork) CK(cudaEventRecord(ctx->ev_short, ctx->lo));
     }
     if (pos_ready) CK(cudaStreamWaitEvent(sl, pos_ready, 0));
@@ -950,11 +951,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
   if (split_short) {  // enqueued after the scan chain so the pair kernel can wait on its end
     CK(cudaEventRecord(ctx->ev_long, sl));
     if (pos_ready) CK(cudaStreamWaitEvent(ctx->lo, pos_ready, 0));
-    if (charge_ready) CK(cudaStreamWaitEvent(ctx->lo, charge_ready, 0));
     const int64_t h0 = home_bound(n, srank, scount), h1 = home_bound(n, srank + 1, scount);
     CK(slab::short_run(sp, swork, a->d_pos, a->d_charge, box.lx, box.ly, box.lz, a->alpha,
                        a->r_c, fshort, u_s, ctx->status, h0, h1, ctx->d_maxnn, ctx->lo, 0, 0.0,
-                       0.0, 0, ctx->ev_long));
+                       0.0, 0, ctx->ev_long, charge_ready));
     CK(cudaEventRecord(ctx->ev_short, ctx->lo));
   }
   if (fork) {  // join

@@ -158,7 +158,8 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
                       int* maxnn_out, cudaStream_t st, int kind = 0, double lj_eps = 0.0,
                       double lj_sigma = 0.0,  // kind 1: WCA core instead of erfc Coulomb
                       int accumulate = 0,     // 1: forces += (full home range only)
-                      cudaEvent_t pairs_after = nullptr);  // pair kernel waits on it
+                      cudaEvent_t pairs_after = nullptr,   // pair kernel waits on it
+                      cudaEvent_t charge_ready = nullptr);  // charges read from here on
 
 // ---------------------------------------------------------------- md.cu
 int64_t md_partials(int64_t n);

@@ -953,7 +953,8 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
                       double lx, double ly, double lz, double alpha, double rc, double* forces,
                       double* energy_out, int* status, int64_t h0, int64_t h1,
                       int* maxnn_out, cudaStream_t st, int kind, double lj_eps,
-                      double lj_sigma, int accumulate, cudaEvent_t pairs_after) {
+                      double lj_sigma, int accumulate, cudaEvent_t pairs_after,
+                      cudaEvent_t charge_ready) {
   const int64_t n = p.n;
   const double sig2 = lj_sigma * lj_sigma;
   if (n < 2 || h1 <= h0) {
@@ -970,7 +971,10 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
   double* eblk = reinterpret_cast<double*>(w);
   w += align256(sizeof(double) * (p.nblk + kOvfBlocks));
   const double rc2 = rc * rc;
+  // the cell search needs positions only: a host-buffer caller's charges may
+  // still be landing (they are first read by the gather / brute kernel)
   if (p.brute) {
+    if (charge_ready) cudaStreamWaitEvent(st, charge_ready, 0);
     double* fbuf = reinterpret_cast<double*>(w);
     const unsigned nbx = (unsigned)((nh + 127) / 128);
     if (partial) cudaMemsetAsync(fbuf, 0, sizeof(double) * 3 * n * p.jsplit, st);
@@ -1012,6 +1016,7 @@ cudaError_t short_run(const ShortPlan& p, void* work, const double* pos, const d
     if (e != cudaSuccess) return e;
     cell_start_kernel<<<(unsigned)((p.ncell + 1 + 255) / 256), 256, 0, st>>>(skey, n, p.ncell,
                                                                              start);
+    if (charge_ready) cudaStreamWaitEvent(st, charge_ready, 0);
     cell_gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pos, charge, order, n, lx,
                                                                     ly, cp, cpf);
     void* twork = w;  // home-order work (tile_work_bytes)
