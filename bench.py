@@ -416,7 +416,9 @@ def run_ours(args, rank, world, local):
     # one GPU: the step replayed as a CUDA graph (all sizes since round 2: at cfg4
     # the ~470 launches' gaps cost 0.14 ms of 8.5 ms eagerly); the scan span is
     # then timed inside the same graph, with its events as record nodes (below)
-    use_graph = world == 1
+    # (round 2: at N > 1 too -- each rank's local parts are graphs, the
+    # collectives run between their replays)
+    use_graph = True
     ev.warmup()  # workspace + short-range neighbour capacity (may rerun once)
     for _ in range(args.warmup):
         ev.step()
@@ -455,6 +457,11 @@ def run_ours(args, rank, world, local):
     clk = clocks.stop()
     scan_ms = None
     if not use_graph:
+        scan_ms = sum(a.elapsed_time(b) for a, b in scan_ev) / K
+    elif world > 1:  # the scan's events on eager steps (they hold collectives)
+        for a, b in scan_ev:
+            ev.step(scan_events=(a, b))
+        torch.cuda.synchronize()
         scan_ms = sum(a.elapsed_time(b) for a, b in scan_ev) / K
     else:  # graph replay: the same step captured with the scan's events inside
         # it (external record nodes), replayed K times after the timed region

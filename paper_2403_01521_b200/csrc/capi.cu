@@ -832,15 +832,14 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
 
   // Fork: the short range runs on ctx->lo (lowest priority) concurrently with
   // the sort / Fourier / k = 0 chain on ctx->hi (highest priority); both join
-  // back into `st` before the assembly.  (A z-split phase 1 returns with the
-  // short range possibly still running; phase 2 joins it.)
+  // back into `st` before the assembly.  (A z-split phase 1 joins its short
+  // range before returning: each phase is capturable as its own graph.)
   const bool fork_all = !a->skip_short_range && n > 0 && (n <= kForkMaxN || (host_entry && kForkHost));
   // Large systems on device buffers: only the z sort + gather run beside the
   // short range (latency-bound passes that barely compete with it); the scan
   // waits for the short range, so its kernels keep the GPU to themselves.
-  // (Also for the two z-split phases: phase 1 forks, phase 2 joins; round 1
-  // ran a z-split rank's sort after its short range, 0.26 ms of a 1.8 ms rank
-  // step at W = 8.)
+  // (Also in z-split phase 1; round 1 ran a z-split rank's sort after its
+  // short range, 0.26 ms of a 1.8 ms rank step at W = 8.)
   const bool fork_sort = kForkSort && !fork_all && !a->skip_short_range && n > 0;
   const bool fork = fork_all || fork_sort;
   // ... and with SLAB_SPLIT_SHORT the neighbour screen (no fp64 work) also runs
@@ -911,6 +910,11 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
       if (fork) {
         CK(cudaEventRecord(ctx->ev_long, sl));
         CK(cudaStreamWaitEvent(st, ctx->ev_long, 0));
+        // the short range is joined here too, so that each phase is
+        // self-contained (a rank captures the two phases as separate CUDA
+        // graphs around the exchange; with the sort fork the scan waited for
+        // it already)
+        if (!a->skip_short_range && !split_short) CK(cudaStreamWaitEvent(st, ctx->ev_short, 0));
       }
       return SLAB_OK;
     }
@@ -957,10 +961,10 @@ static int evaluate_impl(SlabCtx* ctx, const SlabEvalArgs* a, cudaStream_t st,
                        0.0, 0, ctx->ev_long, charge_ready));
     CK(cudaEventRecord(ctx->ev_short, ctx->lo));
   }
-  if (fork) {  // join
+  if (fork) {  // join (a phase 2 joined its short range at the end of phase 1)
     CK(cudaEventRecord(ctx->ev_long, sl));
     CK(cudaStreamWaitEvent(st, ctx->ev_long, 0));
-    CK(cudaStreamWaitEvent(st, ctx->ev_short, 0));
+    if (a->phase != 2 || split_short) CK(cudaStreamWaitEvent(st, ctx->ev_short, 0));
   }
   if (forces) {
     const double plane = lead ? box.sigma_top - box.sigma_bot : 0.0;

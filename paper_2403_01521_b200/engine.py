@@ -380,6 +380,7 @@ class DeviceEvaluator:
         self.forces = self.packed[:3 * self.n].view(self.n, 3)
         self.energy = self.packed[3 * self.n:]
         self.graph = None
+        self.graphs = []
         Q = float(np.sum(system.charge ** 2))
         if P is None:  # deterministic full mode sum (soe_energy_forces)
             self.P = params.kmodes.shape[0]
@@ -428,10 +429,13 @@ class DeviceEvaluator:
         self.pos.copy_(pos if hasattr(pos, "device") else
                        _torch().as_tensor(np.asarray(pos, dtype=np.float64)))
 
-    def _enqueue(self, scan_events=None):
+    def _enqueue_part(self, part, scan_events=None):
+        """One rank's local work of a step: ``part`` "all" (single GPU or the
+        "modes" split), "p1" / "p2" (the z-split phases around the exchange).
+        No collective in here, so each part can be captured as a CUDA graph."""
         torch = _torch()
         ready = None
-        if self.sample:
+        if self.sample and part != "p2":
             # after everything queued so far (the previous step still reads the
             # k-set buffer), concurrently with this step's sort
             self.side.wait_stream(torch.cuda.current_stream(self.eng.device))
@@ -446,13 +450,21 @@ class DeviceEvaluator:
                 cv, self.charge_const)
         kw = dict(forces=self.forces, energy=self.energy, soe_pack=self.pack,
                   shard=(self.rank, self.world), scan_events=scan_events)
-        if self.zsplit:
+        if part == "p1":
             self.eng.evaluate(*args, shard_mode=1, phase=1, xchg=self.xloc, modes_ready=ready,
                               **kw)
-            self.exchange(self.xloc, self.xall)
+        elif part == "p2":
             self.eng.evaluate(*args, shard_mode=1, phase=2, xchg=self.xall, **kw)
         else:
             self.eng.evaluate(*args, modes_ready=ready, **kw)
+
+    def _enqueue(self, scan_events=None):
+        if self.zsplit:
+            self._enqueue_part("p1", scan_events)
+            self.exchange(self.xloc, self.xall)
+            self._enqueue_part("p2", scan_events)
+        else:
+            self._enqueue_part("all", scan_events)
         if self.reduce:
             self.all_reduce(self.packed)
 
@@ -499,29 +511,48 @@ class DeviceEvaluator:
                 return
 
     def capture(self, scan_events=None):
-        """Record one step as a CUDA graph (single GPU; small systems are launch bound).
-        With ``scan_events`` (a pair of timing events) the graph stamps them around
-        the SOE scan on every replay and is returned without replacing the step's
-        own graph (bench.py times the scan span inside the replayed step)."""
+        """Record one step as a CUDA graph (small systems are launch bound).
+        With ``scan_events`` (a pair of timing events, single GPU) the graph
+        stamps them around the SOE scan on every replay and is returned without
+        replacing the step's own graph (bench.py times the scan span inside the
+        replayed step).  Multi-GPU: each rank's local parts are captured (the
+        z-split phases as two graphs) and the collectives stay outside them, run
+        between the replays by ``step``."""
         torch = _torch()
-        if self.world > 1:
-            raise RuntimeError("graph capture is single-GPU only")
+        if self.world > 1 and scan_events is not None:
+            raise RuntimeError("scan-event graphs are single-GPU only")
         s = torch.cuda.Stream(self.eng.device)
         s.wait_stream(torch.cuda.current_stream(self.eng.device))
         with torch.cuda.stream(s):
             self.warmup()  # outside capture: workspace, func attributes
         torch.cuda.current_stream(self.eng.device).wait_stream(s)
         torch.cuda.synchronize(self.eng.device)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._enqueue(scan_events)
+        parts = ("p1", "p2") if self.zsplit else ("all",)
+        graphs = []
+        for part in parts:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                if self.world > 1:
+                    self._enqueue_part(part)
+                else:
+                    self._enqueue(scan_events)
+            graphs.append(g)
         if scan_events is None:
-            self.graph = g
-        return g
+            self.graph = graphs[0]
+            self.graphs = graphs
+        return graphs[0]
 
     def step(self, scan_events=None):
         if self.graph is not None and scan_events is None:
-            self.graph.replay()
+            if self.world == 1:
+                self.graph.replay()
+            else:
+                self.graphs[0].replay()
+                if self.zsplit:
+                    self.exchange(self.xloc, self.xall)
+                    self.graphs[1].replay()
+                if self.reduce:
+                    self.all_reduce(self.packed)
         else:
             self._enqueue(scan_events)
         return self.energy, self.forces

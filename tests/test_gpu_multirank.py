@@ -28,7 +28,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, mode, out):
+def _worker(rank, world, port, name, mode, out, graph=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -44,6 +44,8 @@ def _worker(rank, world, port, name, mode, out):
                          c_q=float(g["c_q"]), modes=g["modes"], sample=False, rank=rank,
                          world=world, group=dist.group.WORLD, shard_mode=mode)
     ev.warmup()
+    if graph:  # the rank's local parts as CUDA graphs, collectives between replays
+        ev.capture()
     e, f = ev.step()
     torch.cuda.synchronize()
     if rank == 0:
@@ -52,14 +54,15 @@ def _worker(rank, world, port, name, mode, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("mode", ["modes", "zsplit"])
 @pytest.mark.parametrize("name", ["small_2000", "cfg4"])
-def test_two_rank_device_evaluator_matches_reference(tmp_path, name, mode):
+def test_two_rank_device_evaluator_matches_reference(tmp_path, name, mode, graph):
     import torch.multiprocessing as mp
     g = load_golden(name)
     out = str(tmp_path / "rank0.npz")
-    mp.start_processes(_worker, args=(2, _free_port(), name, mode, out), nprocs=2, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker, args=(2, _free_port(), name, mode, out, graph), nprocs=2,
+                       join=True, start_method="spawn")
     r = np.load(out)
     e, f = r["energy"], r["forces"]
     assert int(r["status"]) == 0

@@ -3,7 +3,7 @@
     python tools/shard_step.py [config] [W]
 
 Times DeviceEvaluator(rank=0..W-1, world=W).step() with the all-reduce disabled for each rank
-in turn -- the per-GPU work of the multi-GPU run without the NCCL all-reduce
+in turn, its local parts replayed as CUDA graphs like bench.py does (SHARD_GRAPH=0: eager) -- the per-GPU work of the multi-GPU run without the NCCL all-reduce
 (the driver's scaling run measures the real thing)."""
 import sys
 
@@ -17,6 +17,7 @@ from paper_2403_01521_b200.configs import make_workload  # noqa: E402
 from paper_2403_01521_b200.engine import DeviceEvaluator  # noqa: E402
 
 MODE = os.environ.get("SHARD_MODE", "zsplit")
+GRAPH = os.environ.get("SHARD_GRAPH", "1") == "1"  # the rank's parts replayed as CUDA graphs
 
 
 def main():
@@ -31,6 +32,8 @@ def main():
         ev.reduce = False  # one GPU: time the rank's own work only
         ev.exchange = lambda local, gathered: None  # (results meaningless; timing only)
         ev.warmup()
+        if GRAPH:
+            ev.capture()
         for _ in range(2):
             ev.step()
         torch.cuda.synchronize()
