@@ -1231,10 +1231,12 @@ __global__ void __launch_bounds__(32 * kRemWarps, SPL == 2 ? (MH <= 8 ? kRemMinB
         // half-0 lanes of that direction, forward / backward into frem's two buffers
         const int ibase = i - slot;
         const int nd = paired ? 2 : 1;
-        for (int e = lane; e < (slot + 1) * G * nd * 3; e += 32) {
-          const int sl = e / (3 * nd * G), rem = e - sl * 3 * nd * G, gd = rem / 3,
-                    comp = rem - 3 * gd;
-          const int gg = gd / nd, d = gd - nd * gg;
+        // one slot at a time, lanes over its (group, direction, comp) entries:
+        // no run-time integer divisions
+        for (int sl = 0; sl <= slot; ++sl)
+        for (int e = lane; e < G * nd * 3; e += 32) {
+          const int gd = e / 3, comp = e - 3 * gd;
+          const int gg = paired ? gd >> 1 : gd, d = paired ? gd & 1 : 0;
           const int cg = c0 + wg * G + gg;
           const int64_t a0g = (int64_t)cg * R;
           const int leng = cg < c1 ? (int)(a0g + R < n ? R : n - a0g) : 0;
