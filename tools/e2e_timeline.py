@@ -2,7 +2,7 @@
 with page-locked host arrays: where the end-to-end time beyond the device step
 goes.
 
-    python tools/e2e_timeline.py [config]
+    python tools/e2e_timeline.py [config] [--pageable]
 """
 import json
 import os
@@ -26,8 +26,9 @@ def main(name="cfg4"):
     H = rbse2d.normalization_H(wl.alpha, wl.box)
     c_q = rbse2d.charge_term_sum(wl.alpha, wl.box, float(np.sum(wl.system.charge ** 2)))
     s = pk.make_system(wl.system.charge, wl.system.mass, wl.system.pos, box=wl.box)
-    s.pos = pinned_like(wl.system.pos)
-    s.charge = pinned_like(wl.system.charge)
+    if "--pageable" not in sys.argv:
+        s.pos = pinned_like(wl.system.pos)
+        s.charge = pinned_like(wl.system.charge)
     smp = rbse2d.ModeSampler(wl.alpha, wl.box, seed=wl.seed)
     for _ in range(3):
         pk.rb_energy_forces(s, wl.box, params, soe, smp, wl.P, H=H, c_q=c_q)
@@ -61,4 +62,4 @@ def main(name="cfg4"):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["cfg4"]))
+    main(*([a for a in sys.argv[1:2] if not a.startswith("--")] or ["cfg4"]))
