@@ -429,6 +429,41 @@ def test_graph_replay_and_shard_sum_equal_single_eval(pk):
     np.testing.assert_allclose(f, g["forces"], rtol=0, atol=1e-9 * float(g["fmax"]))
 
 
+def test_scan_event_graph_times_the_scan_and_matches_the_step(pk):
+    """bench.py's roofline graph: the step captured with the scan's timing events
+    as external record nodes stamps a positive scan span on every replay, inside
+    the full step, and computes the same bits as the step's own graph."""
+    import torch
+    from paper_2403_01521_b200.configs import make_workload
+    from paper_2403_01521_b200.engine import DeviceEvaluator
+    wl = make_workload("small_2000")
+    soe = pk.build_soe_contour(wl.m)
+    g = load_golden("small_2000")
+    ev = DeviceEvaluator(wl.system, wl.box, wl.params(), soe, P=wl.P, H=float(g["H"]),
+                         c_q=float(g["c_q"]), modes=g["modes"])
+    ev.capture()
+    ev.step()
+    torch.cuda.synchronize()
+    e1, f1 = ev.energy.clone(), ev.forces.clone()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()  # materialise the cudaEvent_t handles (torch creates them lazily)
+    b.record()
+    torch.cuda.synchronize()
+    gt = ev.capture(scan_events=(a, b))
+    assert ev.graph is not gt  # the step's own graph is kept
+    spans = []
+    for _ in range(3):
+        s.record()
+        gt.replay()
+        t.record()
+        torch.cuda.synchronize()
+        spans.append((a.elapsed_time(b), s.elapsed_time(t)))
+    for scan, step in spans:
+        assert 0.0 < scan <= step
+    assert torch.equal(e1, ev.energy) and torch.equal(f1, ev.forces)
+
+
 def test_run_many_batches_matches_per_batch_estimates(pk):
     """Batched forward-sweep energies (slab_batch_energies, several device passes)
     equal one rb_energy_estimate per batch plus the deterministic terms.  Like the
