@@ -336,7 +336,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 __host__ __device__ constexpr int mma_mhp(int mh) { return (mh + 3) / 4 * 4; }
 static size_t agg_mma_smem(int R, int mh) {
   return sizeof(double) * ((size_t)4 * mma_mhp(mh) * (R + 4) + 4 * (size_t)R +
-                           4 * 32 * (size_t)SLAB_AGG_MMA_MAXW);
+                           4 * 32 * (size_t)SLAB_AGG_MMA_MAXW + 32);
 }
 
 #ifndef SLAB_AGG_RCP
@@ -396,23 +396,40 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
     sz[i] = z_end - zs[a0 + i];
     sq[i] = qs[a0 + i];
   }
-  // weights, column (dir * MHP + l) * 2 + e
-  for (int e = threadIdx.x; e < R * MHP * 2; e += blockDim.x) {
-    const int j = e % R, rest = e / R;
-    const int l = rest % MHP, dir = rest / MHP;
-    double wr = 0.0, wi = 0.0;
+  // weights, column (dir * MHP + l) * 2 + e: W^b_j = e^{-b (z_j - z_start)} and
+  // W^f_j = e^{-b (z_end - z_j)} of one particle together, the forward phase by
+  // angle subtraction from the chunk's b.im * span (one sincos per (j, l)
+  // instead of two)
+  double* sspan = sk + 4 * 32 * kAggMaxWarps;  // (cos, sin) of b.im * span per pair
+  const double span_w = z_end - z_start;
+  if (threadIdx.x < MHP) {
+    double sn = 0.0, cs = 1.0;
+    if (threadIdx.x < MH) sincos_fast_cb(b.im[threadIdx.x] * span_w, &sn, &cs);
+    sspan[2 * threadIdx.x] = cs;
+    sspan[2 * threadIdx.x + 1] = sn;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * MHP; e += blockDim.x) {
+    const int j = e % R, l = e / R;
+    double fr = 0.0, fi = 0.0, br = 0.0, bi = 0.0;
     if (j < len && l < MH) {
       const double z = zs[a0 + j];
-      const double dist = dir == 0 ? z_end - z : z - z_start;
-      const double e = exp_neg_cb(b.re[l] * dist);
-      double sn, cs;
-      sincos_fast_cb(b.im[l] * dist, &sn, &cs);
-      wr = e * cs;
-      wi = -e * sn;
+      const double db = z - z_start, df = z_end - z;
+      const double eb = exp_neg_cb(b.re[l] * db), ef = exp_neg_cb(b.re[l] * df);
+      double snb, csb;
+      sincos_fast_cb(b.im[l] * db, &snb, &csb);
+      const double css = sspan[2 * l], sns = sspan[2 * l + 1];
+      const double csf = fma(css, csb, sns * snb), snf = fma(sns, csb, -css * snb);
+      fr = ef * csf;
+      fi = -ef * snf;
+      br = eb * csb;
+      bi = -eb * snb;
     }
-    const int col = (dir * MHP + l) * 2;
-    wt[col * RP + j] = wr;
-    wt[(col + 1) * RP + j] = wi;
+    const int cf = l * 2, cb = (MHP + l) * 2;
+    wt[cf * RP + j] = fr;
+    wt[(cf + 1) * RP + j] = fi;
+    wt[cb * RP + j] = br;
+    wt[(cb + 1) * RP + j] = bi;
   }
   __syncthreads();
 
