@@ -95,20 +95,25 @@ __host__ __device__ inline int ncomp_of(int mh) { return 2 * mh + 1; }
 // k-independent tables
 // ---------------------------------------------------------------------------
 // dtab[a*mh + l] = exp(-b_l (z_a - z_{a-1})), row 0 = 1, row n = 0 (backward guard)
-__global__ void decay_table_kernel(const double* __restrict__ zs, int64_t n, int mh, BVec b,
+// one thread per (row a, pair l), l fastest: coalesced 16-byte stores; MH a
+// template parameter, so the row index is a multiply-shift instead of the
+// 64-bit division of the round-1 form (a thread per row storing its 8 pairs
+// measured slower: 0.071 against 0.061 ms, strided stores)
+template <int MH>
+__global__ void decay_table_kernel(const double* __restrict__ zs, int64_t n, BVec b,
                                    double2* __restrict__ dtab, int64_t a_lo, int64_t a_hi) {
-  int64_t e = a_lo * mh + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= (a_hi + 1) * mh) return;
-  int64_t a = e / mh;
-  int l = (int)(e - a * mh);
+  const int64_t e = a_lo * MH + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (a_hi + 1) * MH) return;
+  const int64_t a = e / MH;
+  const int l = (int)(e - a * MH);
   double2 d;
   if (a == 0) {
     d = make_double2(1.0, 0.0);
   } else if (a == n) {
     d = make_double2(0.0, 0.0);
   } else {
-    double dz = zs[a] - zs[a - 1];
-    C2 v = cexp_neg(b.re[l] * dz, b.im[l] * dz);
+    const double dz = zs[a] - zs[a - 1];
+    const C2 v = cexp_neg(b.re[l] * dz, b.im[l] * dz);
     d = make_double2(v.re, v.im);
   }
   dtab[e] = d;
@@ -1532,8 +1537,15 @@ cudaError_t decay_table(const double* zs, int64_t n, int mh, const BVec& b, doub
   if (a_lo < 0) a_lo = 0;
   if (a_lo > a_hi) return cudaGetLastError();
   const int64_t tot = (a_hi - a_lo + 1) * mh;
-  decay_table_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(zs, n, mh, b, dtab, a_lo,
-                                                                     a_hi);
+  const unsigned grid = (unsigned)((tot + 255) / 256);
+  switch (mh) {
+#define DCASE(K) \
+  case K: decay_table_kernel<K><<<grid, 256, 0, st>>>(zs, n, b, dtab, a_lo, a_hi); break;
+    DCASE(1) DCASE(2) DCASE(3) DCASE(4) DCASE(5) DCASE(6) DCASE(7) DCASE(8) DCASE(9) DCASE(10)
+    DCASE(11) DCASE(12)
+#undef DCASE
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
