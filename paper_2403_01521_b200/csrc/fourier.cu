@@ -556,7 +556,10 @@ __global__ void __launch_bounds__(32 * SLAB_AGG_MMA_MAXW, SLAB_AGG_MINB) fourier
 // G is chosen per plan so that few-item plans (a multi-GPU rank's mode slice)
 // still expose thousands of warps.
 constexpr int kCarrySegs = 32;  // warps per CTA
-constexpr int kCarryBatch = 4;  // loads in flight per thread
+#ifndef SLAB_CARRY_BATCH
+#define SLAB_CARRY_BATCH 4
+#endif
+constexpr int kCarryBatch = SLAB_CARRY_BATCH;  // loads in flight per thread (2 / 8: slower at cfg4)
 
 __device__ __forceinline__ C2 carry_decay(bool isg, bool fwd, int c, int nch, int l, int mh,
                                           double k, const double2* __restrict__ Df,
