@@ -96,10 +96,16 @@ def maybe_relaunch(args) -> int | None:
     return subprocess.call(cmd, env=env)
 
 
+# test-only: SLAB_BENCH_BACKEND=gloo runs the N > 1 path with every rank on
+# cuda:0 and host-staged collectives (the whole multi-rank bench code path,
+# checkable on a one-GPU box; its timings are not scaling numbers)
+BACKEND = os.environ.get("SLAB_BENCH_BACKEND", "nccl")
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) if BACKEND == "nccl" else 0
     return rank, world, local
 
 
@@ -398,7 +404,10 @@ def run_ours(args, rank, world, local):
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(BACKEND)
         group = dist.group.WORLD
     import paper_2403_01521_b200 as pk
     from paper_2403_01521_b200 import _native
